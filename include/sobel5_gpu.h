@@ -1,0 +1,177 @@
+/*
+ * sobel5_gpu.h -- C ABI of the B200-native 4-direction 5x5 Sobel path.
+ *
+ * This is the drop-in boundary for the reference's streaming engine
+ * sobel5::run_stream (reference proj/include/sobel5/pipeline.hpp:452-477).
+ * Every entry point takes plain pointers and sizes; no C++ or torch types
+ * cross it, and nothing here throws.  The C++ API mirror
+ * (include/sobel5_b200/sobel5.hpp) rethrows the reference's exception types
+ * from the status codes; Python binds it with ctypes
+ * (paper_2305_00515_b200/_abi.py).  See INTEGRATION.md for the bindings a
+ * maintainer of the reference would add.
+ *
+ * Output contract (reference StreamResult, pipeline.hpp:284-291): four
+ * int32 gradient planes gx, gy, gd, gdt and the double magnitude g, each
+ * (W-4) x (H-4), valid-mode correlation.  Two optional extra planes are
+ * available: g32 (float magnitude, correctly rounded sqrt of the exact sum)
+ * and u8 (the clamp_abs edge map of image_io.hpp:235-240).  Any plane
+ * pointer may be NULL; only the non-NULL planes are written.
+ */
+#ifndef SOBEL5_GPU_H
+#define SOBEL5_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SOBEL5_GPU_ABI_VERSION 1
+
+/* Status codes.  Each maps to one reference exception type
+ * (reference errors.hpp:9-32); the C++ mirror throws that type. */
+typedef enum sobel5_status {
+    SOBEL5_OK = 0,
+    SOBEL5_IMAGE_TOO_SMALL = 1,     /* ImageTooSmall     pipeline.hpp:454-456   */
+    SOBEL5_DIM_MISMATCH = 2,        /* DimMismatch       pipeline.hpp:457-460   */
+    SOBEL5_PARITY_VIOLATION = 3,    /* ParityViolation   pipeline.hpp:268-273   */
+    SOBEL5_INVALID_ARG = 4,         /* null / misaligned pointer, bad pitch     */
+    SOBEL5_CUDA_ERROR = 5,          /* CUDA runtime error (message via ctx)     */
+    SOBEL5_OUT_OF_MEMORY = 6,       /* device or pinned allocation failed       */
+    SOBEL5_NON_POSITIVE_PARAM = 7,  /* NonPositiveParam  filter_algebra.hpp:158 */
+    SOBEL5_PARAM_OVERFLOW = 8,      /* ParamOverflow     filter_algebra.hpp:185 */
+    SOBEL5_LANE_TOO_NARROW = 9,     /* LaneTooNarrow     strips.hpp:40-42       */
+    SOBEL5_NO_DEVICE = 10           /* no CUDA device: the path never falls back */
+} sobel5_status;
+
+/* POD copy of sobel5::StreamTaps (pipeline.hpp:57-73).  The kernels honour
+ * arbitrary caller-supplied taps (e.g. the CLI's fault injection,
+ * sobel5_cli.cpp:219); wide_vagg is accepted and ignored because 32-bit
+ * wrapping arithmetic gives the int64 path's result after its int32 cast. */
+typedef struct sobel5_taps {
+    int32_t a;
+    int32_t f[5];     /* -1, -b, 0, b, 1                */
+    int32_t h[5];     /*  1,  n, m, n, 1                */
+    int32_t k0[5];    /* a * (-m, -(n+b), -2, -(n+b), -m) */
+    int32_t k1[5];    /* a * (b-n, -mb, -2nb, -mb, b-n) */
+    int32_t gx_v[5];  /* a * (1, n, m, n, 1) on F rows  */
+    int32_t gy_v[5];  /* a * (-1, -b, 0, b, 1) on H rows */
+    int32_t gdm_f[5]; /* a * (m, n+b, 2, n+b, m) on F rows */
+    int32_t gdm_d[5]; /* subtracted coefficients on D rows */
+    int32_t wide_vagg;
+} sobel5_taps;
+
+/* Output planes.  All planes share one row stride `pitch`, in ELEMENTS.
+ * Device entry points require: pitch >= width-4, pitch % 4 == 0, and every
+ * non-NULL plane 32-byte aligned.  sobel5_run_host takes tightly packed host
+ * planes (pitch == width-4, any alignment). */
+typedef struct sobel5_planes {
+    int32_t* gx;
+    int32_t* gy;
+    int32_t* gd;
+    int32_t* gdt;
+    double* g;
+    float* g32;
+    uint8_t* u8;
+    int64_t pitch;
+} sobel5_planes;
+
+/* Device-side diagnostics word set by the kernels (nullable).  Zero it
+ * before the launch; violations != 0 means some pixel had an odd P+M
+ * (recover_diag, pipeline.hpp:268-273) and (sum, diff) is one such pair. */
+typedef struct sobel5_diag {
+    int32_t violations;
+    int32_t sum;
+    int32_t diff;
+    int32_t reserved;
+} sobel5_diag;
+
+/* Reference-schedule tallies (sobel5::OpCounters, pipeline.hpp:26-51). */
+typedef struct sobel5_counters {
+    uint64_t row_conv5_f, row_conv5_h, row_conv5_k0, row_conv5_k1;
+    uint64_t row_diff, row_conv3_f, row_conv3_h, mac;
+} sobel5_counters;
+
+typedef struct sobel5_ctx sobel5_ctx; /* opaque: device, streams, buffers */
+
+/* ---- library ------------------------------------------------------------- */
+int sobel5_abi_version(void);
+const char* sobel5_status_string(int status);
+/* Number of kernel launches this process has issued through the library. */
+uint64_t sobel5_launch_count(void);
+
+/* ---- host-only helpers (no GPU needed) ------------------------------------ */
+
+/* make_stream_taps (pipeline.hpp:75-107) for integer (a, b, m, n), with the
+ * validate_params rules that apply to integers (filter_algebra.hpp:157-188):
+ * a >= 1 and b, m, n > 0 (NON_POSITIVE_PARAM), max |weight| <= 2^15
+ * (PARAM_OVERFLOW). Rational parameters are validated by the C++ mirror. */
+sobel5_status sobel5_make_taps(int64_t a, int64_t b, int64_t m, int64_t n, sobel5_taps* out);
+
+/* OpCounters the reference's run_stream reports for a plan whose strips have
+ * the given output widths (closed form of run_strip's tallies,
+ * pipeline.hpp:304-414). prefetch: 0 off, 1 on. */
+sobel5_status sobel5_plan_counters(int height, const int* strip_out_w, int n_strips,
+                                   const sobel5_taps* taps, int prefetch, sobel5_counters* out);
+
+/* ---- device entry points (caller-owned device memory, asynchronous) ------- */
+
+/* One image.  d_in: width x height uint8, row stride in_pitch bytes
+ * (in_pitch >= width rounded up to 4, in_pitch % 16 == 0, d_in 16-byte
+ * aligned).  prefetch selects the kernel variant (reference Prefetch,
+ * pipeline.hpp:21): 0 = direct loads, 1 = software-pipelined row prefetch.
+ * stream is a cudaStream_t (NULL = legacy default stream).  Returns after
+ * the launch is enqueued. */
+sobel5_status sobel5_launch(const uint8_t* d_in, int64_t in_pitch, int width, int height,
+                            const sobel5_taps* taps, int prefetch, const sobel5_planes* d_out,
+                            sobel5_diag* d_diag, void* stream);
+
+/* n_frames images of the same size in one launch: frame i starts at
+ * d_in + i*in_frame_stride bytes and its planes at element offset
+ * i*out_frame_stride (batched 1080p, config C4). */
+sobel5_status sobel5_launch_batch(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
+                                  int width, int height, int n_frames, const sobel5_taps* taps,
+                                  int prefetch, const sobel5_planes* d_out,
+                                  int64_t out_frame_stride, sobel5_diag* d_diag, void* stream);
+
+/* Row band of a row-partitioned image (config C5).  The band owns input
+ * rows [0, band_rows) of d_in; the two rows above it come from d_top (NULL at
+ * the image top) and the two below from d_bot (NULL at the image bottom).
+ * d_top / d_bot may point into a PEER GPU's buffer (CUDA IPC / P2P mapped),
+ * in which case the halo crosses NVLink inside the kernel, with no separate
+ * exchange.  The output rows written are the valid centre rows of the
+ * stacked image [top; band; bot], i.e. (rows_total - 4) rows starting at the
+ * first centre row. */
+sobel5_status sobel5_launch_band(const uint8_t* d_top, const uint8_t* d_in, const uint8_t* d_bot,
+                                 int64_t in_pitch, int width, int band_rows,
+                                 const sobel5_taps* taps, int prefetch,
+                                 const sobel5_planes* d_out, sobel5_diag* d_diag, void* stream);
+
+/* synth_random (synth.hpp:20-35) generated on the device, optionally masked
+ * (SURVEY.md section 8d inputs).  Pixel i of row-major order is byte i%8 of
+ * splitmix64 word i/8; row_offset lets a band generate its slice. */
+sobel5_status sobel5_synth_random_device(uint8_t* d_img, int64_t pitch, int width, int height,
+                                         int64_t row_offset, uint64_t seed, uint8_t mask,
+                                         void* stream);
+
+/* ---- context: host-buffer path (what the C++ run_stream wrapper calls) ---- */
+
+sobel5_status sobel5_ctx_create(sobel5_ctx** out, int device);
+void sobel5_ctx_destroy(sobel5_ctx* ctx);
+/* Message of the last CUDA error seen by this context ("" if none). */
+const char* sobel5_ctx_last_error(const sobel5_ctx* ctx);
+
+/* Synchronous end-to-end call: host image in (tightly packed W x H), host
+ * planes out (tightly packed, pitch == width-4; NULL planes skipped).
+ * Copies are chunked by row bands over pinned staging and overlapped with
+ * the kernels on the context's streams.  On SOBEL5_PARITY_VIOLATION the
+ * offending pair is returned in *diag_out (nullable). */
+sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
+                              const sobel5_taps* taps, int prefetch, const sobel5_planes* h_out,
+                              sobel5_diag* diag_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOBEL5_GPU_H */

@@ -1,0 +1,270 @@
+"""ctypes bindings for the CPU oracle and the compiled reference.
+
+TEST INFRASTRUCTURE: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / ``--impl reference`` leg import this module, and only as the
+checker or the CPU timing arm.  The product (paper_2305_00515_b200) never
+imports it.
+
+* ``Oracle``  -> oracle/_build/libsobel5_oracle.so, the plain-C restatement
+  (oracle/sobel5_oracle.c, every function citing the reference file:line).
+* ``Reference`` -> oracle/_ref/libsobel5_ref.so, the reference's own headers
+  compiled unmodified (oracle/Makefile, oracle/ref_shim.cpp).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "_build", "libsobel5_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libsobel5_ref.so")
+
+TAP_FIELDS = ("f", "h", "k0", "k1", "gx_v", "gy_v", "gdm_f", "gdm_d")
+
+
+class Taps(C.Structure):
+    """POD mirror of sobel5::StreamTaps (pipeline.hpp:57-73)."""
+
+    _fields_ = [("a", C.c_int32)] + [(n, C.c_int32 * 5) for n in TAP_FIELDS] + [
+        ("wide_vagg", C.c_int32)
+    ]
+
+    def as_dict(self):
+        d = {"a": self.a, "wide_vagg": self.wide_vagg}
+        for n in TAP_FIELDS:
+            d[n] = list(getattr(self, n))
+        return d
+
+    @classmethod
+    def from_dict(cls, d):
+        t = cls()
+        t.a = d["a"]
+        t.wide_vagg = int(d.get("wide_vagg", 0))
+        for n in TAP_FIELDS:
+            getattr(t, n)[:] = list(d[n])
+        return t
+
+    def copy(self):
+        return Taps.from_dict(self.as_dict())
+
+
+class Counters(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "row_conv5_f", "row_conv5_h", "row_conv5_k0", "row_conv5_k1",
+        "row_diff", "row_conv3_f", "row_conv3_h", "mac")]
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def build():
+    """Compile the oracle (and the reference shim where /root/reference exists)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _out_planes(w, h, want=True):
+    ow, oh = w - 4, h - 4
+    if not want:
+        return None
+    return {k: np.empty((oh, ow), np.int32) for k in ("gx", "gy", "gd", "gdt")} | {
+        "g": np.empty((oh, ow), np.float64)}
+
+
+class Oracle:
+    def __init__(self, path: str = ORACLE_SO):
+        if not os.path.exists(path):
+            build()
+        L = self.lib = C.CDLL(path)
+        L.oracle_make_stream_taps.argtypes = [C.c_int64] * 4 + [C.POINTER(Taps)]
+        L.oracle_materialize.argtypes = [C.c_int64] * 4 + [C.c_int, C.c_void_p]
+        L.oracle_run_stream.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(Taps)] + [
+            C.c_void_p] * 7
+        L.oracle_run_stream.restype = C.c_int
+        L.oracle_sobel5_4d.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_int64] * 4 + [
+            C.c_void_p] * 5
+        L.oracle_sobel5_4d.restype = C.c_int
+        L.oracle_clamp_abs_f64.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p]
+        L.oracle_synth_random.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64]
+        L.oracle_stream_counters.argtypes = [C.c_int, C.c_void_p, C.c_int, C.POINTER(Taps),
+                                             C.c_int, C.POINTER(Counters)]
+        L.oracle_fnv1a64.argtypes = [C.c_void_p, C.c_size_t]
+        L.oracle_fnv1a64.restype = C.c_uint64
+
+    def make_stream_taps(self, a=1, b=2, m=6, n=4) -> Taps:
+        t = Taps()
+        self.lib.oracle_make_stream_taps(a, b, m, n, C.byref(t))
+        return t
+
+    def materialize(self, a, b, m, n, direction: int) -> np.ndarray:
+        k = np.empty((5, 5), np.int32)
+        self.lib.oracle_materialize(a, b, m, n, direction, _p(k))
+        return k
+
+    def run_stream(self, img: np.ndarray, taps: Taps | None = None):
+        """Returns (status, planes dict, (bad_sum, bad_diff))."""
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        taps = taps or self.make_stream_taps()
+        if w < 5 or h < 5:
+            return 1, None, None
+        o = _out_planes(w, h)
+        bs, bd = np.zeros(1, np.int32), np.zeros(1, np.int32)
+        st = self.lib.oracle_run_stream(_p(img), w, h, C.byref(taps), _p(o["gx"]), _p(o["gy"]),
+                                        _p(o["gd"]), _p(o["gdt"]), _p(o["g"]), _p(bs), _p(bd))
+        return st, o, (int(bs[0]), int(bd[0]))
+
+    def sobel5_4d(self, img: np.ndarray, a=1, b=2, m=6, n=4):
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        o = _out_planes(w, h)
+        st = self.lib.oracle_sobel5_4d(_p(img), w, h, a, b, m, n, _p(o["gx"]), _p(o["gy"]),
+                                       _p(o["gd"]), _p(o["gdt"]), _p(o["g"]))
+        if st:
+            raise RuntimeError(f"oracle_sobel5_4d status {st}")
+        return o
+
+    def clamp_abs(self, g: np.ndarray) -> np.ndarray:
+        g = np.ascontiguousarray(g, np.float64)
+        out = np.empty(g.shape, np.uint8)
+        self.lib.oracle_clamp_abs_f64(_p(g), g.size, _p(out))
+        return out
+
+    def synth_random(self, w, h, seed=1) -> np.ndarray:
+        img = np.empty((h, w), np.uint8)
+        self.lib.oracle_synth_random(_p(img), w, h, seed)
+        return img
+
+    def stream_counters(self, h, strip_widths, taps: Taps | None = None, prefetch=True):
+        taps = taps or self.make_stream_taps()
+        sw = np.ascontiguousarray(strip_widths, np.int32)
+        c = Counters()
+        self.lib.oracle_stream_counters(h, _p(sw), len(sw), C.byref(taps), int(prefetch),
+                                        C.byref(c))
+        return {n: getattr(c, n) for n, _ in Counters._fields_}
+
+    def fnv1a64(self, a: np.ndarray) -> int:
+        a = np.ascontiguousarray(a)
+        return int(self.lib.oracle_fnv1a64(_p(a), a.nbytes))
+
+
+class Reference:
+    """The reference's own headers, compiled (oracle/_ref/libsobel5_ref.so)."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        L = self.lib = C.CDLL(path)
+        E = [C.c_char_p, C.c_int]
+        L.ref_make_stream_taps.argtypes = [C.c_int64] * 7 + [C.POINTER(Taps)] + E
+        L.ref_materialize.argtypes = [C.c_int64] * 4 + [C.c_int, C.c_void_p] + E
+        L.ref_run_stream.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(Taps), C.c_int,
+                                     C.c_int, C.c_int] + [C.c_void_p] * 6 + E
+        L.ref_sobel5_4d.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_int64] * 4 + [
+            C.c_void_p] * 5 + E
+        L.ref_diag_via_sum_diff.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                            C.c_void_p] + E
+        L.ref_synth_random.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64]
+        L.ref_plan_strips.argtypes = [C.c_int] * 4 + [C.c_void_p] * 4 + E
+        L.ref_hpass.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_int64] * 4 + [
+            C.c_void_p] + E
+        L.ref_recover_diag.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p] + E
+        L.ref_measure_run_stream.argtypes = [C.c_void_p] + [C.c_int] * 6 + [C.c_void_p]
+        L.ref_measure_run_stream.restype = C.c_double
+        L.ref_measure_oracle.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
+        L.ref_measure_oracle.restype = C.c_double
+
+    @staticmethod
+    def _err():
+        return C.create_string_buffer(512)
+
+    def make_stream_taps(self, a=1, b=(2, 1), m=(6, 1), n=(4, 1)):
+        """Returns (code, Taps | None, message). Rationals as (num, den)."""
+        b, m, n = [(x, 1) if isinstance(x, int) else x for x in (b, m, n)]
+        t, e = Taps(), self._err()
+        code = self.lib.ref_make_stream_taps(a, b[0], b[1], m[0], m[1], n[0], n[1], C.byref(t),
+                                             e, 512)
+        return code, (t if code == 0 else None), e.value.decode()
+
+    def materialize(self, a, b, m, n, direction):
+        k, e = np.empty((5, 5), np.int32), self._err()
+        code = self.lib.ref_materialize(a, b, m, n, direction, _p(k), e, 512)
+        return code, k, e.value.decode()
+
+    def run_stream(self, img, taps: Taps | None = None, lanes=32, prefetch=True, workers=1):
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        if taps is None:
+            taps = self.make_stream_taps()[1]
+        o = _out_planes(max(w, 5), max(h, 5))
+        cnt = np.zeros(8, np.uint64)
+        e = self._err()
+        code = self.lib.ref_run_stream(_p(img), w, h, C.byref(taps), lanes, int(prefetch),
+                                       workers, _p(o["gx"]), _p(o["gy"]), _p(o["gd"]),
+                                       _p(o["gdt"]), _p(o["g"]), _p(cnt), e, 512)
+        names = [n for n, _ in Counters._fields_]
+        return code, o, dict(zip(names, (int(x) for x in cnt))), e.value.decode()
+
+    def sobel5_4d(self, img, a=1, b=2, m=6, n=4):
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        o = _out_planes(w, h)
+        e = self._err()
+        code = self.lib.ref_sobel5_4d(_p(img), w, h, a, b, m, n, _p(o["gx"]), _p(o["gy"]),
+                                      _p(o["gd"]), _p(o["gdt"]), _p(o["g"]), e, 512)
+        if code:
+            raise RuntimeError(e.value.decode())
+        return o
+
+    def diag_via_sum_diff(self, img):
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        gd, gdt = np.empty((h - 4, w - 4), np.int32), np.empty((h - 4, w - 4), np.int32)
+        e = self._err()
+        code = self.lib.ref_diag_via_sum_diff(_p(img), w, h, _p(gd), _p(gdt), e, 512)
+        return code, gd, gdt
+
+    def synth_random(self, w, h, seed=1):
+        img = np.empty((h, w), np.uint8)
+        self.lib.ref_synth_random(_p(img), w, h, seed)
+        return img
+
+    def plan_strips(self, width, lanes, radius=2):
+        cap = max(1, width + 1)
+        bufs = [np.zeros(cap, np.int32) for _ in range(3)]
+        n = C.c_int(0)
+        e = self._err()
+        code = self.lib.ref_plan_strips(width, lanes, radius, cap, C.byref(n), *map(_p, bufs), e,
+                                        512)
+        if code:
+            return code, None, e.value.decode()
+        k = n.value
+        return 0, [(int(bufs[0][i]), int(bufs[1][i]), int(bufs[2][i])) for i in range(k)], ""
+
+    def hpass(self, row, which, a=1, b=2, m=6, n=4):
+        row = np.ascontiguousarray(row, np.uint8)
+        out = np.zeros(max(1, row.size - 4), np.int32)
+        e = self._err()
+        code = self.lib.ref_hpass(_p(row), row.size, which, a, b, m, n, _p(out), e, 512)
+        return code, out[: max(0, row.size - 4)], e.value.decode()
+
+    def recover_diag(self, s, d):
+        gd, gdt = np.zeros(1, np.int32), np.zeros(1, np.int32)
+        e = self._err()
+        code = self.lib.ref_recover_diag(s, d, _p(gd), _p(gdt), e, 512)
+        return code, (int(gd[0]), int(gdt[0])), e.value.decode()
+
+    def measure_run_stream(self, img, lanes=256, prefetch=True, workers=1, iters=1):
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        sd = np.zeros(1, np.float64)
+        mean = self.lib.ref_measure_run_stream(_p(img), w, h, lanes, int(prefetch), workers,
+                                               iters, _p(sd))
+        return mean, float(sd[0])
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)

@@ -1,0 +1,126 @@
+"""ctypes binding of include/sobel5_gpu.h (the product's C ABI).
+
+Loading fails loudly if the in-tree extension is missing: there is no CPU
+fallback anywhere on the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import build as _build
+
+TAP_FIELDS = ("f", "h", "k0", "k1", "gx_v", "gy_v", "gdm_f", "gdm_d")
+
+
+class Taps(C.Structure):
+    """sobel5_taps == POD sobel5::StreamTaps (pipeline.hpp:57-73)."""
+
+    _fields_ = [("a", C.c_int32)] + [(n, C.c_int32 * 5) for n in TAP_FIELDS] + [
+        ("wide_vagg", C.c_int32)]
+
+    def as_dict(self) -> dict:
+        d = {"a": int(self.a), "wide_vagg": int(self.wide_vagg)}
+        for n in TAP_FIELDS:
+            d[n] = [int(v) for v in getattr(self, n)]
+        return d
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "Taps":
+        t = cls()
+        t.a = int(d["a"])
+        t.wide_vagg = int(d.get("wide_vagg", 0))
+        for n in TAP_FIELDS:
+            getattr(t, n)[:] = [int(v) for v in d[n]]
+        return t
+
+    def copy(self) -> "Taps":
+        return Taps.from_dict(self.as_dict())
+
+    def __eq__(self, other):
+        return isinstance(other, Taps) and self.as_dict() == other.as_dict()
+
+
+class Planes(C.Structure):
+    _fields_ = [("gx", C.c_void_p), ("gy", C.c_void_p), ("gd", C.c_void_p), ("gdt", C.c_void_p),
+                ("g", C.c_void_p), ("g32", C.c_void_p), ("u8", C.c_void_p),
+                ("pitch", C.c_int64)]
+
+
+class Diag(C.Structure):
+    _fields_ = [("violations", C.c_int32), ("sum", C.c_int32), ("diff", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class Counters(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "row_conv5_f", "row_conv5_h", "row_conv5_k0", "row_conv5_k1",
+        "row_diff", "row_conv3_f", "row_conv3_h", "mac")]
+
+
+PLANE_NAMES = ("gx", "gy", "gd", "gdt", "g", "g32", "u8")
+
+# sobel5_status
+OK, IMAGE_TOO_SMALL, DIM_MISMATCH, PARITY_VIOLATION, INVALID_ARG, CUDA_ERROR, \
+    OUT_OF_MEMORY, NON_POSITIVE_PARAM, PARAM_OVERFLOW, LANE_TOO_NARROW, NO_DEVICE = range(11)
+
+EXPORTS = (
+    "sobel5_abi_version", "sobel5_status_string", "sobel5_launch_count", "sobel5_make_taps",
+    "sobel5_plan_counters", "sobel5_launch", "sobel5_launch_batch", "sobel5_launch_band",
+    "sobel5_synth_random_device", "sobel5_ctx_create", "sobel5_ctx_destroy",
+    "sobel5_ctx_last_error", "sobel5_run_host",
+)
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True) -> C.CDLL:
+    """Load libsobel5_b200.so (building it in-tree first if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = lib_path()
+    if not os.path.exists(path):
+        if not build_if_missing:
+            raise RuntimeError(f"sobel5 CUDA extension missing: {path}")
+        _build.build()
+    L = C.CDLL(path)
+    vp, i32, i64 = C.c_void_p, C.c_int, C.c_int64
+    L.sobel5_abi_version.restype = i32
+    L.sobel5_status_string.argtypes = [i32]
+    L.sobel5_status_string.restype = C.c_char_p
+    L.sobel5_launch_count.restype = C.c_uint64
+    L.sobel5_make_taps.argtypes = [i64] * 4 + [C.POINTER(Taps)]
+    L.sobel5_make_taps.restype = i32
+    L.sobel5_plan_counters.argtypes = [i32, vp, i32, C.POINTER(Taps), i32, C.POINTER(Counters)]
+    L.sobel5_plan_counters.restype = i32
+    L.sobel5_launch.argtypes = [vp, i64, i32, i32, C.POINTER(Taps), i32, C.POINTER(Planes), vp,
+                                vp]
+    L.sobel5_launch.restype = i32
+    L.sobel5_launch_batch.argtypes = [vp, i64, i64, i32, i32, i32, C.POINTER(Taps), i32,
+                                      C.POINTER(Planes), i64, vp, vp]
+    L.sobel5_launch_batch.restype = i32
+    L.sobel5_launch_band.argtypes = [vp, vp, vp, i64, i32, i32, C.POINTER(Taps), i32,
+                                     C.POINTER(Planes), vp, vp]
+    L.sobel5_launch_band.restype = i32
+    L.sobel5_synth_random_device.argtypes = [vp, i64, i32, i32, i64, C.c_uint64, C.c_uint8, vp]
+    L.sobel5_synth_random_device.restype = i32
+    L.sobel5_ctx_create.argtypes = [C.POINTER(vp), i32]
+    L.sobel5_ctx_create.restype = i32
+    L.sobel5_ctx_destroy.argtypes = [vp]
+    L.sobel5_ctx_destroy.restype = None
+    L.sobel5_ctx_last_error.argtypes = [vp]
+    L.sobel5_ctx_last_error.restype = C.c_char_p
+    L.sobel5_run_host.argtypes = [vp, vp, i32, i32, C.POINTER(Taps), i32, C.POINTER(Planes),
+                                  C.POINTER(Diag)]
+    L.sobel5_run_host.restype = i32
+    _lib = L
+    return L
+
+
+def status_string(code: int) -> str:
+    return load().sobel5_status_string(code).decode()

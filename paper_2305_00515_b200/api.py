@@ -1,0 +1,383 @@
+"""Python mirror of the reference's run_stream interface over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference headers
+(proj/include/sobel5/): ``FilterParams``/``validate_params``/``materialize``
+(filter_algebra.hpp:58-199), ``make_stream_taps`` (pipeline.hpp:75-107),
+``plan_strips`` (strips.hpp:35-61), ``Prefetch`` (pipeline.hpp:21),
+``StreamResult`` (pipeline.hpp:284-291) and ``run_stream``
+(pipeline.hpp:452-477).  The compute always runs on the GPU through
+libsobel5_b200.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+import numpy as np
+
+from . import _abi
+from ._abi import Counters, Diag, Planes, Taps
+
+# ---- errors (reference errors.hpp:9-32) -------------------------------------
+
+
+class Error(RuntimeError):
+    pass
+
+
+class NonPositiveParam(Error): pass
+class NonIntegralWeight(Error): pass
+class ParamOverflow(Error): pass
+class ImageTooSmall(Error): pass
+class RowTooShort(Error): pass
+class MissingRow(Error): pass
+class VariantMismatch(Error): pass
+class ParityViolation(Error): pass
+class LaneTooNarrow(Error): pass
+class DimMismatch(Error): pass
+class EmptyPlane(Error): pass
+class CudaError(Error): pass
+
+
+_STATUS_EXC = {
+    _abi.IMAGE_TOO_SMALL: ImageTooSmall,
+    _abi.DIM_MISMATCH: DimMismatch,
+    _abi.PARITY_VIOLATION: ParityViolation,
+    _abi.NON_POSITIVE_PARAM: NonPositiveParam,
+    _abi.PARAM_OVERFLOW: ParamOverflow,
+    _abi.LANE_TOO_NARROW: LaneTooNarrow,
+}
+
+
+def check(status: int, what: str = "") -> None:
+    if status == _abi.OK:
+        return
+    exc = _STATUS_EXC.get(status, CudaError)
+    msg = _abi.status_string(status)
+    raise exc(f"{what}: {msg}" if what else msg)
+
+
+# ---- filter algebra (filter_algebra.hpp) ------------------------------------
+
+K_MAX_WEIGHT_MAGNITUDE = 1 << 15  # filter_algebra.hpp:148
+DIRECTIONS = ("Kx", "Ky", "Kd", "Kdt")  # direction_name, filter_algebra.hpp:67-75
+
+
+def _rat_str(r: Fraction) -> str:
+    return str(r.numerator) if r.denominator == 1 else f"{r.numerator}/{r.denominator}"
+
+
+@dataclass(frozen=True)
+class FilterParams:
+    """(a, b, m, n) of Eq. 5; defaults reproduce Eq. 3 (filter_algebra.hpp:58-63)."""
+
+    a: int = 1
+    b: Fraction | int = 2
+    m: Fraction | int = 6
+    n: Fraction | int = 4
+
+
+def _materialize_exact(p: FilterParams, direction: int):
+    """filter_algebra.hpp:82-134 (exact rationals)."""
+    a, b, m, n = Fraction(p.a), Fraction(p.b), Fraction(p.m), Fraction(p.n)
+    one, zero = Fraction(1), Fraction(0)
+    if direction == 0:
+        col, row = (one, n, m, n, one), (-one, -b, zero, b, one)
+        return [[a * col[i] * row[j] for j in range(5)] for i in range(5)]
+    if direction == 1:
+        col, row = (-one, -b, zero, b, one), (one, n, m, n, one)
+        return [[a * col[i] * row[j] for j in range(5)] for i in range(5)]
+    nb, mb = n * b, m * b
+    if direction == 2:
+        k = [[-m, -n, -one, -b, zero], [-n, -mb, -nb, zero, b], [-one, -nb, zero, nb, one],
+             [-b, zero, nb, mb, n], [zero, b, one, n, m]]
+    else:
+        k = [[zero, -b, -one, -n, -m], [b, zero, -nb, -mb, -n], [one, nb, zero, -nb, -one],
+             [n, mb, nb, zero, -b], [m, n, one, b, zero]]
+    return [[a * e for e in row] for row in k]
+
+
+def validate_params(p: FilterParams) -> None:
+    """filter_algebra.hpp:157-188, same checks, order and messages."""
+    if p.a < 1:
+        raise NonPositiveParam(f"a = {p.a} must be a positive integer")
+    for name in ("b", "m", "n"):
+        v = Fraction(getattr(p, name))
+        if v <= 0:
+            raise NonPositiveParam(f"{name} = {_rat_str(v)} must be positive")
+    max_mag = 0
+    for d in range(4):
+        k = _materialize_exact(p, d)
+        for i in range(5):
+            for j in range(5):
+                if k[i][j].denominator != 1:
+                    raise NonIntegralWeight(
+                        f"{DIRECTIONS[d]}({i},{j}) = {_rat_str(k[i][j])} is not an integer")
+                max_mag = max(max_mag, abs(k[i][j].numerator))
+    for name in ("b", "m", "n"):
+        v = Fraction(getattr(p, name))
+        if v.denominator != 1:
+            raise NonIntegralWeight(f"parameter {name} = {_rat_str(v)} must be an integer "
+                                    "(streaming taps are integer vectors)")
+    if max_mag > K_MAX_WEIGHT_MAGNITUDE:
+        raise ParamOverflow(f"largest weight magnitude {max_mag} exceeds "
+                            f"{K_MAX_WEIGHT_MAGNITUDE}")
+
+
+def materialize(p: FilterParams, direction: int) -> np.ndarray:
+    """filter_algebra.hpp:192-199 (params must already be valid)."""
+    k = _materialize_exact(p, direction)
+    return np.array([[int(e) for e in row] for row in k], dtype=np.int32)
+
+
+def make_stream_taps(p: FilterParams = FilterParams()) -> Taps:
+    """pipeline.hpp:75-107 (validation, then the C ABI builds the taps)."""
+    validate_params(p)
+    t = Taps()
+    check(_abi.load().sobel5_make_taps(int(p.a), int(Fraction(p.b)), int(Fraction(p.m)),
+                                       int(Fraction(p.n)), C.byref(t)), "make_stream_taps")
+    return t
+
+
+# ---- strips (strips.hpp) ------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class Strip:
+    in_off: int = 0
+    out_off: int = 0
+    out_w: int = 0
+
+
+@dataclass
+class StripPlan:
+    in_width: int = 0
+    out_width: int = 0
+    lane_width: int = 0
+    radius: int = 0
+    strips: list = field(default_factory=list)
+
+
+def plan_strips(width: int, lane_width: int, radius: int) -> StripPlan:
+    """strips.hpp:35-61, same errors and messages."""
+    if radius <= 0:
+        raise DimMismatch(f"strip radius must be positive, got {radius}")
+    if lane_width <= 2 * radius:
+        raise LaneTooNarrow(f"lane width {lane_width} leaves no output columns at radius "
+                            f"{radius}")
+    if width < 2 * radius + 1:
+        raise ImageTooSmall(f"width {width} is below the minimum {2 * radius + 1} for radius "
+                            f"{radius}")
+    plan = StripPlan(width, width - 2 * radius, lane_width, radius, [])
+    step = lane_width - 2 * radius
+    for off in range(0, plan.out_width, step):
+        plan.strips.append(Strip(off, off, min(step, plan.out_width - off)))
+    return plan
+
+
+# ---- run_stream -----------------------------------------------------------------
+
+
+class Prefetch(enum.IntEnum):
+    off = 0
+    on = 1
+
+
+@dataclass
+class StreamResult:
+    gx: np.ndarray
+    gy: np.ndarray
+    gd: np.ndarray
+    gdt: np.ndarray
+    g: np.ndarray
+    counters: dict
+    u8: np.ndarray | None = None
+
+
+def plan_counters(height: int, plan: StripPlan, taps: Taps, prefetch: Prefetch) -> dict:
+    """Reference-schedule OpCounters (pipeline.hpp:26-51, closed form)."""
+    widths = np.array([s.out_w for s in plan.strips], dtype=np.int32)
+    c = Counters()
+    check(_abi.load().sobel5_plan_counters(height, widths.ctypes.data_as(C.c_void_p),
+                                           len(widths), C.byref(taps), int(prefetch),
+                                           C.byref(c)), "plan_counters")
+    return {n: int(getattr(c, n)) for n, _ in Counters._fields_}
+
+
+class Context:
+    """Per-thread, per-device context (streams + cached device buffers)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = _abi.load()
+        h = C.c_void_p()
+        check(self._lib.sobel5_ctx_create(C.byref(h), device), "sobel5_ctx_create")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.sobel5_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def last_error(self) -> str:
+        return self._lib.sobel5_ctx_last_error(self._h).decode()
+
+    def run_host(self, img: np.ndarray, taps: Taps, prefetch: Prefetch = Prefetch.on,
+                 planes=("gx", "gy", "gd", "gdt", "g"), out: dict | None = None):
+        """Host arrays in / out.  Returns (status, dict of planes, Diag)."""
+        img = np.ascontiguousarray(img, dtype=np.uint8)
+        h, w = img.shape
+        ow, oh = max(w - 4, 0), max(h - 4, 0)
+        dt = {"gx": np.int32, "gy": np.int32, "gd": np.int32, "gdt": np.int32, "g": np.float64,
+              "g32": np.float32, "u8": np.uint8}
+        res = out if out is not None else {
+            k: np.empty((oh, ow), dt[k]) for k in planes} if (ow > 0 and oh > 0) else {}
+        pl = Planes(pitch=ow)
+        for k, v in res.items():
+            setattr(pl, k, v.ctypes.data)
+        d = Diag()
+        st = self._lib.sobel5_run_host(self._h, img.ctypes.data, w, h, C.byref(taps),
+                                       int(prefetch), C.byref(pl), C.byref(d))
+        return st, res, d
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def run_stream(img: np.ndarray, taps_or_params, plan: StripPlan, prefetch: Prefetch,
+               workers: int = 1, ctx: Context | None = None) -> StreamResult:
+    """Drop-in for sobel5::run_stream (pipeline.hpp:452-477).
+
+    ``workers`` is accepted and ignored (the GPU grid replaces the thread
+    pool); ``plan`` is validated like the reference and drives the
+    reference-schedule counters, while the GPU tiling is independent of it
+    (SPEC.md: correctness is independent of the plan).
+    """
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    if img.ndim != 2:
+        raise DimMismatch("image must be 2-D")
+    h, w = img.shape
+    if w < 5 or h < 5:  # pipeline.hpp:454-456
+        raise ImageTooSmall(f"streaming filter needs at least 5x5, got {w}x{h}")
+    if plan.in_width != w or plan.radius != 2:  # pipeline.hpp:457-460
+        raise DimMismatch(f"strip plan covers {plan.in_width} columns at radius {plan.radius}, "
+                          f"image has {w}")
+    taps = taps_or_params if isinstance(taps_or_params, Taps) else make_stream_taps(
+        taps_or_params)
+    ctx = ctx or default_context()
+    st, res, d = ctx.run_host(img, taps, prefetch)
+    if st == _abi.PARITY_VIOLATION:  # pipeline.hpp:269-271
+        raise ParityViolation(f"odd sum/difference pair ({d.sum}, {d.diff})")
+    if st != _abi.OK:
+        check(st, f"run_stream ({ctx.last_error()})")
+    return StreamResult(res["gx"], res["gy"], res["gd"], res["gdt"], res["g"],
+                        plan_counters(h, plan, taps, prefetch))
+
+
+# ---- device-resident helpers (torch tensors as device memory) --------------------
+
+
+def round_up(v: int, m: int) -> int:
+    return (v + m - 1) // m * m
+
+
+def alloc_input(width: int, height: int, device="cuda", frames: int = 1):
+    """Pitched uint8 device image(s): returns (tensor, pitch_bytes)."""
+    import torch
+    pitch = round_up(width, 128)
+    t = torch.empty((frames, height, pitch) if frames > 1 else (height, pitch),
+                    dtype=torch.uint8, device=device)
+    return t, pitch
+
+
+def alloc_planes(out_w: int, out_h: int, which=("gx", "gy", "gd", "gdt", "g"), device="cuda",
+                 frames: int = 1):
+    """Pitched device planes sharing one element pitch: (dict, pitch_elems)."""
+    import torch
+    pitch = round_up(out_w, 32)
+    dt = {"gx": torch.int32, "gy": torch.int32, "gd": torch.int32, "gdt": torch.int32,
+          "g": torch.float64, "g32": torch.float32, "u8": torch.uint8}
+    shape = (frames, out_h, pitch) if frames > 1 else (out_h, pitch)
+    return {k: torch.empty(shape, dtype=dt[k], device=device) for k in which}, pitch
+
+
+def planes_struct(planes: dict, pitch: int) -> Planes:
+    pl = Planes(pitch=pitch)
+    for k, v in planes.items():
+        setattr(pl, k, v.data_ptr())
+    return pl
+
+
+def launch(d_in, in_pitch: int, width: int, height: int, taps: Taps, prefetch: int,
+           planes: dict, pitch: int, diag=None, stream=None) -> None:
+    """Enqueue one device-resident image (sobel5_launch)."""
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    pl = planes_struct(planes, pitch)
+    check(_abi.load().sobel5_launch(d_in.data_ptr(), in_pitch, width, height, C.byref(taps),
+                                    int(prefetch), C.byref(pl),
+                                    None if diag is None else diag.data_ptr(), s),
+          "sobel5_launch")
+
+
+def launch_batch(d_in, in_pitch: int, in_frame_stride: int, width: int, height: int,
+                 n_frames: int, taps: Taps, prefetch: int, planes: dict, pitch: int,
+                 out_frame_stride: int, diag=None, stream=None) -> None:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    pl = planes_struct(planes, pitch)
+    check(_abi.load().sobel5_launch_batch(d_in.data_ptr(), in_pitch, in_frame_stride, width,
+                                          height, n_frames, C.byref(taps), int(prefetch),
+                                          C.byref(pl), out_frame_stride,
+                                          None if diag is None else diag.data_ptr(), s),
+          "sobel5_launch_batch")
+
+
+def launch_band(d_top, d_in, d_bot, in_pitch: int, width: int, band_rows: int, taps: Taps,
+                prefetch: int, planes: dict, pitch: int, diag=None, stream=None) -> None:
+    """Row band with optional 2-row halos (pointers may be peer-mapped)."""
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    pl = planes_struct(planes, pitch)
+
+    def ptr(x):
+        if x is None:
+            return None
+        return x if isinstance(x, int) else x.data_ptr()
+
+    check(_abi.load().sobel5_launch_band(ptr(d_top), ptr(d_in), ptr(d_bot), in_pitch, width,
+                                         band_rows, C.byref(taps), int(prefetch), C.byref(pl),
+                                         None if diag is None else diag.data_ptr(), s),
+          "sobel5_launch_band")
+
+
+def synth_random_device(d_img, pitch: int, width: int, height: int, seed: int = 1,
+                        mask: int = 0xFF, row_offset: int = 0, stream=None) -> None:
+    """synth_random (synth.hpp:20-35) generated on the GPU."""
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    check(_abi.load().sobel5_synth_random_device(d_img.data_ptr(), pitch, width, height,
+                                                 row_offset, seed, mask, s),
+          "sobel5_synth_random_device")
+
+
+def launch_count() -> int:
+    return int(_abi.load().sobel5_launch_count())

@@ -1,0 +1,350 @@
+// sobel5_abi.cu -- the extern "C" boundary (include/sobel5_gpu.h): argument
+// validation in the reference's order, kernel selection, device launch
+// entry points, and the host-buffer path with chunked copy/compute overlap.
+//
+// Reference interface replaced: sobel5::run_stream (pipeline.hpp:452-477).
+// No CPU fallback exists: without a device every compute entry point returns
+// SOBEL5_NO_DEVICE / SOBEL5_CUDA_ERROR.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sobel5_gpu.h"
+#include "sobel5_stream.cuh"
+
+using namespace sobel5_b200;
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+constexpr int64_t kMaxWeight = int64_t{1} << 15;  // filter_algebra.hpp:148
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// ---- taps analysis ---------------------------------------------------------
+
+bool taps_are_default(const sobel5_taps& t) {
+    const DefaultTaps d;
+    (void)d;
+    for (int i = 0; i < 5; ++i) {
+        if (t.f[i] != DefaultTaps::f[i] || t.h[i] != DefaultTaps::h[i] ||
+            t.k0[i] != DefaultTaps::k0[i] || t.k1[i] != DefaultTaps::k1[i] ||
+            t.gx_v[i] != DefaultTaps::gx_v[i] || t.gy_v[i] != DefaultTaps::gy_v[i] ||
+            t.gdm_f[i] != DefaultTaps::gdm_f[i] || t.gdm_d[i] != DefaultTaps::gdm_d[i])
+            return false;
+    }
+    return true;
+}
+
+// 255 * max(sum of positive weights, sum of |negative weights|): the largest
+// |response| of a 5x5 integer kernel over uint8 input.
+int64_t response_bound(const int64_t k[25]) {
+    int64_t pos = 0, neg = 0;
+    for (int i = 0; i < 25; ++i) (k[i] > 0 ? pos : neg) += k[i] > 0 ? k[i] : -k[i];
+    return 255 * std::max(pos, neg);
+}
+
+// The effective 5x5 kernels of the streaming schedule for arbitrary taps,
+// and from them whether the exact integer sum of squares fits uint32 (then
+// double(S) and the reference's double sum are the same number).
+MagMode choose_mag(const sobel5_taps& t) {
+    int64_t kx[25], ky[25], kp[25], km[25];
+    const int64_t dd[5] = {0, -1, 0, 1, 0};
+    for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < 5; ++j) {
+            kx[i * 5 + j] = int64_t{t.gx_v[i]} * t.f[j];
+            ky[i * 5 + j] = int64_t{t.gy_v[i]} * t.h[j];
+            km[i * 5 + j] = int64_t{t.gdm_f[i]} * t.f[j] - int64_t{t.gdm_d[i]} * dd[j];
+            const int64_t kpr[5] = {t.k0[j], t.k1[j], 0, -int64_t{t.k1[j]}, -int64_t{t.k0[j]}};
+            kp[i * 5 + j] = kpr[i];
+        }
+    const int64_t bx = response_bound(kx), by = response_bound(ky);
+    const int64_t bp = response_bound(kp), bm = response_bound(km);
+    const int64_t lim = int64_t{1} << 31;
+    if (bx >= lim || by >= lim || bp + bm >= lim) return kMagF64;
+    const int64_t bd = (bp + bm) / 2;
+    const unsigned __int128 S = (unsigned __int128)(bx * bx) + (unsigned __int128)(by * by) +
+                                2 * (unsigned __int128)(bd * bd);
+    return S < ((unsigned __int128)1 << 32) ? kMagU32 : kMagF64;
+}
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
+
+// Output rows per CTA band.  Small bands cost 4/band extra halo rows of
+// horizontal work; large ones leave too few CTAs to fill 148 SMs.
+int choose_band(int out_w, int out_h, int frames) {
+    const int forced = env_int("SOBEL5_BAND", 0);
+    if (forced > 0) return forced;
+    const int64_t cols = (out_w + kCtaCols - 1) / kCtaCols;
+    int band = 64;
+    // keep >= ~8 CTAs per SM worth of work where the image allows it
+    while (band > 16 && cols * frames * ((out_h + band - 1) / band) < 148 * 8) band /= 2;
+    return band;
+}
+
+void fill_taps(KernelParams& kp, const sobel5_taps& t) {
+    std::memcpy(kp.f, t.f, sizeof kp.f);
+    std::memcpy(kp.h, t.h, sizeof kp.h);
+    std::memcpy(kp.k0, t.k0, sizeof kp.k0);
+    std::memcpy(kp.k1, t.k1, sizeof kp.k1);
+    std::memcpy(kp.gx_v, t.gx_v, sizeof kp.gx_v);
+    std::memcpy(kp.gy_v, t.gy_v, sizeof kp.gy_v);
+    std::memcpy(kp.gdm_f, t.gdm_f, sizeof kp.gdm_f);
+    std::memcpy(kp.gdm_d, t.gdm_d, sizeof kp.gdm_d);
+}
+
+bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+sobel5_status check_planes(const sobel5_planes* o, int out_w) {
+    if (!o) return SOBEL5_INVALID_ARG;
+    if (o->pitch < out_w || o->pitch % 4 != 0) return SOBEL5_INVALID_ARG;
+    const void* ps[7] = {o->gx, o->gy, o->gd, o->gdt, o->g, o->g32, o->u8};
+    for (const void* q : ps)
+        if (q && !aligned(q, 32)) return SOBEL5_INVALID_ARG;
+    return SOBEL5_OK;
+}
+
+template <int PF, class TAPS, int MAG>
+cudaError_t launch_one(const KernelParams& kp, dim3 grid, cudaStream_t s) {
+    sobel5_stream_kernel<PF, TAPS, MAG><<<grid, kCtaThreads, 0, s>>>(kp);
+    return cudaGetLastError();
+}
+
+cudaError_t dispatch(const KernelParams& kp, dim3 grid, int prefetch, bool dflt, MagMode mag,
+                     cudaStream_t s) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (dflt) {
+        // default taps always satisfy the uint32 magnitude bound
+        return prefetch ? launch_one<1, DefaultTaps, kMagU32>(kp, grid, s)
+                        : launch_one<0, DefaultTaps, kMagU32>(kp, grid, s);
+    }
+    if (mag == kMagU32)
+        return prefetch ? launch_one<1, KernelParams, kMagU32>(kp, grid, s)
+                        : launch_one<0, KernelParams, kMagU32>(kp, grid, s);
+    return prefetch ? launch_one<1, KernelParams, kMagF64>(kp, grid, s)
+                    : launch_one<0, KernelParams, kMagF64>(kp, grid, s);
+}
+
+sobel5_status map_cuda(cudaError_t e) {
+    if (e == cudaSuccess) return SOBEL5_OK;
+    if (e == cudaErrorMemoryAllocation) return SOBEL5_OUT_OF_MEMORY;
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) return SOBEL5_NO_DEVICE;
+    return SOBEL5_CUDA_ERROR;
+}
+
+// Common launch path for plain, batched and band launches.
+sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_t* bot,
+                            int64_t in_pitch, int64_t in_frame_stride, int width, int mid_rows,
+                            int frames, const sobel5_taps* taps, int prefetch,
+                            const sobel5_planes* out, int64_t out_frame_stride,
+                            sobel5_diag* diag, void* stream) {
+    const int top_rows = top ? 2 : 0, bot_rows = bot ? 2 : 0;
+    const int64_t rows = int64_t{top_rows} + mid_rows + bot_rows;
+    // run_stream validation order: size first (pipeline.hpp:454-456)
+    if (width < 5 || rows < 5) return SOBEL5_IMAGE_TOO_SMALL;
+    if (!taps || !mid || frames < 1) return SOBEL5_INVALID_ARG;
+    if (in_pitch < round_up(width, 4) || in_pitch % 16 != 0) return SOBEL5_INVALID_ARG;
+    if (!aligned(mid, 16) || (top && !aligned(top, 16)) || (bot && !aligned(bot, 16)))
+        return SOBEL5_INVALID_ARG;
+    if (frames > 1 && (in_frame_stride % 16 != 0 || out_frame_stride % 4 != 0))
+        return SOBEL5_INVALID_ARG;
+    const int out_w = width - 4;
+    const int out_h = static_cast<int>(rows - 4);
+    if (sobel5_status st = check_planes(out, out_w); st != SOBEL5_OK) return st;
+    if (rows > (int64_t{1} << 30) || frames > 65535) return SOBEL5_INVALID_ARG;
+
+    KernelParams kp{};
+    kp.top = top;
+    kp.mid = mid;
+    kp.bot = bot;
+    kp.in_pitch = in_pitch;
+    kp.in_frame_stride = in_frame_stride;
+    kp.top_rows = top_rows;
+    kp.mid_rows = mid_rows;
+    kp.width = width;
+    kp.out_w = out_w;
+    kp.out_h = out_h;
+    kp.band = choose_band(out_w, out_h, frames);
+    kp.gx = out->gx;
+    kp.gy = out->gy;
+    kp.gd = out->gd;
+    kp.gdt = out->gdt;
+    kp.g = out->g;
+    kp.g32 = out->g32;
+    kp.u8 = out->u8;
+    kp.pitch = out->pitch;
+    kp.out_frame_stride = out_frame_stride;
+    kp.diag = diag;
+    kp.need_mag = (out->g || out->g32 || out->u8) ? 1 : 0;
+    fill_taps(kp, *taps);
+
+    const dim3 grid(static_cast<unsigned>((out_w + kCtaCols - 1) / kCtaCols),
+                    static_cast<unsigned>((out_h + kp.band - 1) / kp.band),
+                    static_cast<unsigned>(frames));
+    if (grid.y > 65535u) {
+        // very tall images: grow the band until the grid fits
+        kp.band = (out_h + 65534) / 65535;
+    }
+    const dim3 grid2(grid.x, static_cast<unsigned>((out_h + kp.band - 1) / kp.band), grid.z);
+    const cudaError_t e = dispatch(kp, grid2, prefetch, taps_are_default(*taps), choose_mag(*taps),
+                                   static_cast<cudaStream_t>(stream));
+    return map_cuda(e);
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int sobel5_abi_version(void) { return SOBEL5_GPU_ABI_VERSION; }
+
+uint64_t sobel5_launch_count(void) { return g_launches.load(); }
+
+const char* sobel5_status_string(int status) {
+    switch (status) {
+        case SOBEL5_OK: return "ok";
+        case SOBEL5_IMAGE_TOO_SMALL: return "image too small (need at least 5x5)";
+        case SOBEL5_DIM_MISMATCH: return "dimension mismatch";
+        case SOBEL5_PARITY_VIOLATION: return "odd sum/difference pair";
+        case SOBEL5_INVALID_ARG: return "invalid argument";
+        case SOBEL5_CUDA_ERROR: return "CUDA error";
+        case SOBEL5_OUT_OF_MEMORY: return "out of memory";
+        case SOBEL5_NON_POSITIVE_PARAM: return "non-positive filter parameter";
+        case SOBEL5_PARAM_OVERFLOW: return "filter weight magnitude exceeds 2^15";
+        case SOBEL5_LANE_TOO_NARROW: return "lane width too narrow";
+        case SOBEL5_NO_DEVICE: return "no CUDA device";
+        default: return "unknown status";
+    }
+}
+
+sobel5_status sobel5_make_taps(int64_t a, int64_t b, int64_t m, int64_t n, sobel5_taps* t) {
+    if (!t) return SOBEL5_INVALID_ARG;
+    // validate_params order (filter_algebra.hpp:158-165): a, then b, m, n
+    if (a < 1 || b <= 0 || m <= 0 || n <= 0) return SOBEL5_NON_POSITIVE_PARAM;
+    // every materialized weight is a*{1, b, m, n, mb, nb} (filter_algebra.hpp:82-134)
+    if (a > kMaxWeight || b > kMaxWeight || m > kMaxWeight || n > kMaxWeight)
+        return SOBEL5_PARAM_OVERFLOW;
+    const int64_t mag = a * std::max({int64_t{1}, b, m, n, m * b, n * b});
+    if (mag > kMaxWeight) return SOBEL5_PARAM_OVERFLOW;
+    const int32_t A = static_cast<int32_t>(a), B = static_cast<int32_t>(b),
+                  M = static_cast<int32_t>(m), N = static_cast<int32_t>(n);
+    // make_stream_taps (pipeline.hpp:82-92)
+    const int32_t f[5] = {-1, -B, 0, B, 1};
+    const int32_t h[5] = {1, N, M, N, 1};
+    const int32_t k0[5] = {-A * M, -A * (N + B), -2 * A, -A * (N + B), -A * M};
+    const int32_t k1[5] = {A * (B - N), -A * M * B, -2 * A * N * B, -A * M * B, A * (B - N)};
+    const int32_t gx_v[5] = {A, A * N, A * M, A * N, A};
+    const int32_t gy_v[5] = {-A, -A * B, 0, A * B, A};
+    const int32_t gdm_f[5] = {A * M, A * (N + B), 2 * A, A * (N + B), A * M};
+    const int32_t t0 = A * (M * B + B - N), t1 = A * (N * B + B * B - M * B),
+                  t2 = A * (2 * B - 2 * N * B);
+    const int32_t gdm_d[5] = {t0, t1, t2, t1, t0};
+    t->a = A;
+    std::memcpy(t->f, f, sizeof f);
+    std::memcpy(t->h, h, sizeof h);
+    std::memcpy(t->k0, k0, sizeof k0);
+    std::memcpy(t->k1, k1, sizeof k1);
+    std::memcpy(t->gx_v, gx_v, sizeof gx_v);
+    std::memcpy(t->gy_v, gy_v, sizeof gy_v);
+    std::memcpy(t->gdm_f, gdm_f, sizeof gdm_f);
+    std::memcpy(t->gdm_d, gdm_d, sizeof gdm_d);
+    // wide_vagg (pipeline.hpp:94-105)
+    auto abs_sum = [](const int32_t* v) {
+        int64_t s = 0;
+        for (int i = 0; i < 5; ++i) s += v[i] < 0 ? -int64_t{v[i]} : int64_t{v[i]};
+        return s;
+    };
+    const int64_t mf = 255 * abs_sum(f), mh = 255 * abs_sum(h);
+    const int64_t bound = std::max({abs_sum(gx_v) * mf, abs_sum(gy_v) * mh,
+                                    abs_sum(gdm_f) * mf + abs_sum(gdm_d) * 510});
+    t->wide_vagg = bound > INT32_MAX ? 1 : 0;
+    return SOBEL5_OK;
+}
+
+sobel5_status sobel5_plan_counters(int height, const int* strip_out_w, int n_strips,
+                                   const sobel5_taps* t, int prefetch, sobel5_counters* out) {
+    if (!t || !out || (n_strips > 0 && !strip_out_w) || height < 5) return SOBEL5_INVALID_ARG;
+    auto nz = [](const int32_t* v) {
+        uint64_t c = 0;
+        for (int i = 0; i < 5; ++i) c += v[i] != 0;
+        return c;
+    };
+    // Closed form of run_strip's tallies (pipeline.hpp:330-343, 347-352,
+    // 357-411) for one strip over H rows:
+    //   hpass rows: 5 primed + one per later centre  -> H   (both modes)
+    //   k0: 2 primed + (H-5) new rows + (H-5) recomputed -> 2H-8
+    //   k1: 3 primed + (H-5) switches                 -> H-2
+    const uint64_t H = static_cast<uint64_t>(height);
+    const uint64_t rows = H, k0 = 2 * H - 8, k1 = H - 2, centres = H - 4;
+    (void)prefetch;  // the prefetch schedule reorders but does not change counts
+    uint64_t width_sum = 0;
+    for (int i = 0; i < n_strips; ++i) {
+        if (strip_out_w[i] <= 0) return SOBEL5_INVALID_ARG;
+        width_sum += static_cast<uint64_t>(strip_out_w[i]);
+    }
+    const uint64_t S = static_cast<uint64_t>(n_strips);
+    out->row_conv5_f = rows * S;
+    out->row_conv5_h = rows * S;
+    out->row_diff = rows * S;
+    out->row_conv5_k0 = k0 * S;
+    out->row_conv5_k1 = k1 * S;
+    out->row_conv3_f = 0;
+    out->row_conv3_h = 0;
+    const uint64_t per_w = (nz(t->f) + nz(t->h) + 2) * rows + nz(t->k0) * k0 + nz(t->k1) * k1 +
+                           (nz(t->gx_v) + nz(t->gy_v) + 4 + nz(t->gdm_f) + nz(t->gdm_d)) * centres;
+    out->mac = per_w * width_sum;
+    return SOBEL5_OK;
+}
+
+sobel5_status sobel5_launch(const uint8_t* d_in, int64_t in_pitch, int width, int height,
+                            const sobel5_taps* taps, int prefetch, const sobel5_planes* d_out,
+                            sobel5_diag* d_diag, void* stream) {
+    return launch_common(nullptr, d_in, nullptr, in_pitch, 0, width, height, 1, taps, prefetch,
+                         d_out, 0, d_diag, stream);
+}
+
+sobel5_status sobel5_launch_batch(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
+                                  int width, int height, int n_frames, const sobel5_taps* taps,
+                                  int prefetch, const sobel5_planes* d_out,
+                                  int64_t out_frame_stride, sobel5_diag* d_diag, void* stream) {
+    return launch_common(nullptr, d_in, nullptr, in_pitch, in_frame_stride, width, height,
+                         n_frames, taps, prefetch, d_out, out_frame_stride, d_diag, stream);
+}
+
+sobel5_status sobel5_launch_band(const uint8_t* d_top, const uint8_t* d_in, const uint8_t* d_bot,
+                                 int64_t in_pitch, int width, int band_rows,
+                                 const sobel5_taps* taps, int prefetch,
+                                 const sobel5_planes* d_out, sobel5_diag* d_diag, void* stream) {
+    return launch_common(d_top, d_in, d_bot, in_pitch, 0, width, band_rows, 1, taps, prefetch,
+                         d_out, 0, d_diag, stream);
+}
+
+sobel5_status sobel5_synth_random_device(uint8_t* d_img, int64_t pitch, int width, int height,
+                                         int64_t row_offset, uint64_t seed, uint8_t mask,
+                                         void* stream) {
+    if (!d_img || width < 1 || height < 1 || pitch < width || height > 65535 * 1024)
+        return SOBEL5_INVALID_ARG;
+    // grid.y is limited to 65535: generate in slabs
+    for (int y0 = 0; y0 < height; y0 += 65535) {
+        const int hh = std::min(65535, height - y0);
+        const dim3 grid(static_cast<unsigned>((width + 255) / 256), static_cast<unsigned>(hh));
+        synth_random_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+            d_img + static_cast<int64_t>(y0) * pitch, pitch, width, hh, row_offset + y0, seed,
+            mask);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return map_cuda(e);
+    }
+    return SOBEL5_OK;
+}
+
+}  // extern "C"

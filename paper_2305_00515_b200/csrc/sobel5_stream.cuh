@@ -1,0 +1,401 @@
+// sobel5_stream.cuh -- the fused streaming 4-direction 5x5 Sobel kernel for
+// sm_100a (B200).
+//
+// One kernel replaces the reference's whole per-strip schedule
+// (pipeline.hpp:304-414): horizontal passes F/H/D/K0/K1 (row_conv5 :117-122,
+// row_diff :124-127), vertical aggregation of gx, gy, Gd- and Gd+ (vagg5
+// :136-150, vagg_gd_minus :166-189, vagg_gd_plus :152-164), exact halving
+// (recover_diag :268-282), the double magnitude (:401-407) and, optionally,
+// the clamp_abs uint8 edge map (image_io.hpp:235-240) and a float magnitude.
+//
+// Geometry:
+//   * a warp owns 128 consecutive output columns, 4 per lane; a CTA is 4
+//     warps side by side (512 columns) and streams a band of `band` output
+//     rows top to bottom (band + 4 input rows, the 2r vertical halo).
+//   * each lane loads ONE 32-bit word (4 pixels) per input row; the 4 pixels
+//     to its right come from lane+1 by __shfl_down_sync (the paper's warp
+//     shuffle column sharing); lane 31 loads its right
+//     neighbour word itself, so no lane of the warp idles.
+//   * instead of a ring of horizontal rows (RowRing, ring.hpp:16-57) the
+//     kernel keeps the vertical sums as running accumulators: input row r
+//     contributes coefficient i = r - v to the four pending output rows
+//     v = r-4 .. r.  That needs 4 quantities x 4 live rows x 4 pixels = 64
+//     registers instead of a 5 x 5-quantity ring, and the K_d+ stream needs
+//     no bank: each row's K0 and K1 are computed once and folded with their
+//     Eq. 14 signs (+K0 at i=0, +K1 at i=1, -K1 at i=3, -K0 at i=4).
+//   * all 32-bit arithmetic wraps (unsigned), which reproduces both the
+//     reference's int32 path and its int64 "wide_vagg" path followed by the
+//     int32 narrowing cast, for ANY caller-supplied taps.
+#pragma once
+
+#include <cstdint>
+
+#include "sobel5_gpu.h"
+
+namespace sobel5_b200 {
+
+constexpr int kWarpCols = 128;          // output columns per warp (4 per lane)
+constexpr int kCtaWarps = 4;            // warps per CTA, side by side
+constexpr int kCtaCols = kWarpCols * kCtaWarps;
+constexpr int kCtaThreads = 32 * kCtaWarps;
+
+enum MagMode : int {
+    kMagU32 = 0,  // exact integer sum of squares fits uint32 (host-proven bound)
+    kMagF64 = 1,  // general: the reference's ((x*x + y*y) + d*d) + t*t in double
+};
+
+struct KernelParams {
+    // input: three vertical segments (halo above, body, halo below); a plain
+    // image is body only.  Rows are addressed in "stacked" coordinates.
+    const uint8_t* top;
+    const uint8_t* mid;
+    const uint8_t* bot;
+    int64_t in_pitch;
+    int64_t in_frame_stride;
+    int top_rows;  // 0 or 2
+    int mid_rows;
+    int width;     // input columns
+    int out_w;     // width - 4
+    int out_h;     // total stacked rows - 4
+    int band;      // output rows per CTA
+    // outputs
+    int32_t* gx;
+    int32_t* gy;
+    int32_t* gd;
+    int32_t* gdt;
+    double* g;
+    float* g32;
+    uint8_t* u8;
+    int64_t pitch;
+    int64_t out_frame_stride;
+    sobel5_diag* diag;
+    int need_mag;
+    // taps (kernel parameter space -> constant-bank operands)
+    int32_t f[5], h[5], k0[5], k1[5], gx_v[5], gy_v[5], gdm_f[5], gdm_d[5];
+};
+
+// Compile-time default taps, (a, b, m, n) = (1, 2, 6, 4) (make_stream_taps,
+// pipeline.hpp:75-107); used by the specialised instantiation only when the
+// host has compared the caller's taps equal to these.
+struct DefaultTaps {
+    static constexpr int32_t f[5] = {-1, -2, 0, 2, 1};
+    static constexpr int32_t h[5] = {1, 4, 6, 4, 1};
+    static constexpr int32_t k0[5] = {-6, -6, -2, -6, -6};
+    static constexpr int32_t k1[5] = {-2, -12, -16, -12, -2};
+    static constexpr int32_t gx_v[5] = {1, 4, 6, 4, 1};
+    static constexpr int32_t gy_v[5] = {-1, -2, 0, 2, 1};
+    static constexpr int32_t gdm_f[5] = {6, 6, 2, 6, 6};
+    static constexpr int32_t gdm_d[5] = {10, 0, -12, 0, 10};
+};
+
+__device__ __forceinline__ uint32_t ld_row_word(const uint8_t* p) {
+    return __ldg(reinterpret_cast<const unsigned int*>(p));
+}
+
+__device__ __forceinline__ void st_cs_v4(int32_t* p, int32_t a, int32_t b, int32_t c, int32_t d) {
+    asm volatile("st.global.cs.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c),
+                 "r"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void st_cs_v4f(float* p, float a, float b, float c, float d) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+                 "f"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void st_cs_v2d(double* p, double a, double b) {
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+__device__ __forceinline__ void st_cs_u32(uint8_t* p, uint32_t v) {
+    asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// clamp_abs (image_io.hpp:235-240): min(255, round(|g|)); g >= 0 here and
+// CUDA round() is round-half-away-from-zero like std::round.
+__device__ __forceinline__ uint32_t clamp_abs_u8(double g) {
+    const double r = round(g);
+    return r < 255.0 ? static_cast<uint32_t>(r) : 255u;
+}
+
+// Byte k (0..7) of the 8-byte window lo|hi.
+__device__ __forceinline__ uint32_t byte_of(uint32_t lo, uint32_t hi, int k) {
+    return k < 4 ? (lo >> (8 * k)) & 0xffu : (hi >> (8 * (k - 4))) & 0xffu;
+}
+
+template <class T>
+struct TapSource;  // selects runtime (KernelParams) or compile-time taps
+
+template <>
+struct TapSource<KernelParams> {
+    const KernelParams& p;
+    __device__ __forceinline__ int32_t f(int i) const { return p.f[i]; }
+    __device__ __forceinline__ int32_t h(int i) const { return p.h[i]; }
+    __device__ __forceinline__ int32_t k0(int i) const { return p.k0[i]; }
+    __device__ __forceinline__ int32_t k1(int i) const { return p.k1[i]; }
+    __device__ __forceinline__ int32_t gx_v(int i) const { return p.gx_v[i]; }
+    __device__ __forceinline__ int32_t gy_v(int i) const { return p.gy_v[i]; }
+    __device__ __forceinline__ int32_t gdm_f(int i) const { return p.gdm_f[i]; }
+    __device__ __forceinline__ int32_t gdm_d(int i) const { return p.gdm_d[i]; }
+};
+
+__host__ __device__ constexpr int32_t pick5(int i, int32_t a, int32_t b, int32_t c, int32_t d,
+                                            int32_t e) {
+    return i == 0 ? a : i == 1 ? b : i == 2 ? c : i == 3 ? d : e;
+}
+
+template <>
+struct TapSource<DefaultTaps> {
+    const KernelParams& p;
+    __device__ static constexpr int32_t f(int i) { return pick5(i, -1, -2, 0, 2, 1); }
+    __device__ static constexpr int32_t h(int i) { return pick5(i, 1, 4, 6, 4, 1); }
+    __device__ static constexpr int32_t k0(int i) { return pick5(i, -6, -6, -2, -6, -6); }
+    __device__ static constexpr int32_t k1(int i) { return pick5(i, -2, -12, -16, -12, -2); }
+    __device__ static constexpr int32_t gx_v(int i) { return pick5(i, 1, 4, 6, 4, 1); }
+    __device__ static constexpr int32_t gy_v(int i) { return pick5(i, -1, -2, 0, 2, 1); }
+    __device__ static constexpr int32_t gdm_f(int i) { return pick5(i, 6, 6, 2, 6, 6); }
+    __device__ static constexpr int32_t gdm_d(int i) { return pick5(i, 10, 0, -12, 0, 10); }
+};
+
+// Row pointer of stacked input row `row` (0-based, stacked coordinates).
+__device__ __forceinline__ const uint8_t* stacked_row(const KernelParams& p, int64_t frame_off,
+                                                      int row) {
+    if (row < p.top_rows) return p.top + frame_off + static_cast<int64_t>(row) * p.in_pitch;
+    row -= p.top_rows;
+    if (row < p.mid_rows) return p.mid + frame_off + static_cast<int64_t>(row) * p.in_pitch;
+    row -= p.mid_rows;
+    return p.bot + frame_off + static_cast<int64_t>(row) * p.in_pitch;
+}
+
+// The fused streaming kernel.
+//   PF     : 0 = load each row when it is consumed (Prefetch::off);
+//            1 = the next row's load is issued before the current row is
+//                processed (Prefetch::on, the paper's Eq. 9 mod-6 ring);
+//   TAPS   : KernelParams (runtime taps) or DefaultTaps (compile-time);
+//   MAG    : MagMode.
+template <int PF, class TAPS, int MAG>
+__global__ void __launch_bounds__(kCtaThreads)
+    sobel5_stream_kernel(const __grid_constant__ KernelParams p) {
+    const TapSource<TAPS> T{p};
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int x0 = (blockIdx.x * kCtaWarps + warp) * kWarpCols + lane * 4;
+    if ((x0 - lane * 4) >= p.out_w) return;  // whole warp right of the image
+    const int oy0 = blockIdx.y * p.band;
+    const int n_out = min(p.band, p.out_h - oy0);
+    const int n_in = n_out + 4;
+    const int64_t in_frame = static_cast<int64_t>(blockIdx.z) * p.in_frame_stride;
+    const int64_t out_frame = static_cast<int64_t>(blockIdx.z) * p.out_frame_stride;
+    const bool load_a = x0 < p.width;
+    const bool load_b = lane == 31 && x0 + 4 < p.width;
+    const bool full = x0 + 3 < p.out_w;
+
+    // Pending vertical accumulators, slot = (output row) mod 5.
+    uint32_t acc_x[5][4], acc_y[5][4], acc_p[5][4], acc_m[5][4];
+
+    uint32_t nxt_a = 0, nxt_b = 0;
+    if (PF) {
+        const uint8_t* rp = stacked_row(p, in_frame, oy0);
+        nxt_a = load_a ? ld_row_word(rp + x0) : 0u;
+        nxt_b = load_b ? ld_row_word(rp + x0 + 4) : 0u;
+    }
+
+    for (int base = 0; base < n_in; base += 5) {
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+            const int r = base + s;
+            if (r >= n_in) break;
+            uint32_t wa, wb;
+            if (PF) {
+                wa = nxt_a;
+                wb = nxt_b;
+                if (r + 1 < n_in) {
+                    const uint8_t* rp = stacked_row(p, in_frame, oy0 + r + 1);
+                    nxt_a = load_a ? ld_row_word(rp + x0) : 0u;
+                    nxt_b = load_b ? ld_row_word(rp + x0 + 4) : 0u;
+                }
+            } else {
+                const uint8_t* rp = stacked_row(p, in_frame, oy0 + r);
+                wa = load_a ? ld_row_word(rp + x0) : 0u;
+                wb = load_b ? ld_row_word(rp + x0 + 4) : 0u;
+            }
+            // Column sharing: the 4 pixels right of this lane's word.
+            const uint32_t sh = __shfl_down_sync(0xffffffffu, wa, 1);
+            if (lane != 31) wb = sh;
+
+            uint32_t px[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) px[k] = byte_of(wa, wb, k);
+
+            // Horizontal passes for the 4 pixels of this lane.
+            uint32_t F[4], H[4], D[4], K0[4], K1[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t f = 0, hh = 0, a0 = 0, a1 = 0;
+#pragma unroll
+                for (int t = 0; t < 5; ++t) {
+                    f += static_cast<uint32_t>(T.f(t)) * px[j + t];
+                    hh += static_cast<uint32_t>(T.h(t)) * px[j + t];
+                    a0 += static_cast<uint32_t>(T.k0(t)) * px[j + t];
+                    a1 += static_cast<uint32_t>(T.k1(t)) * px[j + t];
+                }
+                F[j] = f;
+                H[j] = hh;
+                K0[j] = a0;
+                K1[j] = a1;
+                D[j] = px[j + 3] - px[j + 1];
+            }
+
+            // Vertical: row r feeds output rows v = r - i, i = 0..4.
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                const int slot = (s - i + 5) % 5;
+                const uint32_t cx = static_cast<uint32_t>(T.gx_v(i));
+                const uint32_t cy = static_cast<uint32_t>(T.gy_v(i));
+                const uint32_t cf = static_cast<uint32_t>(T.gdm_f(i));
+                const uint32_t cd = static_cast<uint32_t>(T.gdm_d(i));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t vx = cx * F[j];
+                    const uint32_t vy = cy * H[j];
+                    const uint32_t vm = cf * F[j] - cd * D[j];
+                    uint32_t vp;
+                    if (i == 0) vp = K0[j];
+                    else if (i == 1) vp = K1[j];
+                    else if (i == 3) vp = 0u - K1[j];
+                    else if (i == 4) vp = 0u - K0[j];
+                    else vp = 0u;
+                    if (i == 0) {
+                        acc_x[slot][j] = vx;
+                        acc_y[slot][j] = vy;
+                        acc_m[slot][j] = vm;
+                        acc_p[slot][j] = vp;
+                    } else {
+                        acc_x[slot][j] += vx;
+                        acc_y[slot][j] += vy;
+                        acc_m[slot][j] += vm;
+                        if (i != 2) acc_p[slot][j] += vp;
+                    }
+                }
+            }
+
+            // Output row v = r - 4 is complete: epilogue + stores.
+            if (r >= 4) {
+                const int slot = (s + 1) % 5;  // (s - 4) mod 5
+                const int v = r - 4;
+                int32_t gx[4], gy[4], gd[4], gdt[4];
+                bool odd_any = false;
+                int32_t odd_p = 0, odd_m = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t P = acc_p[slot][j], M = acc_m[slot][j];
+                    const uint32_t sum = P + M, dif = P - M;
+                    const bool odd = (sum & 1u) != 0u && (x0 + j) < p.out_w;
+                    if (odd && !odd_any) {
+                        odd_p = static_cast<int32_t>(P);
+                        odd_m = static_cast<int32_t>(M);
+                    }
+                    odd_any |= odd;
+                    gx[j] = static_cast<int32_t>(acc_x[slot][j]);
+                    gy[j] = static_cast<int32_t>(acc_y[slot][j]);
+                    gd[j] = static_cast<int32_t>(sum) >> 1;
+                    gdt[j] = static_cast<int32_t>(dif) >> 1;
+                }
+                // recover_diag's ParityViolation (pipeline.hpp:268-273),
+                // recorded once per warp instead of thrown.
+                const unsigned odd_mask = __ballot_sync(0xffffffffu, odd_any);
+                if (odd_mask && p.diag && lane == __ffs(odd_mask) - 1) {
+                    if (atomicAdd(&p.diag->violations, 1) == 0) {
+                        p.diag->sum = odd_p;
+                        p.diag->diff = odd_m;
+                    }
+                }
+
+                const int64_t row_off = out_frame + static_cast<int64_t>(oy0 + v) * p.pitch + x0;
+                if (full) {
+                    if (p.gx) st_cs_v4(p.gx + row_off, gx[0], gx[1], gx[2], gx[3]);
+                    if (p.gy) st_cs_v4(p.gy + row_off, gy[0], gy[1], gy[2], gy[3]);
+                    if (p.gd) st_cs_v4(p.gd + row_off, gd[0], gd[1], gd[2], gd[3]);
+                    if (p.gdt) st_cs_v4(p.gdt + row_off, gdt[0], gdt[1], gdt[2], gdt[3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (x0 + j < p.out_w) {
+                            if (p.gx) p.gx[row_off + j] = gx[j];
+                            if (p.gy) p.gy[row_off + j] = gy[j];
+                            if (p.gd) p.gd[row_off + j] = gd[j];
+                            if (p.gdt) p.gdt[row_off + j] = gdt[j];
+                        }
+                    }
+                }
+                if (p.need_mag) {
+                    double g[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (MAG == kMagU32) {
+                            const uint32_t ux = static_cast<uint32_t>(gx[j]);
+                            const uint32_t uy = static_cast<uint32_t>(gy[j]);
+                            const uint32_t ud = static_cast<uint32_t>(gd[j]);
+                            const uint32_t ut = static_cast<uint32_t>(gdt[j]);
+                            const uint32_t S = ux * ux + uy * uy + ud * ud + ut * ut;
+                            g[j] = __dsqrt_rn(__uint2double_rn(S));
+                        } else {
+                            const double dx = gx[j], dy = gy[j], dd = gd[j], dt = gdt[j];
+                            double S = __dmul_rn(dx, dx);
+                            S = __dadd_rn(S, __dmul_rn(dy, dy));
+                            S = __dadd_rn(S, __dmul_rn(dd, dd));
+                            S = __dadd_rn(S, __dmul_rn(dt, dt));
+                            g[j] = __dsqrt_rn(S);
+                        }
+                    }
+                    if (full) {
+                        if (p.g) {
+                            st_cs_v2d(p.g + row_off, g[0], g[1]);
+                            st_cs_v2d(p.g + row_off + 2, g[2], g[3]);
+                        }
+                        if (p.g32)
+                            st_cs_v4f(p.g32 + row_off, __double2float_rn(g[0]),
+                                      __double2float_rn(g[1]), __double2float_rn(g[2]),
+                                      __double2float_rn(g[3]));
+                        if (p.u8) {
+                            const uint32_t q = clamp_abs_u8(g[0]) | (clamp_abs_u8(g[1]) << 8) |
+                                               (clamp_abs_u8(g[2]) << 16) |
+                                               (clamp_abs_u8(g[3]) << 24);
+                            st_cs_u32(p.u8 + row_off, q);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            if (x0 + j < p.out_w) {
+                                if (p.g) p.g[row_off + j] = g[j];
+                                if (p.g32) p.g32[row_off + j] = __double2float_rn(g[j]);
+                                if (p.u8) p.u8[row_off + j] = static_cast<uint8_t>(clamp_abs_u8(g[j]));
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Device-side synth_random (synth.hpp:11-35), random-access form:
+// pixel i = byte (i mod 8) of splitmix64 output word floor(i/8), where word
+// k is mix(seed + (k+1) * 0x9E3779B97F4A7C15).
+__device__ __forceinline__ uint64_t splitmix64_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+__global__ void synth_random_kernel(uint8_t* img, int64_t pitch, int width, int height,
+                                    int64_t row_offset, uint64_t seed, uint8_t mask) {
+    const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    if (x >= width || y >= height) return;
+    const uint64_t i = static_cast<uint64_t>(row_offset + y) * static_cast<uint64_t>(width) +
+                       static_cast<uint64_t>(x);
+    const uint64_t word = splitmix64_mix(seed + (i / 8 + 1) * 0x9E3779B97F4A7C15ULL);
+    img[static_cast<int64_t>(y) * pitch + x] =
+        static_cast<uint8_t>((word >> (8 * (i % 8))) & 0xff) & mask;
+}
+
+}  // namespace sobel5_b200
