@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""Benchmark: 4-direction 5x5 Sobel on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload 8k|1080p-batch|32k-bands] [--contract sr|u8|sr32]
+
+One "step" = one pass of the hot path over one synthetic image (or batch):
+the fused sm_100a kernel over an input already resident in HBM.  Default
+workload is BASELINE config C3, 7680x4320 uint8 (the north-star roofline
+case); at N>1 every rank processes its own frame (weak scaling, no
+communication: the batch-split sharding of SURVEY.md section 8e).
+
+Prints ONE JSON line (rank 0).  `value` is whole-job Gpixel/s (input pixels,
+metrics.hpp:176 convention) timed with CUDA events on the launching stream,
+max over ranks; `e2e` is the same metric through the C ABI host-buffer entry
+(sobel5_run_host) with pinned host buffers, copies inside the timed region;
+`roofline` is algorithmic bytes per launch / launch time vs the measured HBM
+copy bandwidth; `cpu_baseline` is the reference's own run_stream compiled from
+its headers (oracle/_ref) timed on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gpixel/s and achieved HBM GB/s (% of peak) for 4-dir 5x5 Sobel, 1/2/4/8 B200"
+UNIT = "Gpixel/s"
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+OUT_BYTES = {"sr": 24, "sr32": 20, "u8": 1}  # per output pixel
+CONTRACT_PLANES = {"sr": ("gx", "gy", "gd", "gdt", "g"), "sr32": ("gx", "gy", "gd", "gdt", "g32"),
+                   "u8": ("u8",)}
+WORKLOADS = {
+    "8k": dict(w=7680, h=4320, frames=1, name="7680x4320 uint8 single image (BASELINE C3)"),
+    "4k": dict(w=3840, h=2160, frames=1, name="3840x2160 uint8 single image (BASELINE C2)"),
+    "1080p-batch": dict(w=1920, h=1080, frames=256,
+                        name="batch of 256 1920x1080 uint8 frames split across ranks (C4)"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="8k", choices=sorted(WORKLOADS))
+    ap.add_argument("--contract", default="sr", choices=sorted(OUT_BYTES))
+    ap.add_argument("--prefetch", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="budget of CPU work for the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured", d
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback", {}
+
+
+# ---- clocks sampling (nvml) during the timed region --------------------------------
+
+
+class ClockSampler:
+    REASONS = {
+        0x0000000000000001: "gpu_idle", 0x0000000000000002: "applications_clocks_setting",
+        0x0000000000000004: "sw_power_cap", 0x0000000000000008: "hw_slowdown",
+        0x0000000000000010: "sync_boost", 0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown", 0x0000000000000080: "hw_power_brake_slowdown",
+        0x0000000000000100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.nv, self.err = None, str(e)
+
+    def _sample(self):
+        nv = self.nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        mask = fn(self.h)
+        for bit, name in self.REASONS.items():
+            if mask & bit and name != "gpu_idle":
+                self.reasons.add(name)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            time.sleep(0.005)
+
+    def start(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self.nv:
+            self._stop.set()
+            self._t.join()
+            try:
+                self._sample()
+            except Exception:
+                pass
+
+    def summary(self):
+        if not self.nv or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---- CPU reference arm ----------------------------------------------------------------
+
+
+def cpu_reference(w, h, frames, seconds, max_iters=None):
+    """The reference's run_stream (pipeline.hpp:474) from its own headers,
+    lanes 256, prefetch on, one worker per host core, timed with the
+    reference's measure() (metrics.hpp:142-179).  Falls back to the C oracle
+    port when the compiled reference is absent."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    cores = os.cpu_count() or 1
+    if pyoracle.ref_available():
+        R = pyoracle.Reference()
+        img = R.synth_random(w, h, 1)
+        t0 = time.perf_counter()
+        mean1, _ = R.measure_run_stream(img, lanes=256, prefetch=True, workers=cores, iters=1)
+        first = time.perf_counter() - t0
+        iters = max(1, min(30, int(seconds / max(mean1, 1e-6))))
+        if max_iters:
+            iters = min(iters, max_iters)
+        mean, sd = R.measure_run_stream(img, lanes=256, prefetch=True, workers=cores,
+                                        iters=iters)
+        kind = "reference"
+        sample = (f"{iters} timed + 1 warm-up reference run_stream calls (lanes 256, prefetch on, "
+                  f"workers {cores}) on one {w}x{h} synth_random frame; first call {first:.2f}s")
+        cores_used = cores
+    else:  # oracle port, single thread
+        O = pyoracle.Oracle()
+        img = O.synth_random(w, h, 1)
+        t0 = time.perf_counter()
+        O.run_stream(img)
+        mean = time.perf_counter() - t0
+        sd, kind, cores_used = 0.0, "port", 1
+        sample = f"1 oracle-port run_stream call on one {w}x{h} frame (reference not built)"
+    gpx = w * h / mean / 1e9
+    return {"value": gpx, "unit": UNIT, "cores": cores_used, "kind": kind, "sample": sample,
+            "mean_s_per_frame": mean, "stddev_s": sd,
+            "note": f"per-frame rate; a {frames}-frame workload scales linearly"}
+
+
+def run_reference_arm(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    wl = WORKLOADS[a.workload]
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    cores = os.cpu_count() or 1
+    w, h = wl["w"], wl["h"]
+    if pyoracle.ref_available():
+        R = pyoracle.Reference()
+        img = R.synth_random(w, h, 1)
+        for _ in range(max(0, min(a.warmup, 2))):
+            R.measure_run_stream(img, lanes=256, prefetch=True, workers=cores, iters=1)
+        steps = max(1, min(a.steps, 20))
+        mean, sd = R.measure_run_stream(img, lanes=256, prefetch=True, workers=cores,
+                                        iters=steps)
+        kind = "reference"
+    else:
+        O = pyoracle.Oracle()
+        img = O.synth_random(w, h, 1)
+        steps = 1
+        t0 = time.perf_counter()
+        O.run_stream(img)
+        mean, sd, kind, cores = time.perf_counter() - t0, 0.0, "port", 1
+    gpx = w * h / mean / 1e9
+    sample = (f"{steps} timed reference run_stream calls (lanes 256, prefetch on, workers "
+              f"{cores}) on one {w}x{h} frame, 1 frame per step")
+    line = {"metric": METRIC, "value": gpx, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": steps, "warmup": min(a.warmup, 2), "ms_per_step": mean * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (synth_random seed 1)",
+            "config": {"workload": wl["name"], "contract": "sr (4 x int32 + f64 g)",
+                       "stddev_s": sd},
+            "cpu_baseline": {"value": gpx, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": gpx, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm ------------------------------------------------------------------------------
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference_arm(a)
+
+    rank, world, local = dist_env()
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_00515_b200 import _abi, api
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    _abi.load()
+
+    wl = WORKLOADS[a.workload]
+    w, h = wl["w"], wl["h"]
+    frames = wl["frames"]
+    if frames > 1:  # batch split across ranks, no communication (C4)
+        frames = max(1, frames // world)
+    ow, oh = w - 4, h - 4
+    planes_names = CONTRACT_PLANES[a.contract]
+    taps = api.make_stream_taps()
+    stream = torch.cuda.current_stream(dev)
+    s_ptr = stream.cuda_stream
+
+    # Inputs: rotate over enough frames that the input set exceeds L2 (126 MB);
+    # the outputs alone (24 B/px) are 6x L2 at 8K.
+    in_bytes = w * h * frames
+    n_in = max(2, int(np.ceil(2 * 126e6 / in_bytes)))
+    n_in = min(n_in, 8)
+    ins = []
+    for i in range(n_in):
+        d, pitch = api.alloc_input(w, h, dev, frames=frames)
+        for f in range(frames):
+            sub = d[f] if frames > 1 else d
+            api.synth_random_device(sub, pitch, w, h, seed=1 + i * frames + f, stream=s_ptr)
+        ins.append(d)
+    out, op = api.alloc_planes(ow, oh, planes_names, dev, frames=frames)
+    torch.cuda.synchronize()
+
+    def step(i):
+        d = ins[i % n_in]
+        if frames > 1:
+            api.launch_batch(d, pitch, h * pitch, w, h, frames, taps, a.prefetch, out, op,
+                             oh * op, stream=s_ptr)
+        else:
+            api.launch(d, pitch, w, h, taps, a.prefetch, out, op, stream=s_ptr)
+
+    for i in range(a.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    launches0 = api.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.start()
+    e0.record(stream)
+    for i in range(a.steps):
+        step(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks.stop()
+    launches = api.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms_step = ms / a.steps
+    px_step = w * h * frames
+    value = px_step * world / (ms_step * 1e-3) / 1e9
+
+    hbm_peak, peak_kind, peaks = measured_peaks()
+    alg_bytes = px_step + ow * oh * frames * OUT_BYTES[a.contract]
+    achieved = alg_bytes / (ms_step * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tr = json.load(f)
+            traffic = tr.get(f"{a.workload}/{a.contract}")
+        except Exception:
+            traffic = None
+
+    # ---- variants (same workload, other output contracts / prefetch off) ----
+    variants = {}
+    if rank == 0 and frames == 1:
+        for name, contract, pf in (("u8", "u8", 1), ("sr32", "sr32", 1), ("sr_prefetch_off",
+                                                                          "sr", 0)):
+            if contract == a.contract and pf == a.prefetch:
+                continue
+            vo, vp = api.alloc_planes(ow, oh, CONTRACT_PLANES[contract], dev)
+            for i in range(5):
+                api.launch(ins[i % n_in], pitch, w, h, taps, pf, vo, vp, stream=s_ptr)
+            torch.cuda.synchronize()
+            v0, v1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            v0.record(stream)
+            n = 50
+            for i in range(n):
+                api.launch(ins[i % n_in], pitch, w, h, taps, pf, vo, vp, stream=s_ptr)
+            v1.record(stream)
+            torch.cuda.synchronize()
+            vms = v0.elapsed_time(v1) / n
+            vb = w * h + ow * oh * OUT_BYTES[contract]
+            variants[name] = {"gpx_s": w * h / vms / 1e6, "us": vms * 1e3,
+                              "hbm_gbs": vb / vms / 1e6, "frac": vb / vms / 1e6 / hbm_peak,
+                              "alg_bytes": vb}
+            del vo
+        torch.cuda.empty_cache()
+
+    # ---- e2e through the C ABI host entry with pinned buffers ----
+    e2e = None
+    if rank == 0 and not a.no_e2e and frames == 1:
+        import ctypes as C
+        ctx = api.Context(local)
+        h_in = torch.empty((h, w), dtype=torch.uint8, pin_memory=True)
+        h_in.copy_(ins[0][:, :w].cpu())
+        dt = {"gx": torch.int32, "gy": torch.int32, "gd": torch.int32, "gdt": torch.int32,
+              "g": torch.float64, "g32": torch.float32, "u8": torch.uint8}
+        h_out = {k: torch.empty((oh, ow), dtype=dt[k], pin_memory=True) for k in planes_names}
+        pl = _abi.Planes(pitch=ow)
+        for k, v in h_out.items():
+            setattr(pl, k, v.data_ptr())
+        diag = _abi.Diag()
+        L = _abi.load()
+
+        def e2e_call():
+            st = L.sobel5_run_host(ctx.handle, h_in.data_ptr(), w, h, C.byref(taps), a.prefetch,
+                                   C.byref(pl), C.byref(diag))
+            api.check(st, "sobel5_run_host")
+
+        for _ in range(3):
+            e2e_call()
+        n_e2e = max(5, min(a.steps, 30))
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            e2e_call()
+        t1 = time.perf_counter()
+        s_e2e = (t1 - t0) / n_e2e
+        d2h = sum(v.numel() * v.element_size() for v in h_out.values())
+        e2e = {"value": w * h / s_e2e / 1e9, "unit": UNIT, "h2d_bytes_per_step": w * h,
+               "d2h_bytes_per_step": d2h, "ms_per_step": s_e2e * 1e3, "steps": n_e2e,
+               "path": "sobel5_run_host (C ABI), pinned host buffers, chunked H2D/kernel/D2H "
+                       "overlap on 3 streams"}
+        ctx.close()
+
+    cpu = None
+    if rank == 0 and not a.no_cpu_baseline:
+        cpu = cpu_reference(w, h, frames, a.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (synth_random seed 1+i generated on device, reference generator)",
+            "config": {"workload": wl["name"], "frames_per_rank": frames,
+                       "contract": a.contract + " (" + "+".join(planes_names) + ")",
+                       "prefetch": bool(a.prefetch), "parallelism": f"batch-split x{world}",
+                       "l2": f"inputs rotated over {n_in} buffers ({n_in * in_bytes / 1e6:.0f} MB)"
+                             f" + {ow * oh * frames * OUT_BYTES[a.contract] / 1e6:.0f} MB of "
+                             "outputs per step, both > 126 MB L2",
+                       "hbm_gbs_achieved": achieved},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
+                         if peak_kind == "measured" else "fallback (B200_PROFILING.md)",
+                         "alg_bytes_per_launch": alg_bytes, "kernel": "sobel5_stream_kernel",
+                         "kernel_us": ms_step * 1e3},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "variants": variants,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

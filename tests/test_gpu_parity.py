@@ -1,0 +1,250 @@
+"""GPU parity: the sm_100a kernels through the C ABI vs the oracle and the
+reference's golden fixtures.  Integer planes and the clamp_abs uint8 map
+must be bit-exact; the double magnitude is bit-exact too (the kernel
+reproduces the reference's rounding sequence); the optional float magnitude
+is within 1 ulp of the double one (tolerance stated in
+test_float_magnitude_within_one_ulp)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+PLANES = ("gx", "gy", "gd", "gdt", "g")
+ALL = PLANES + ("g32", "u8")
+
+with open(os.path.join(GOLD, "cases.json")) as f:
+    CASES = json.load(f)
+ARRS = np.load(os.path.join(GOLD, "cases.npz"))
+with open(os.path.join(GOLD, "hashes.json")) as f:
+    HASHES = json.load(f)
+
+
+@pytest.fixture(scope="module")
+def S(cuda):
+    import paper_2305_00515_b200 as S
+    return S
+
+
+def run_device(S, img, taps, prefetch, planes=ALL):
+    import torch
+    from paper_2305_00515_b200 import api
+    h, w = img.shape
+    d_in, pitch = api.alloc_input(w, h)
+    d_in.zero_()
+    d_in[:, :w].copy_(torch.from_numpy(np.ascontiguousarray(img)))
+    out, op = api.alloc_planes(w - 4, h - 4, planes)
+    for v in out.values():
+        v.fill_(0x5A if v.dtype == torch.uint8 else 7)  # poison: every pixel must be written
+    diag = torch.zeros(4, dtype=torch.int32, device="cuda")
+    api.launch(d_in, pitch, w, h, taps, prefetch, out, op, diag)
+    torch.cuda.synchronize()
+    return {k: v[:, : w - 4].cpu().numpy() for k, v in out.items()}, diag.cpu().tolist()
+
+
+def taps_of(S, d):
+    return S.Taps.from_dict(d)
+
+
+@pytest.mark.parametrize("prefetch", [0, 1])
+@pytest.mark.parametrize("i", range(len(CASES)), ids=[c["name"] for c in CASES])
+def test_golden_case_device(S, i, prefetch):
+    c = CASES[i]
+    img = ARRS[f"img{i}"]
+    taps = taps_of(S, c["taps"])
+    if c["status"] == 13:
+        with pytest.raises(S.ImageTooSmall):
+            run_device(S, img, taps, prefetch)
+        return
+    got, diag = run_device(S, img, taps, prefetch)
+    if c["status"] == 17:
+        assert diag[0] > 0  # recover_diag parity violation recorded
+        return
+    assert diag[0] == 0
+    for k in PLANES:
+        np.testing.assert_array_equal(got[k], ARRS[f"{k}{i}"], err_msg=k)
+    np.testing.assert_array_equal(got["u8"], ARRS[f"u8{i}"])
+
+
+@pytest.mark.parametrize("i", range(len(CASES)), ids=[c["name"] for c in CASES])
+def test_golden_case_run_stream_api(S, i):
+    """The drop-in run_stream (host buffers, chunked copy pipeline)."""
+    c = CASES[i]
+    img = ARRS[f"img{i}"]
+    w = img.shape[1]
+    taps = taps_of(S, c["taps"])
+    plan = S.plan_strips(max(w, 5), c["lanes"], 2)
+    if c["status"] == 13:
+        with pytest.raises(S.ImageTooSmall):
+            S.run_stream(img, taps, plan, S.Prefetch.on)
+        return
+    if c["status"] == 17:
+        with pytest.raises(S.ParityViolation) as ei:
+            S.run_stream(img, taps, plan, S.Prefetch(c["prefetch"]))
+        assert str(ei.value).startswith("odd sum/difference pair (")
+        return
+    r = S.run_stream(img, taps, plan, S.Prefetch(c["prefetch"]))
+    for k in PLANES:
+        np.testing.assert_array_equal(getattr(r, k), ARRS[f"{k}{i}"], err_msg=k)
+    assert r.counters == c["counters"]
+
+
+def test_random_sweep_vs_oracle(S, oracle):
+    """SPEC ACCEPTANCE 1 analogue: seeded random images 5x5..700x150, both
+    kernel variants, default / non-default / fault-injected taps."""
+    import pyoracle
+    rng = np.random.default_rng(11)
+    variants = [oracle.make_stream_taps(), oracle.make_stream_taps(2, 3, 5, 1),
+                oracle.make_stream_taps(1, 32768, 1, 1)]
+    fault = oracle.make_stream_taps()
+    fault.k0[0] += 2
+    variants.append(fault)
+    for trial in range(48):
+        w, h = int(rng.integers(5, 700)), int(rng.integers(5, 150))
+        img = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        if trial % 3 == 0:
+            img &= 7
+        t = variants[trial % len(variants)]
+        st, ref, _ = oracle.run_stream(img, t)
+        assert st == 0
+        got, diag = run_device(S, img, S.Taps.from_dict(t.as_dict()), trial % 2)
+        assert diag[0] == 0
+        for k in PLANES:
+            np.testing.assert_array_equal(got[k], ref[k], err_msg=f"{k} {w}x{h} taps{trial % 4}")
+        np.testing.assert_array_equal(got["u8"], oracle.clamp_abs(ref["g"]))
+    del pyoracle
+
+
+def test_float_magnitude_within_one_ulp(S, oracle):
+    """g32: tolerance 1 ulp of float32 relative to the double magnitude."""
+    rng = np.random.default_rng(5)
+    img = rng.integers(0, 256, (130, 777), dtype=np.uint8)
+    got, _ = run_device(S, img, S.make_stream_taps(), 1)
+    ref = got["g"]
+    exact = ref.astype(np.float32)
+    ulps = np.abs(got["g32"].view(np.int32).astype(np.int64) - exact.view(np.int32))
+    assert ulps.max() <= 1
+
+
+def test_subset_of_planes(S, oracle):
+    """Only requested planes are written (NULL planes skipped)."""
+    rng = np.random.default_rng(2)
+    img = rng.integers(0, 256, (40, 300), dtype=np.uint8)
+    st, ref, _ = oracle.run_stream(img)
+    for planes in (("gx",), ("u8",), ("gd", "g"), ("gdt", "g32")):
+        got, _ = run_device(S, img, S.make_stream_taps(), 1, planes)
+        assert set(got) == set(planes)
+        for k in planes:
+            if k in ref:
+                np.testing.assert_array_equal(got[k], ref[k])
+        if "u8" in planes:
+            np.testing.assert_array_equal(got["u8"], oracle.clamp_abs(ref["g"]))
+
+
+def test_batch_launch(S, oracle):
+    import torch
+    from paper_2305_00515_b200 import api
+    rng = np.random.default_rng(3)
+    w, h, n = 301, 37, 5
+    imgs = rng.integers(0, 256, (n, h, w), dtype=np.uint8)
+    d_in, pitch = api.alloc_input(w, h, frames=n)
+    d_in[:, :, :w].copy_(torch.from_numpy(imgs))
+    out, op = api.alloc_planes(w - 4, h - 4, PLANES, frames=n)
+    api.launch_batch(d_in, pitch, h * pitch, w, h, n, S.make_stream_taps(), 1, out, op,
+                     (h - 4) * op)
+    torch.cuda.synchronize()
+    for f in range(n):
+        st, ref, _ = oracle.run_stream(imgs[f])
+        for k in PLANES:
+            np.testing.assert_array_equal(out[k][f, :, : w - 4].cpu().numpy(), ref[k])
+
+
+@pytest.mark.parametrize("n_bands", [2, 3, 5])
+def test_row_band_partition_equals_whole(S, oracle, n_bands):
+    """C5 row-band tiler: bands with 2-row halos above/below stitch to the
+    single-image result (the multi-GPU partition, exercised on one GPU)."""
+    import torch
+    from paper_2305_00515_b200 import api
+    rng = np.random.default_rng(4)
+    w, h = 523, 97
+    img = rng.integers(0, 256, (h, w), dtype=np.uint8)
+    st, ref, _ = oracle.run_stream(img)
+    bounds = np.linspace(0, h, n_bands + 1).astype(int)
+    for b in range(n_bands):
+        r0, r1 = int(bounds[b]), int(bounds[b + 1])
+        body, pitch = api.alloc_input(w, r1 - r0)
+        body[:, :w].copy_(torch.from_numpy(img[r0:r1]))
+        top = bot = None
+        if r0 > 0:
+            top, _ = api.alloc_input(w, 2)
+            top[:, :w].copy_(torch.from_numpy(img[r0 - 2:r0]))
+        if r1 < h:
+            bot, _ = api.alloc_input(w, 2)
+            bot[:, :w].copy_(torch.from_numpy(img[r1:r1 + 2]))
+        rows = (r1 - r0) + (2 if top is not None else 0) + (2 if bot is not None else 0) - 4
+        out, op = api.alloc_planes(w - 4, rows, PLANES)
+        api.launch_band(top, body, bot, pitch, w, r1 - r0, S.make_stream_taps(), 1, out, op)
+        torch.cuda.synchronize()
+        y0 = r0 - 2 if top is not None else 0
+        for k in PLANES:
+            np.testing.assert_array_equal(out[k][:, : w - 4].cpu().numpy(), ref[k][y0:y0 + rows],
+                                          err_msg=f"band {b} {k}")
+
+
+def test_device_synth_matches_reference_generator(S, oracle):
+    import torch
+    from paper_2305_00515_b200 import api
+    for (w, h, seed, mask) in [(16, 1, 1, 0xFF), (1920, 1080, 1, 0xFF), (333, 17, 9, 0x07)]:
+        d, pitch = api.alloc_input(w, h)
+        api.synth_random_device(d, pitch, w, h, seed, mask)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(d[:, :w].cpu().numpy(),
+                                      oracle.synth_random(w, h, seed) & mask)
+    # a band generated with a row offset equals the same rows of the full image
+    d, pitch = api.alloc_input(100, 7)
+    api.synth_random_device(d, pitch, 100, 7, 5, 0xFF, row_offset=13)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(d[:, :100].cpu().numpy(),
+                                  oracle.synth_random(100, 20, 5)[13:20])
+
+
+@pytest.mark.parametrize("key", list(HASHES))
+def test_golden_hashes_full_size(S, oracle, key):
+    """Full-size C1..C3 planes hashed against the reference's FNV-1a values."""
+    import torch
+    from paper_2305_00515_b200 import api
+    e = HASHES[key]
+    w, h = e["w"], e["h"]
+    d_in, pitch = api.alloc_input(w, h)
+    api.synth_random_device(d_in, pitch, w, h, e["seed"], e["mask"])
+    out, op = api.alloc_planes(w - 4, h - 4, PLANES + ("u8",))
+    diag = torch.zeros(4, dtype=torch.int32, device="cuda")
+    api.launch(d_in, pitch, w, h, S.make_stream_taps(), 1, out, op, diag)
+    torch.cuda.synchronize()
+    assert diag[0].item() == 0
+    assert f"{oracle.fnv1a64(d_in[:, :w].cpu().numpy()):016x}" == e["fnv1a64"]["input"]
+    for k in PLANES + ("u8",):
+        host = np.ascontiguousarray(out[k][:, : w - 4].cpu().numpy())
+        assert f"{oracle.fnv1a64(host):016x}" == e["fnv1a64"][k], k
+
+
+def test_launch_count_increments(S):
+    from paper_2305_00515_b200 import api
+    before = api.launch_count()
+    run_device(S, np.zeros((8, 8), np.uint8), S.make_stream_taps(), 1)
+    assert api.launch_count() == before + 1
+
+
+def test_misaligned_arguments_rejected(S):
+    import torch
+    from paper_2305_00515_b200 import api
+    d_in, pitch = api.alloc_input(64, 16)
+    out, op = api.alloc_planes(60, 12, ("gx",))
+    with pytest.raises(S.Error):  # pitch not a multiple of 16
+        api.launch(d_in, 65, 64, 16, S.make_stream_taps(), 1, out, op)
+    with pytest.raises(S.Error):  # output pitch below width-4
+        api.launch(d_in, pitch, 64, 16, S.make_stream_taps(), 1, out, 56)
+    del torch

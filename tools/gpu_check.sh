@@ -1,0 +1,19 @@
+#!/bin/bash
+# One gpurun call: GPU tests, smoke, bench, launch list + one ncu --set full
+# capture of the top kernel.  Outputs land in gpurun_out/.
+set -x
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > gpurun_out/gpu.txt
+(nproc; lscpu | grep -E "Model name|Socket|Thread") > gpurun_out/host.txt
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+if [ "${NCU:-1}" = "1" ]; then
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sobel5_stream_kernel -s 4 -c 1 \
+  -o gpurun_out/prof_sr -f python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
+fi
+tail -3 gpurun_out/pytest_gpu.log
+cat gpurun_out/bench.json
