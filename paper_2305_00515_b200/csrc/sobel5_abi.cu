@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "sobel5_gpu.h"
+#include "sobel5_packed.cuh"
 #include "sobel5_stream.cuh"
 
 using namespace sobel5_b200;
@@ -87,8 +88,10 @@ int choose_band(int out_w, int out_h, int frames) {
     if (forced > 0) return forced;
     const int64_t cols = (out_w + kCtaCols - 1) / kCtaCols;
     int band = 64;
-    // keep >= ~8 CTAs per SM worth of work where the image allows it
-    while (band > 16 && cols * frames * ((out_h + band - 1) / band) < 148 * 8) band /= 2;
+    // keep >= ~16 CTAs per SM (4 resident x 4 waves) so the last partial
+    // wave costs little; measured on B200 at 8K: band 16 154.5 us, 32
+    // 159.3 us, 64 161.0 us (tools/sweep.py)
+    while (band > 16 && cols * frames * ((out_h + band - 1) / band) < 148 * 16) band /= 2;
     return band;
 }
 
@@ -120,11 +123,41 @@ cudaError_t launch_one(const KernelParams& kp, dim3 grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <int PF, bool SEG>
+cudaError_t launch_packed(const KernelParams& kp, dim3 grid, cudaStream_t s) {
+    sobel5_packed_default_kernel<PF, SEG><<<grid, kCtaThreads, 0, s>>>(kp);
+    return cudaGetLastError();
+}
+
+// Prefetch depth of the packed kernel (rows of loads in flight ahead of the
+// row being processed); Prefetch::off maps to 0.
+int prefetch_depth(int prefetch) {
+    if (!prefetch) return 0;
+    const int d = env_int("SOBEL5_PF", 2);
+    return d < 1 ? 1 : (d > 4 ? 4 : d);
+}
+
+template <bool SEG>
+cudaError_t dispatch_packed(const KernelParams& kp, dim3 grid, int depth, cudaStream_t s) {
+    switch (depth) {
+        case 0: return launch_packed<0, SEG>(kp, grid, s);
+        case 1: return launch_packed<1, SEG>(kp, grid, s);
+        case 2: return launch_packed<2, SEG>(kp, grid, s);
+        case 3: return launch_packed<3, SEG>(kp, grid, s);
+        default: return launch_packed<4, SEG>(kp, grid, s);
+    }
+}
+
 cudaError_t dispatch(const KernelParams& kp, dim3 grid, int prefetch, bool dflt, MagMode mag,
                      cudaStream_t s) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (dflt && env_int("SOBEL5_GENERIC", 0) == 0) {
+        // default taps: packed two-pixels-per-register kernel (sobel5_packed.cuh)
+        const bool seg = kp.top_rows > 0 || kp.bot != nullptr;
+        return seg ? dispatch_packed<true>(kp, grid, prefetch_depth(prefetch), s)
+                   : dispatch_packed<false>(kp, grid, prefetch_depth(prefetch), s);
+    }
     if (dflt) {
-        // default taps always satisfy the uint32 magnitude bound
         return prefetch ? launch_one<1, DefaultTaps, kMagU32>(kp, grid, s)
                         : launch_one<0, DefaultTaps, kMagU32>(kp, grid, s);
     }

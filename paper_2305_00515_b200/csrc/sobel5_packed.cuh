@@ -1,0 +1,252 @@
+// sobel5_packed.cuh -- two-pixels-per-register variant of the fused kernel.
+//
+// Every stage of the operator is linear with integer coefficients, so two
+// pixels can share one 32-bit register as V = lo + hi * 2^16 (lo, hi signed):
+// IADD / IMAD-by-constant / LEA on V act on both lanes at once, and 32-bit
+// wrap-around is harmless because arithmetic mod 2^32 is a ring
+// homomorphism.  The lanes are recovered exactly at the end,
+//     lo = sext16(V),   hi = (V + 0x8000) >> 16 (arithmetic),
+// provided every EXTRACTED quantity lies in [-2^15, 2^15).  The host proves
+// that bound from the taps before selecting this kernel (choose_kernel in
+// sobel5_abi.cu); for the default (1, 2, 6, 4) taps the extracted maxima are
+// |gx|, |gy|, |gd|, |gdt| <= 12240 and |P|/2 <= 8925.
+//
+// Lane pairing: a lane owns output columns x0..x0+3 and packs pixel pairs
+// (x0, x0+2) and (x0+1, x0+3); the 5-tap window of pair A is E0..E4 and of
+// pair B E1..E5 with E_k = byte_k | byte_{k+2} << 16 of the 8-byte window.
+//
+// Default-taps algebra (make_stream_taps for (1,2,6,4), pipeline.hpp:82-92),
+// with s04 = p0+p4, s13 = p1+p3, D = p3-p1 (row_diff), d04 = p4-p0:
+//   F   = d04 + 2 D                      (Eq. 6, b = 2)
+//   H   = s04 + 4 s13 + 6 p2             (h = 1,4,6,4,1)
+//   K0  = -2 K0',  K0' = 3 (s04 + s13) + p2
+//   K1  = -2 K1',  K1' = s04 + 6 s13 + 8 p2
+//   gx  = F(v) + 4F(v+1) + 6F(v+2) + 4F(v+3) + F(v+4)          (Eq. 7)
+//   gy  = -H(v) - 2H(v+1) + 2H(v+3) + H(v+4)
+//   P   = -2 Q,  Q = K0'(v) + K1'(v+1) - K1'(v+3) - K0'(v+4)  (Eq. 14/15)
+//   M   =  2 N,  N = 3F(v)+3F(v+1)+F(v+2)+3F(v+3)+3F(v+4)
+//                    - 5D(v) + 6D(v+2) - 5D(v+4)              (Eq. 19/21)
+//   gd  = (P+M)/2 = N - Q,   gdt = (P-M)/2 = -N - Q           (Eq. 11)
+// P+M = 2(N-Q) is even by construction, so recover_diag's ParityViolation
+// (pipeline.hpp:268-273) cannot fire and needs no per-pixel check.
+#pragma once
+
+#include <cstdint>
+
+#include "sobel5_stream.cuh"
+
+namespace sobel5_b200 {
+
+__device__ __forceinline__ int32_t lane_lo(uint32_t v) {
+    return static_cast<int32_t>(static_cast<int16_t>(v & 0xffffu));
+}
+__device__ __forceinline__ int32_t lane_hi(uint32_t v) {
+    return static_cast<int32_t>(v + 0x8000u) >> 16;
+}
+
+// Default taps, packed.  PF = number of input rows whose loads are in flight
+// ahead of the row being processed (0 = Prefetch::off, >= 1 = on).
+// SEG = stacked three-segment input (row bands with halos) vs plain image.
+template <int PF, bool SEG>
+__global__ void __launch_bounds__(kCtaThreads, 4)
+    sobel5_packed_default_kernel(const __grid_constant__ KernelParams p) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int x0 = (blockIdx.x * kCtaWarps + warp) * kWarpCols + lane * 4;
+    if ((x0 - lane * 4) >= p.out_w) return;
+    const int oy0 = blockIdx.y * p.band;
+    const int n_out = min(p.band, p.out_h - oy0);
+    const int n_in = n_out + 4;
+    const int64_t in_frame = static_cast<int64_t>(blockIdx.z) * p.in_frame_stride;
+    const int64_t out_frame = static_cast<int64_t>(blockIdx.z) * p.out_frame_stride;
+    const bool load_a = x0 < p.width;
+    const bool load_b = lane == 31 && x0 + 4 < p.width;
+    const bool full = x0 + 3 < p.out_w;
+
+    // row pointer for plain images: advanced by one pitch per row
+    const uint8_t* plain = p.mid + in_frame + static_cast<int64_t>(oy0) * p.in_pitch + x0;
+    auto row_ptr = [&](int r) -> const uint8_t* {
+        if (SEG) return stacked_row(p, in_frame, oy0 + r) + x0;
+        return plain + static_cast<int64_t>(r) * p.in_pitch;
+    };
+    auto load_row = [&](int r, uint32_t& a, uint32_t& b) {
+        const uint8_t* rp = row_ptr(r);
+        a = load_a ? ld_row_word(rp) : 0u;
+        b = load_b ? ld_row_word(rp + 4) : 0u;
+    };
+
+    // pending accumulators [slot = output row mod 5][pair]
+    uint32_t ax[5][2], ay[5][2], an[5][2], aq[5][2];
+
+    constexpr int Q = PF > 0 ? PF : 1;
+    uint32_t qa[Q], qb[Q];
+    if (PF > 0) {
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+            if (k < n_in) load_row(k, qa[k], qb[k]);
+            else qa[k] = qb[k] = 0u;
+        }
+    }
+
+    for (int base = 0; base < n_in; base += 5) {
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+            const int r = base + s;
+            if (r >= n_in) break;
+            uint32_t wa, wb;
+            if (PF > 0) {
+                wa = qa[0];
+                wb = qb[0];
+#pragma unroll
+                for (int k = 0; k + 1 < Q; ++k) {
+                    qa[k] = qa[k + 1];
+                    qb[k] = qb[k + 1];
+                }
+                if (r + Q < n_in) load_row(r + Q, qa[Q - 1], qb[Q - 1]);
+            } else {
+                load_row(r, wa, wb);
+            }
+            // warp-shuffle column sharing
+            const uint32_t sh = __shfl_down_sync(0xffffffffu, wa, 1);
+            if (lane != 31) wb = sh;
+
+            // E_k = byte k | byte k+2 << 16
+            const uint32_t mid = __byte_perm(wa, wb, 0x5432);  // bytes 2,3,4,5
+            uint32_t e[6];
+            e[0] = __byte_perm(wa, 0u, 0x4240);
+            e[1] = __byte_perm(wa, 0u, 0x4341);
+            e[2] = __byte_perm(mid, 0u, 0x4240);
+            e[3] = __byte_perm(mid, 0u, 0x4341);
+            e[4] = __byte_perm(wb, 0u, 0x4240);
+            e[5] = __byte_perm(wb, 0u, 0x4341);
+
+            uint32_t F[2], H[2], D[2], K0[2], K1[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const uint32_t p0 = e[q], p1 = e[q + 1], p2 = e[q + 2], p3 = e[q + 3],
+                               p4 = e[q + 4];
+                const uint32_t s04 = p0 + p4, s13 = p1 + p3;
+                const uint32_t d = p3 - p1, d04 = p4 - p0;
+                D[q] = d;
+                F[q] = d04 + 2u * d;
+                H[q] = s04 + 4u * s13 + 6u * p2;
+                K0[q] = 3u * (s04 + s13) + p2;
+                K1[q] = s04 + 6u * s13 + 8u * p2;
+            }
+
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const uint32_t f = F[q], hh = H[q], d = D[q];
+                const uint32_t f3 = 3u * f;
+                const uint32_t na = f3 - 5u * d;  // i = 0, 4
+                const uint32_t nc = f + 6u * d;   // i = 2
+                // i = 0: open output row r
+                const int s0 = s;
+                ax[s0][q] = f;
+                ay[s0][q] = 0u - hh;
+                an[s0][q] = na;
+                aq[s0][q] = K0[q];
+                // i = 1
+                const int s1 = (s + 4) % 5;
+                ax[s1][q] += 4u * f;
+                ay[s1][q] -= 2u * hh;
+                an[s1][q] += f3;
+                aq[s1][q] += K1[q];
+                // i = 2
+                const int s2 = (s + 3) % 5;
+                ax[s2][q] += 6u * f;
+                an[s2][q] += nc;
+                // i = 3
+                const int s3 = (s + 2) % 5;
+                ax[s3][q] += 4u * f;
+                ay[s3][q] += 2u * hh;
+                an[s3][q] += f3;
+                aq[s3][q] -= K1[q];
+                // i = 4: closes output row r - 4
+                const int s4 = (s + 1) % 5;
+                ax[s4][q] += f;
+                ay[s4][q] += hh;
+                an[s4][q] += na;
+                aq[s4][q] -= K0[q];
+            }
+
+            if (r >= 4) {
+                const int sl = (s + 1) % 5;
+                const int v = r - 4;
+                int32_t gx[4], gy[4], gd[4], gdt[4];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const uint32_t vd = an[sl][q] - aq[sl][q];
+                    const uint32_t vt = 0u - an[sl][q] - aq[sl][q];
+                    // pair q holds pixels (q, q + 2)
+                    gx[q] = lane_lo(ax[sl][q]);
+                    gx[q + 2] = lane_hi(ax[sl][q]);
+                    gy[q] = lane_lo(ay[sl][q]);
+                    gy[q + 2] = lane_hi(ay[sl][q]);
+                    gd[q] = lane_lo(vd);
+                    gd[q + 2] = lane_hi(vd);
+                    gdt[q] = lane_lo(vt);
+                    gdt[q + 2] = lane_hi(vt);
+                }
+                const int64_t row_off = out_frame + static_cast<int64_t>(oy0 + v) * p.pitch + x0;
+                if (full) {
+                    if (p.gx) st_cs_v4(p.gx + row_off, gx[0], gx[1], gx[2], gx[3]);
+                    if (p.gy) st_cs_v4(p.gy + row_off, gy[0], gy[1], gy[2], gy[3]);
+                    if (p.gd) st_cs_v4(p.gd + row_off, gd[0], gd[1], gd[2], gd[3]);
+                    if (p.gdt) st_cs_v4(p.gdt + row_off, gdt[0], gdt[1], gdt[2], gdt[3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (x0 + j < p.out_w) {
+                            if (p.gx) p.gx[row_off + j] = gx[j];
+                            if (p.gy) p.gy[row_off + j] = gy[j];
+                            if (p.gd) p.gd[row_off + j] = gd[j];
+                            if (p.gdt) p.gdt[row_off + j] = gdt[j];
+                        }
+                    }
+                }
+                if (p.need_mag) {
+                    double g[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        // exact: every square < 2^28 and the sum < 2^32, so
+                        // double(S) equals the reference's double sum
+                        const uint32_t S = static_cast<uint32_t>(gx[j] * gx[j]) +
+                                           static_cast<uint32_t>(gy[j] * gy[j]) +
+                                           static_cast<uint32_t>(gd[j] * gd[j]) +
+                                           static_cast<uint32_t>(gdt[j] * gdt[j]);
+                        g[j] = __dsqrt_rn(__uint2double_rn(S));
+                    }
+                    if (full) {
+                        if (p.g) {
+                            st_cs_v2d(p.g + row_off, g[0], g[1]);
+                            st_cs_v2d(p.g + row_off + 2, g[2], g[3]);
+                        }
+                        if (p.g32)
+                            st_cs_v4f(p.g32 + row_off, __double2float_rn(g[0]),
+                                      __double2float_rn(g[1]), __double2float_rn(g[2]),
+                                      __double2float_rn(g[3]));
+                        if (p.u8) {
+                            const uint32_t qv = clamp_abs_u8(g[0]) | (clamp_abs_u8(g[1]) << 8) |
+                                                (clamp_abs_u8(g[2]) << 16) |
+                                                (clamp_abs_u8(g[3]) << 24);
+                            st_cs_u32(p.u8 + row_off, qv);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            if (x0 + j < p.out_w) {
+                                if (p.g) p.g[row_off + j] = g[j];
+                                if (p.g32) p.g32[row_off + j] = __double2float_rn(g[j]);
+                                if (p.u8)
+                                    p.u8[row_off + j] = static_cast<uint8_t>(clamp_abs_u8(g[j]));
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+}  // namespace sobel5_b200

@@ -1,0 +1,35 @@
+"""Kernel timing sweep over env knobs (SOBEL5_BAND, SOBEL5_PF, SOBEL5_GENERIC)."""
+import itertools, os, sys, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2305_00515_b200 import api
+
+w, h = int(os.environ.get("W", 7680)), int(os.environ.get("H", 4320))
+contract = os.environ.get("CONTRACT", "sr")
+planes_names = {"sr": ("gx", "gy", "gd", "gdt", "g"), "u8": ("u8",), "int": ("gx", "gy", "gd", "gdt")}[contract]
+outb = {"sr": 24, "u8": 1, "int": 16}[contract]
+taps = api.make_stream_taps()
+ins = []
+for i in range(6):
+    d, pitch = api.alloc_input(w, h)
+    api.synth_random_device(d, pitch, w, h, 1 + i)
+    ins.append(d)
+out, op = api.alloc_planes(w - 4, h - 4, planes_names)
+bands = [int(x) for x in os.environ.get("BANDS", "16,32,48,64,96,128").split(",")]
+pfs = [int(x) for x in os.environ.get("PFS", "1,2,3").split(",")]
+res = {}
+for band, pf in itertools.product(bands, pfs):
+    os.environ["SOBEL5_BAND"] = str(band)
+    os.environ["SOBEL5_PF"] = str(pf)
+    for i in range(5):
+        api.launch(ins[i % 6], pitch, w, h, taps, 1, out, op)
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    torch.cuda.synchronize(); e0.record()
+    N = 60
+    for i in range(N):
+        api.launch(ins[i % 6], pitch, w, h, taps, 1, out, op)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / N
+    b = w * h + (w - 4) * (h - 4) * outb
+    res[f"{band},{pf}"] = ms * 1e3
+    print(f"band={band:4d} pf={pf} {ms*1e3:7.1f} us {w*h/ms/1e6:7.1f} Gpx/s {b/ms/1e6:6.0f} GB/s", flush=True)
