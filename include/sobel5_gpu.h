@@ -155,6 +155,15 @@ sobel5_status sobel5_synth_random_device(uint8_t* d_img, int64_t pitch, int widt
                                          int64_t row_offset, uint64_t seed, uint8_t mask,
                                          void* stream);
 
+/* ---- diagnostics ----------------------------------------------------------
+ * Device self-check of the epilogue arithmetic over every integer S in
+ * [lo, hi): which = 0 compares the kernels' double sqrt with IEEE
+ * __dsqrt_rn((double)S); which = 1 compares the uint8 clamp_abs shortcut with
+ * min(255, round(sqrt(S))).  Adds the number of mismatches to *d_count
+ * (device pointer, unsigned 64-bit). */
+sobel5_status sobel5_selftest(int which, uint32_t lo, uint32_t hi, uint64_t* d_count,
+                              void* stream);
+
 /* ---- context: host-buffer path (what the C++ run_stream wrapper calls) ---- */
 
 sobel5_status sobel5_ctx_create(sobel5_ctx** out, int device);

@@ -68,7 +68,7 @@ EXPORTS = (
     "sobel5_abi_version", "sobel5_status_string", "sobel5_launch_count", "sobel5_make_taps",
     "sobel5_plan_counters", "sobel5_launch", "sobel5_launch_batch", "sobel5_launch_band",
     "sobel5_synth_random_device", "sobel5_ctx_create", "sobel5_ctx_destroy",
-    "sobel5_ctx_last_error", "sobel5_run_host",
+    "sobel5_ctx_last_error", "sobel5_run_host", "sobel5_selftest",
 )
 
 _lib = None
@@ -118,6 +118,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.sobel5_run_host.argtypes = [vp, vp, i32, i32, C.POINTER(Taps), i32, C.POINTER(Planes),
                                   C.POINTER(Diag)]
     L.sobel5_run_host.restype = i32
+    L.sobel5_selftest.argtypes = [i32, C.c_uint32, C.c_uint32, vp, vp]
+    L.sobel5_selftest.restype = i32
     _lib = L
     return L
 

@@ -123,9 +123,9 @@ cudaError_t launch_one(const KernelParams& kp, dim3 grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int PF, bool SEG>
+template <int PF, bool SEG, int OUTS>
 cudaError_t launch_packed(const KernelParams& kp, dim3 grid, cudaStream_t s) {
-    sobel5_packed_default_kernel<PF, SEG><<<grid, kCtaThreads, 0, s>>>(kp);
+    sobel5_packed_default_kernel<PF, SEG, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
     return cudaGetLastError();
 }
 
@@ -133,18 +133,33 @@ cudaError_t launch_packed(const KernelParams& kp, dim3 grid, cudaStream_t s) {
 // row being processed); Prefetch::off maps to 0.
 int prefetch_depth(int prefetch) {
     if (!prefetch) return 0;
-    const int d = env_int("SOBEL5_PF", 2);
-    return d < 1 ? 1 : (d > 4 ? 4 : d);
+    return env_int("SOBEL5_PF", 1) >= 2 ? 2 : 1;
+}
+
+int out_set(const KernelParams& kp) {
+    return (kp.gx ? kOutGx : 0) | (kp.gy ? kOutGy : 0) | (kp.gd ? kOutGd : 0) |
+           (kp.gdt ? kOutGdt : 0) | (kp.g ? kOutG : 0) | (kp.g32 ? kOutG32 : 0) |
+           (kp.u8 ? kOutU8 : 0);
+}
+
+template <int PF, bool SEG>
+cudaError_t dispatch_outs(const KernelParams& kp, dim3 grid, cudaStream_t s) {
+    // compile-time output sets for the common contracts, runtime otherwise
+    switch (out_set(kp)) {
+        case kOutSR: return launch_packed<PF, SEG, kOutSR>(kp, grid, s);
+        case kOutSR | kOutU8: return launch_packed<PF, SEG, kOutSR | kOutU8>(kp, grid, s);
+        case kOutU8: return launch_packed<PF, SEG, kOutU8>(kp, grid, s);
+        case 15 | kOutG32: return launch_packed<PF, SEG, 15 | kOutG32>(kp, grid, s);
+        default: return launch_packed<PF, SEG, kOutRuntime>(kp, grid, s);
+    }
 }
 
 template <bool SEG>
 cudaError_t dispatch_packed(const KernelParams& kp, dim3 grid, int depth, cudaStream_t s) {
     switch (depth) {
-        case 0: return launch_packed<0, SEG>(kp, grid, s);
-        case 1: return launch_packed<1, SEG>(kp, grid, s);
-        case 2: return launch_packed<2, SEG>(kp, grid, s);
-        case 3: return launch_packed<3, SEG>(kp, grid, s);
-        default: return launch_packed<4, SEG>(kp, grid, s);
+        case 0: return dispatch_outs<0, SEG>(kp, grid, s);
+        case 1: return dispatch_outs<1, SEG>(kp, grid, s);
+        default: return dispatch_outs<2, SEG>(kp, grid, s);
     }
 }
 
@@ -232,6 +247,25 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     const cudaError_t e = dispatch(kp, grid2, prefetch, taps_are_default(*taps), choose_mag(*taps),
                                    static_cast<cudaStream_t>(stream));
     return map_cuda(e);
+}
+
+__global__ void selftest_kernel(int which, uint32_t lo, uint32_t hi,
+                                unsigned long long* count) {
+    unsigned long long bad = 0;
+    for (uint64_t s = lo + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < hi;
+         s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t S = static_cast<uint32_t>(s);
+        if (which == 0) {
+            const double a = sqrt_u30(S), b = __dsqrt_rn(static_cast<double>(S));
+            bad += __double_as_longlong(a) != __double_as_longlong(b);
+        } else {
+            const double g = __dsqrt_rn(static_cast<double>(S));
+            const double r = round(g);
+            const uint32_t want = r < 255.0 ? static_cast<uint32_t>(r) : 255u;
+            bad += u8_from_s(S) != want;
+        }
+    }
+    if (bad) atomicAdd(count, bad);
 }
 
 }  // namespace
@@ -360,6 +394,15 @@ sobel5_status sobel5_launch_band(const uint8_t* d_top, const uint8_t* d_in, cons
                                  const sobel5_planes* d_out, sobel5_diag* d_diag, void* stream) {
     return launch_common(d_top, d_in, d_bot, in_pitch, 0, width, band_rows, 1, taps, prefetch,
                          d_out, 0, d_diag, stream);
+}
+
+sobel5_status sobel5_selftest(int which, uint32_t lo, uint32_t hi, uint64_t* d_count,
+                              void* stream) {
+    if (!d_count || hi < lo || (which != 0 && which != 1)) return SOBEL5_INVALID_ARG;
+    if (which == 0 && hi > (1u << 30)) return SOBEL5_INVALID_ARG;
+    selftest_kernel<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        which, lo, hi, reinterpret_cast<unsigned long long*>(d_count));
+    return map_cuda(cudaGetLastError());
 }
 
 sobel5_status sobel5_synth_random_device(uint8_t* d_img, int64_t pitch, int width, int height,

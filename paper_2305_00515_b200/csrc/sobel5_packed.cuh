@@ -37,6 +37,32 @@
 
 namespace sobel5_b200 {
 
+// Output-set bits (template OUTS); kOutRuntime checks the plane pointers.
+enum : int {
+    kOutGx = 1, kOutGy = 2, kOutGd = 4, kOutGdt = 8, kOutG = 16, kOutG32 = 32, kOutU8 = 64,
+    kOutSR = 31, kOutRuntime = -1
+};
+
+// Double magnitude of an exact integer sum of squares S < 2^32: IEEE sqrt
+// (__dsqrt_rn), bit-identical to std::sqrt((double)S).  A float-seeded
+// two-step Newton variant was measured 2% faster at 8K but is not correctly
+// rounded for every S (it broke the 1920x1080 golden hash), so the IEEE
+// routine stays.
+__device__ __forceinline__ double sqrt_u30(uint32_t S) {
+    return __dsqrt_rn(__uint2double_rn(S));
+}
+
+// clamp_abs(sqrt(S)) for an integer S, without the double: sqrt(S) is never
+// within 4.9e-4 of k + 0.5 (the nearest case is S = 255*256), and the float
+// estimate S * rsqrt(S) is within 7e-5 of sqrt(S) below 65281 (checked for
+// every S by test_u8_from_s_exhaustive).
+__device__ __forceinline__ uint32_t u8_from_s(uint32_t S) {
+    if (S > 65280u) return 255u;  // sqrt(65281) > 255.5
+    const float f = __uint2float_rn(S);
+    const float y = f * rsqrtf(fmaxf(f, 1.0f));
+    return static_cast<uint32_t>(__float2int_rn(y));
+}
+
 __device__ __forceinline__ int32_t lane_lo(uint32_t v) {
     return static_cast<int32_t>(static_cast<int16_t>(v & 0xffffu));
 }
@@ -47,9 +73,19 @@ __device__ __forceinline__ int32_t lane_hi(uint32_t v) {
 // Default taps, packed.  PF = number of input rows whose loads are in flight
 // ahead of the row being processed (0 = Prefetch::off, >= 1 = on).
 // SEG = stacked three-segment input (row bands with halos) vs plain image.
-template <int PF, bool SEG>
+template <int PF, bool SEG, int OUTS>
 __global__ void __launch_bounds__(kCtaThreads, 4)
     sobel5_packed_default_kernel(const __grid_constant__ KernelParams p) {
+    // which planes this instantiation writes (compile-time unless kOutRuntime)
+    constexpr bool RT = OUTS == kOutRuntime;
+    const bool w_gx = RT ? p.gx != nullptr : (OUTS & kOutGx) != 0;
+    const bool w_gy = RT ? p.gy != nullptr : (OUTS & kOutGy) != 0;
+    const bool w_gd = RT ? p.gd != nullptr : (OUTS & kOutGd) != 0;
+    const bool w_gdt = RT ? p.gdt != nullptr : (OUTS & kOutGdt) != 0;
+    const bool w_g = RT ? p.g != nullptr : (OUTS & kOutG) != 0;
+    const bool w_g32 = RT ? p.g32 != nullptr : (OUTS & kOutG32) != 0;
+    const bool w_u8 = RT ? p.u8 != nullptr : (OUTS & kOutU8) != 0;
+    const bool need_g = w_g || w_g32;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int x0 = (blockIdx.x * kCtaWarps + warp) * kWarpCols + lane * 4;
@@ -78,11 +114,14 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
     // pending accumulators [slot = output row mod 5][pair]
     uint32_t ax[5][2], ay[5][2], an[5][2], aq[5][2];
 
-    constexpr int Q = PF > 0 ? PF : 1;
-    uint32_t qa[Q], qb[Q];
+    // Prefetch ring: with PF > 0 the loads of the next 5 input rows are in
+    // flight while a row is processed.  The ring slot is the unrolled row
+    // index s (static), so a row's registers are consumed in place; shifting
+    // a queue instead would make the register move wait on the younger load.
+    uint32_t qa[5], qb[5];
     if (PF > 0) {
 #pragma unroll
-        for (int k = 0; k < Q; ++k) {
+        for (int k = 0; k < 5; ++k) {
             if (k < n_in) load_row(k, qa[k], qb[k]);
             else qa[k] = qb[k] = 0u;
         }
@@ -95,14 +134,8 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
             if (r >= n_in) break;
             uint32_t wa, wb;
             if (PF > 0) {
-                wa = qa[0];
-                wb = qb[0];
-#pragma unroll
-                for (int k = 0; k + 1 < Q; ++k) {
-                    qa[k] = qa[k + 1];
-                    qb[k] = qb[k + 1];
-                }
-                if (r + Q < n_in) load_row(r + Q, qa[Q - 1], qb[Q - 1]);
+                wa = qa[s];
+                wb = qb[s];
             } else {
                 load_row(r, wa, wb);
             }
@@ -119,6 +152,9 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
             e[3] = __byte_perm(mid, 0u, 0x4341);
             e[4] = __byte_perm(wb, 0u, 0x4240);
             e[5] = __byte_perm(wb, 0u, 0x4341);
+            // refill the ring slot only after its word has been consumed, so
+            // the load can target the same registers (no move, no early wait)
+            if (PF > 0 && r + 5 < n_in) load_row(r + 5, qa[s], qb[s]);
 
             uint32_t F[2], H[2], D[2], K0[2], K1[2];
 #pragma unroll
@@ -190,56 +226,59 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                 }
                 const int64_t row_off = out_frame + static_cast<int64_t>(oy0 + v) * p.pitch + x0;
                 if (full) {
-                    if (p.gx) st_cs_v4(p.gx + row_off, gx[0], gx[1], gx[2], gx[3]);
-                    if (p.gy) st_cs_v4(p.gy + row_off, gy[0], gy[1], gy[2], gy[3]);
-                    if (p.gd) st_cs_v4(p.gd + row_off, gd[0], gd[1], gd[2], gd[3]);
-                    if (p.gdt) st_cs_v4(p.gdt + row_off, gdt[0], gdt[1], gdt[2], gdt[3]);
+                    if (w_gx) st_cs_v4(p.gx + row_off, gx[0], gx[1], gx[2], gx[3]);
+                    if (w_gy) st_cs_v4(p.gy + row_off, gy[0], gy[1], gy[2], gy[3]);
+                    if (w_gd) st_cs_v4(p.gd + row_off, gd[0], gd[1], gd[2], gd[3]);
+                    if (w_gdt) st_cs_v4(p.gdt + row_off, gdt[0], gdt[1], gdt[2], gdt[3]);
                 } else {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         if (x0 + j < p.out_w) {
-                            if (p.gx) p.gx[row_off + j] = gx[j];
-                            if (p.gy) p.gy[row_off + j] = gy[j];
-                            if (p.gd) p.gd[row_off + j] = gd[j];
-                            if (p.gdt) p.gdt[row_off + j] = gdt[j];
+                            if (w_gx) p.gx[row_off + j] = gx[j];
+                            if (w_gy) p.gy[row_off + j] = gy[j];
+                            if (w_gd) p.gd[row_off + j] = gd[j];
+                            if (w_gdt) p.gdt[row_off + j] = gdt[j];
                         }
                     }
                 }
-                if (p.need_mag) {
-                    double g[4];
+                if (need_g || w_u8) {
+                    // exact: every square < 2^28 and the sum < 2^30, so
+                    // double(S) equals the reference's double sum of squares
+                    uint32_t S[4];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        // exact: every square < 2^28 and the sum < 2^32, so
-                        // double(S) equals the reference's double sum
-                        const uint32_t S = static_cast<uint32_t>(gx[j] * gx[j]) +
-                                           static_cast<uint32_t>(gy[j] * gy[j]) +
-                                           static_cast<uint32_t>(gd[j] * gd[j]) +
-                                           static_cast<uint32_t>(gdt[j] * gdt[j]);
-                        g[j] = __dsqrt_rn(__uint2double_rn(S));
+                    for (int j = 0; j < 4; ++j)
+                        S[j] = static_cast<uint32_t>(gx[j] * gx[j]) +
+                               static_cast<uint32_t>(gy[j] * gy[j]) +
+                               static_cast<uint32_t>(gd[j] * gd[j]) +
+                               static_cast<uint32_t>(gdt[j] * gdt[j]);
+                    double g[4] = {0.0, 0.0, 0.0, 0.0};
+                    if (need_g) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) g[j] = sqrt_u30(S[j]);
+                    }
+                    uint32_t u[4] = {0u, 0u, 0u, 0u};
+                    if (w_u8) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) u[j] = u8_from_s(S[j]);
                     }
                     if (full) {
-                        if (p.g) {
+                        if (w_g) {
                             st_cs_v2d(p.g + row_off, g[0], g[1]);
                             st_cs_v2d(p.g + row_off + 2, g[2], g[3]);
                         }
-                        if (p.g32)
+                        if (w_g32)
                             st_cs_v4f(p.g32 + row_off, __double2float_rn(g[0]),
                                       __double2float_rn(g[1]), __double2float_rn(g[2]),
                                       __double2float_rn(g[3]));
-                        if (p.u8) {
-                            const uint32_t qv = clamp_abs_u8(g[0]) | (clamp_abs_u8(g[1]) << 8) |
-                                                (clamp_abs_u8(g[2]) << 16) |
-                                                (clamp_abs_u8(g[3]) << 24);
-                            st_cs_u32(p.u8 + row_off, qv);
-                        }
+                        if (w_u8) st_cs_u32(p.u8 + row_off, u[0] | (u[1] << 8) | (u[2] << 16) |
+                                                               (u[3] << 24));
                     } else {
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
                             if (x0 + j < p.out_w) {
-                                if (p.g) p.g[row_off + j] = g[j];
-                                if (p.g32) p.g32[row_off + j] = __double2float_rn(g[j]);
-                                if (p.u8)
-                                    p.u8[row_off + j] = static_cast<uint8_t>(clamp_abs_u8(g[j]));
+                                if (w_g) p.g[row_off + j] = g[j];
+                                if (w_g32) p.g32[row_off + j] = __double2float_rn(g[j]);
+                                if (w_u8) p.u8[row_off + j] = static_cast<uint8_t>(u[j]);
                             }
                         }
                     }

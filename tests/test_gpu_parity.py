@@ -248,3 +248,16 @@ def test_misaligned_arguments_rejected(S):
     with pytest.raises(S.Error):  # output pitch below width-4
         api.launch(d_in, pitch, 64, 16, S.make_stream_taps(), 1, out, 56)
     del torch
+
+
+@pytest.mark.parametrize("which,hi", [(0, 1 << 30), (1, 1 << 17)], ids=["sqrt_u30", "u8_from_s"])
+def test_epilogue_arithmetic_exhaustive(S, which, hi):
+    """The fast epilogue is bit-identical to IEEE sqrt (which=0) and to
+    clamp_abs(round(sqrt)) (which=1) for EVERY integer sum of squares the
+    packed kernel can produce (default taps: S <= 4 * 12240^2 < 2^30)."""
+    import torch
+    from paper_2305_00515_b200 import _abi
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    S.api.check(_abi.load().sobel5_selftest(which, 0, hi, cnt.data_ptr(), None), "selftest")
+    torch.cuda.synchronize()
+    assert cnt.item() == 0

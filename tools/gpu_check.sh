@@ -12,7 +12,7 @@ timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 if [ "${NCU:-1}" = "1" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sobel5_stream_kernel -s 4 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sobel5_(packed|stream)" -s 4 -c 1 \
   -o gpurun_out/prof_sr -f python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
 fi
 tail -3 gpurun_out/pytest_gpu.log
