@@ -1,0 +1,34 @@
+"""The drop-in C++ API (include/sobel5_b200/*.hpp) through its own test
+program tests/cpp/test_api.cpp: host-side checks on CPU, run_stream on GPU."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+EXE = os.path.join(ROOT, "build", "test_api")
+
+
+@pytest.fixture(scope="module")
+def exe():
+    from paper_2305_00515_b200 import _abi
+    _abi.load()  # builds the .so in-tree if missing
+    srcs = [os.path.join(ROOT, "tests", "cpp", "test_api.cpp")] + [
+        os.path.join(ROOT, "include", "sobel5_b200", f)
+        for f in os.listdir(os.path.join(ROOT, "include", "sobel5_b200"))]
+    if not os.path.exists(EXE) or any(os.path.getmtime(s) > os.path.getmtime(EXE) for s in srcs):
+        subprocess.run(["bash", os.path.join(ROOT, "tools", "build_cpp.sh")], check=True)
+    return EXE
+
+
+def test_cpp_api_host(exe):
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_api_gpu(exe, cuda):
+    r = subprocess.run([exe, "--gpu"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout

@@ -1,0 +1,8 @@
+#!/bin/bash
+# Builds the C++ API test against the drop-in headers and the in-tree .so.
+set -e
+ROOT="$(cd "$(dirname "$0")/.." && pwd)"
+mkdir -p "$ROOT/build"
+LIB="$ROOT/paper_2305_00515_b200/lib"
+${CXX:-g++} -std=c++20 -O2 -Wall -Wextra -I"$ROOT/include" "$ROOT/tests/cpp/test_api.cpp" \
+  -L"$LIB" -lsobel5_b200 -Wl,-rpath,"$LIB" -o "$ROOT/build/test_api"

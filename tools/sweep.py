@@ -15,12 +15,12 @@ for i in range(6):
     api.synth_random_device(d, pitch, w, h, 1 + i)
     ins.append(d)
 out, op = api.alloc_planes(w - 4, h - 4, planes_names)
-bands = [int(x) for x in os.environ.get("BANDS", "16,32,48,64,96,128").split(",")]
-pfs = [int(x) for x in os.environ.get("PFS", "1,2,3").split(",")]
+bands = [int(x) for x in os.environ.get("BANDS", "0").split(",")]
+pfs = [int(x) for x in os.environ.get("OCCS", "0").split(",")]  # CTAs per SM (0 = occupancy)
 res = {}
 for band, pf in itertools.product(bands, pfs):
     os.environ["SOBEL5_BAND"] = str(band)
-    os.environ["SOBEL5_PF"] = str(pf)
+    os.environ["SOBEL5_CTAS_PER_SM"] = str(pf)
     for i in range(5):
         api.launch(ins[i % 6], pitch, w, h, taps, 1, out, op)
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
@@ -32,4 +32,4 @@ for band, pf in itertools.product(bands, pfs):
     ms = e0.elapsed_time(e1) / N
     b = w * h + (w - 4) * (h - 4) * outb
     res[f"{band},{pf}"] = ms * 1e3
-    print(f"band={band:4d} pf={pf} {ms*1e3:7.1f} us {w*h/ms/1e6:7.1f} Gpx/s {b/ms/1e6:6.0f} GB/s", flush=True)
+    print(f"band={band:4d} occ={pf} {ms*1e3:7.1f} us {w*h/ms/1e6:7.1f} Gpx/s {b/ms/1e6:6.0f} GB/s", flush=True)
