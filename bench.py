@@ -42,6 +42,9 @@ WORKLOADS = {
     "4k": dict(w=3840, h=2160, frames=1, name="3840x2160 uint8 single image (BASELINE C2)"),
     "1080p-batch": dict(w=1920, h=1080, frames=256,
                         name="batch of 256 1920x1080 uint8 frames split across ranks (C4)"),
+    "32k-bands": dict(w=32768, h=32768, frames=1,
+                      name="32768x32768 uint8 single image row-band partitioned across ranks "
+                           "with 2-row halos (C5)"),
 }
 
 
@@ -54,6 +57,8 @@ def parse():
     ap.add_argument("--workload", default="8k", choices=sorted(WORKLOADS))
     ap.add_argument("--contract", default="sr", choices=sorted(OUT_BYTES))
     ap.add_argument("--prefetch", type=int, default=1)
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl", "gloo"],
+                    help="32k-bands halo transport")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -255,28 +260,52 @@ def main():
     stream = torch.cuda.current_stream(dev)
     s_ptr = stream.cuda_stream
 
-    # Inputs: rotate over enough frames that the input set exceeds L2 (126 MB);
-    # the outputs alone (24 B/px) are 6x L2 at 8K.
-    in_bytes = w * h * frames
-    n_in = max(2, int(np.ceil(2 * 126e6 / in_bytes)))
-    n_in = min(n_in, 8)
-    ins = []
-    for i in range(n_in):
-        d, pitch = api.alloc_input(w, h, dev, frames=frames)
-        for f in range(frames):
-            sub = d[f] if frames > 1 else d
-            api.synth_random_device(sub, pitch, w, h, seed=1 + i * frames + f, stream=s_ptr)
-        ins.append(d)
-    out, op = api.alloc_planes(ow, oh, planes_names, dev, frames=frames)
-    torch.cuda.synchronize()
+    scaling = "weak"
+    if a.workload == "32k-bands":
+        # C5: one 32768^2 image row-band partitioned over the ranks (strong
+        # scaling); halos from the neighbours via peer-mapped buffers read
+        # inside the kernel (default) or NCCL send/recv (--transport nccl)
+        from paper_2305_00515_b200.bands import RowBandPartition, plan_bands
+        scaling = "strong"
+        plan = plan_bands(w, h, world, rank)
+        body, pitch = api.alloc_input(w, plan.body_rows, dev)
+        api.synth_random_device(body, pitch, w, plan.body_rows, seed=1, row_offset=plan.r0,
+                                stream=s_ptr)
+        torch.cuda.synchronize()
+        part = RowBandPartition(plan, body, pitch, transport=a.transport)
+        out, op = api.alloc_planes(ow, plan.out_rows, planes_names, dev)
+        n_in, in_bytes = 1, w * plan.body_rows
+        px_job = w * h
+        rank_in_px, rank_out_px = w * plan.body_rows, ow * plan.out_rows
 
-    def step(i):
-        d = ins[i % n_in]
-        if frames > 1:
-            api.launch_batch(d, pitch, h * pitch, w, h, frames, taps, a.prefetch, out, op,
-                             oh * op, stream=s_ptr)
-        else:
-            api.launch(d, pitch, w, h, taps, a.prefetch, out, op, stream=s_ptr)
+        def step(i):
+            part.run(taps, out, op, a.prefetch, stream=s_ptr)
+    else:
+        # Inputs: rotate over enough frames that the input set exceeds L2
+        # (126 MB); the outputs alone (24 B/px) are 6x L2 at 8K.
+        in_bytes = w * h * frames
+        n_in = max(2, int(np.ceil(2 * 126e6 / in_bytes)))
+        n_in = min(n_in, 8)
+        ins = []
+        for i in range(n_in):
+            d, pitch = api.alloc_input(w, h, dev, frames=frames)
+            for f in range(frames):
+                sub = d[f] if frames > 1 else d
+                api.synth_random_device(sub, pitch, w, h, seed=1 + (rank * frames + f) + i * 1000,
+                                        stream=s_ptr)
+            ins.append(d)
+        out, op = api.alloc_planes(ow, oh, planes_names, dev, frames=frames)
+        px_job = w * h * frames * world
+        rank_in_px, rank_out_px = w * h * frames, ow * oh * frames
+
+        def step(i):
+            d = ins[i % n_in]
+            if frames > 1:
+                api.launch_batch(d, pitch, h * pitch, w, h, frames, taps, a.prefetch, out, op,
+                                 oh * op, stream=s_ptr)
+            else:
+                api.launch(d, pitch, w, h, taps, a.prefetch, out, op, stream=s_ptr)
+    torch.cuda.synchronize()
 
     for i in range(a.warmup):
         step(i)
@@ -303,11 +332,10 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ms_step = ms / a.steps
-    px_step = w * h * frames
-    value = px_step * world / (ms_step * 1e-3) / 1e9
+    value = px_job / (ms_step * 1e-3) / 1e9
 
     hbm_peak, peak_kind, peaks = measured_peaks()
-    alg_bytes = px_step + ow * oh * frames * OUT_BYTES[a.contract]
+    alg_bytes = rank_in_px + rank_out_px * OUT_BYTES[a.contract]  # per rank, per launch set
     achieved = alg_bytes / (ms_step * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -321,7 +349,7 @@ def main():
 
     # ---- variants (same workload, other output contracts / prefetch off) ----
     variants = {}
-    if rank == 0 and frames == 1:
+    if rank == 0 and frames == 1 and a.workload != "32k-bands":
         for name, contract, pf in (("u8", "u8", 1), ("sr32", "sr32", 1), ("sr_prefetch_off",
                                                                           "sr", 0)):
             if contract == a.contract and pf == a.prefetch:
@@ -347,7 +375,7 @@ def main():
 
     # ---- e2e through the C ABI host entry with pinned buffers ----
     e2e = None
-    if rank == 0 and not a.no_e2e and frames == 1:
+    if rank == 0 and not a.no_e2e and frames == 1 and a.workload != "32k-bands":
         import ctypes as C
         ctx = api.Context(local)
         h_in = torch.empty((h, w), dtype=torch.uint8, pin_memory=True)
@@ -389,11 +417,13 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic (synth_random seed 1+i generated on device, reference generator)",
+            "scaling": scaling, "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (synth_random generated on device, reference generator)",
             "config": {"workload": wl["name"], "frames_per_rank": frames,
                        "contract": a.contract + " (" + "+".join(planes_names) + ")",
-                       "prefetch": bool(a.prefetch), "parallelism": f"batch-split x{world}",
+                       "prefetch": bool(a.prefetch),
+                       "parallelism": (f"row-bands x{world} ({a.transport} halos)"
+                                       if a.workload == "32k-bands" else f"batch-split x{world}"),
                        "l2": f"inputs rotated over {n_in} buffers ({n_in * in_bytes / 1e6:.0f} MB)"
                              f" + {ow * oh * frames * OUT_BYTES[a.contract] / 1e6:.0f} MB of "
                              "outputs per step, both > 126 MB L2",

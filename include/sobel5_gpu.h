@@ -155,6 +155,21 @@ sobel5_status sobel5_synth_random_device(uint8_t* d_img, int64_t pitch, int widt
                                          int64_t row_offset, uint64_t seed, uint8_t mask,
                                          void* stream);
 
+/* ---- peer (CUDA IPC) mapping for row bands across GPUs -------------------
+ * One rank exports the device buffer of its band; a neighbour imports it and
+ * passes the imported pointer (plus row offsets) as d_top / d_bot of
+ * sobel5_launch_band, so the 2-row halos are read over NVLink inside the
+ * kernel.  d_ptr may point anywhere inside an allocation. */
+typedef struct sobel5_ipc_handle {
+    unsigned char bytes[64]; /* cudaIpcMemHandle_t of the containing allocation */
+    int64_t offset;          /* byte offset of the exported pointer inside it */
+} sobel5_ipc_handle;
+
+sobel5_status sobel5_ipc_export(const void* d_ptr, sobel5_ipc_handle* out);
+/* Maps a peer's exported buffer into this process (current device). */
+sobel5_status sobel5_ipc_import(const sobel5_ipc_handle* h, const void** d_ptr);
+sobel5_status sobel5_ipc_release(const void* d_ptr);
+
 /* ---- diagnostics ----------------------------------------------------------
  * Device self-check of the epilogue arithmetic over every integer S in
  * [lo, hi): which = 0 compares the kernels' double sqrt with IEEE

@@ -52,6 +52,10 @@ class Diag(C.Structure):
                 ("reserved", C.c_int32)]
 
 
+class IpcHandle(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 64), ("offset", C.c_int64)]
+
+
 class Counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "row_conv5_f", "row_conv5_h", "row_conv5_k0", "row_conv5_k1",
@@ -68,7 +72,8 @@ EXPORTS = (
     "sobel5_abi_version", "sobel5_status_string", "sobel5_launch_count", "sobel5_make_taps",
     "sobel5_plan_counters", "sobel5_launch", "sobel5_launch_batch", "sobel5_launch_band",
     "sobel5_synth_random_device", "sobel5_ctx_create", "sobel5_ctx_destroy",
-    "sobel5_ctx_last_error", "sobel5_run_host", "sobel5_selftest",
+    "sobel5_ctx_last_error", "sobel5_run_host", "sobel5_selftest", "sobel5_ipc_export",
+    "sobel5_ipc_import", "sobel5_ipc_release",
 )
 
 _lib = None
@@ -118,6 +123,12 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.sobel5_run_host.argtypes = [vp, vp, i32, i32, C.POINTER(Taps), i32, C.POINTER(Planes),
                                   C.POINTER(Diag)]
     L.sobel5_run_host.restype = i32
+    L.sobel5_ipc_export.argtypes = [vp, C.POINTER(IpcHandle)]
+    L.sobel5_ipc_export.restype = i32
+    L.sobel5_ipc_import.argtypes = [C.POINTER(IpcHandle), C.POINTER(vp)]
+    L.sobel5_ipc_import.restype = i32
+    L.sobel5_ipc_release.argtypes = [vp]
+    L.sobel5_ipc_release.restype = i32
     L.sobel5_selftest.argtypes = [i32, C.c_uint32, C.c_uint32, vp, vp]
     L.sobel5_selftest.restype = i32
     _lib = L

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libsobel5_b200.so")
-SOURCES = ["sobel5_abi.cu", "sobel5_ctx.cu"]
+SOURCES = ["sobel5_abi.cu", "sobel5_ctx.cu", "sobel5_ipc.cu"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
