@@ -119,12 +119,19 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
     // index s (static), so a row's registers are consumed in place; shifting
     // a queue instead would make the register move wait on the younger load.
     uint32_t qa[5], qb[5];
+    // (cur_a, cur_b): the next row's 8-byte window, already shuffled.  The
+    // shuffle for row r+1 is issued while row r is computed, so its latency
+    // is off the critical path (profiled: SHFL + SEL were 26% of stalls).
+    uint32_t cur_a = 0u, cur_b = 0u;
     if (PF > 0) {
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
             if (k < n_in) load_row(k, qa[k], qb[k]);
             else qa[k] = qb[k] = 0u;
         }
+        cur_a = qa[0];
+        const uint32_t sh0 = __shfl_down_sync(0xffffffffu, cur_a, 1);
+        cur_b = lane != 31 ? sh0 : qb[0];
     }
 
     for (int base = 0; base < n_in; base += 5) {
@@ -134,14 +141,14 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
             if (r >= n_in) break;
             uint32_t wa, wb;
             if (PF > 0) {
-                wa = qa[s];
-                wb = qb[s];
+                wa = cur_a;
+                wb = cur_b;
             } else {
                 load_row(r, wa, wb);
+                // warp-shuffle column sharing
+                const uint32_t sh = __shfl_down_sync(0xffffffffu, wa, 1);
+                if (lane != 31) wb = sh;
             }
-            // warp-shuffle column sharing
-            const uint32_t sh = __shfl_down_sync(0xffffffffu, wa, 1);
-            if (lane != 31) wb = sh;
 
             // E_k = byte k | byte k+2 << 16
             const uint32_t mid = __byte_perm(wa, wb, 0x5432);  // bytes 2,3,4,5
@@ -154,7 +161,14 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
             e[5] = __byte_perm(wb, 0u, 0x4341);
             // refill the ring slot only after its word has been consumed, so
             // the load can target the same registers (no move, no early wait)
-            if (PF > 0 && r + 5 < n_in) load_row(r + 5, qa[s], qb[s]);
+            if (PF > 0) {
+                if (r + 5 < n_in) load_row(r + 5, qa[s], qb[s]);
+                // warp-shuffle column sharing for row r+1
+                const int sn = (s + 1) % 5;
+                cur_a = qa[sn];
+                const uint32_t shn = __shfl_down_sync(0xffffffffu, cur_a, 1);
+                cur_b = lane != 31 ? shn : qb[sn];
+            }
 
             uint32_t F[2], H[2], D[2], K0[2], K1[2];
 #pragma unroll
@@ -263,8 +277,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                     }
                     if (full) {
                         if (w_g) {
-                            st_cs_v2d(p.g + row_off, g[0], g[1]);
-                            st_cs_v2d(p.g + row_off + 2, g[2], g[3]);
+                            st_cs_v4d(p.g + row_off, g[0], g[1], g[2], g[3]);
                         }
                         if (w_g32)
                             st_cs_v4f(p.g32 + row_off, __double2float_rn(g[0]),

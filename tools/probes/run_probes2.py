@@ -1,0 +1,47 @@
+"""Write-bandwidth probes (store width, cache hint, per-warp contiguity)."""
+import os, subprocess
+import numpy as np, torch
+from cuda.bindings import driver as cu
+HERE = os.path.dirname(os.path.abspath(__file__))
+cub = "/tmp/p2.cubin"
+subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-cubin", "-o", cub,
+                os.path.join(HERE, "store_probe2.cu")], check=True)
+torch.zeros(1, device="cuda")
+err, mod = cu.cuModuleLoad(cub.encode())
+def fn(name):
+    e, f = cu.cuModuleGetFunction(mod, name.encode()); assert e == cu.CUresult.CUDA_SUCCESS, (name, e); return f
+def launch(f, grid, block, args):
+    vals = [np.array(v, dtype=t) for v, t in args]
+    ptrs = np.array([v.ctypes.data for v in vals], dtype=np.uint64)
+    e, = cu.cuLaunchKernel(f, *grid, *block, 0, torch.cuda.current_stream().cuda_stream, ptrs.ctypes.data, 0)
+    assert e == cu.CUresult.CUDA_SUCCESS, e
+def timeit(g, n=30):
+    for _ in range(3): g()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    torch.cuda.synchronize(); e0.record()
+    for _ in range(n): g()
+    e1.record(); torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n * 1e3
+W, H = 7676, 4316
+pitch = (W + 31) // 32 * 32
+byts = W * H * 24
+buf = torch.empty(byts + (1 << 20), dtype=torch.uint8, device="cuda")
+for vec in (16, 32):
+    for hint in (0, 1, 2):
+        for blocks in (148 * 8, 148 * 32):
+            f = fn(f"_Z4flatILi{vec}ELi{hint}EEvPcl")
+            us = timeit(lambda: launch(f, (blocks, 1, 1), (256, 1, 1), [(buf.data_ptr(), np.uint64), (byts, np.int64)]))
+            print(f"flat vec={vec} hint={hint} blocks={blocks}: {us:.1f} us {byts/us/1e3:.0f} GB/s", flush=True)
+del buf
+pl = [torch.empty((H, pitch * 4), dtype=torch.uint8, device="cuda") for _ in range(4)]
+g = torch.empty((H, pitch * 8), dtype=torch.uint8, device="cuda")
+for px, vec, hint in ((4, 16, 0), (4, 16, 1), (4, 16, 2), (8, 16, 0), (8, 16, 1), (8, 32, 0), (8, 32, 1), (8, 32, 2)):
+    f = fn(f"_Z6planesILi{px}ELi{vec}ELi{hint}EEvPcS0_S0_S0_S0_liii")
+    for band in (16, 32):
+        cols = 128 * px
+        args = [(p.data_ptr(), np.uint64) for p in pl] + [(g.data_ptr(), np.uint64), (pitch, np.int64),
+                (W, np.int32), (H, np.int32), (band, np.int32)]
+        us = timeit(lambda: launch(f, ((W + cols - 1) // cols, (H + band - 1) // band, 1), (128, 1, 1), args))
+        print(f"planes px={px} vec={vec} hint={hint} band={band}: {us:.1f} us {byts/us/1e3:.0f} GB/s", flush=True)
+t = torch.empty(byts // 4, dtype=torch.int32, device="cuda")
+us = timeit(lambda: t.fill_(3)); print(f"torch fill_: {us:.1f} us {byts/us/1e3:.0f} GB/s")
