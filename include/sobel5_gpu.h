@@ -42,7 +42,8 @@ typedef enum sobel5_status {
     SOBEL5_NON_POSITIVE_PARAM = 7,  /* NonPositiveParam  filter_algebra.hpp:158 */
     SOBEL5_PARAM_OVERFLOW = 8,      /* ParamOverflow     filter_algebra.hpp:185 */
     SOBEL5_LANE_TOO_NARROW = 9,     /* LaneTooNarrow     strips.hpp:40-42       */
-    SOBEL5_NO_DEVICE = 10           /* no CUDA device: the path never falls back */
+    SOBEL5_NO_DEVICE = 10,          /* no CUDA device: the path never falls back */
+    SOBEL5_EMPTY_PLANE = 11         /* EmptyPlane        image_io.hpp:280         */
 } sobel5_status;
 
 /* POD copy of sobel5::StreamTaps (pipeline.hpp:57-73).  The kernels honour
@@ -92,6 +93,29 @@ typedef struct sobel5_counters {
     uint64_t row_conv5_f, row_conv5_h, row_conv5_k0, row_conv5_k1;
     uint64_t row_diff, row_conv3_f, row_conv3_h, mac;
 } sobel5_counters;
+
+/* Per-frame scratch of the normalize export (image_io.hpp:242-255).
+ * minmax: order-preserving keys of the smallest / largest value
+ * (key(v) = bits(v) ^ (v < 0 ? ~0 : 1 << 63) for a double v, compared as
+ * unsigned 64-bit integers); filled by pass 1, initialised by the library.  norm_table: the exact
+ * piecewise-constant map S -> u8 of pass 2 for integer sums of squares
+ * (thr[k] = smallest S whose normalized value is >= k), plus a float
+ * estimate (lo_f, scale_f) used to seed the lookup. */
+typedef struct sobel5_minmax {
+    uint64_t lo_key;
+    uint64_t hi_key;
+} sobel5_minmax;
+
+typedef struct sobel5_norm_table {
+    double lo;          /* min g */
+    double span;        /* max g - min g */
+    float lo_f;         /* (float) lo */
+    float scale_f;      /* (float) (255 / span), 0 if span <= 0 */
+    uint32_t exact_s;   /* 1: thresholds valid (integer S), 0: use lo/span directly */
+    uint32_t pad_;
+    uint32_t thr[257];  /* thr[0] = 0, thr[256] = UINT32_MAX */
+    uint32_t pad2_[3];
+} sobel5_norm_table;
 
 typedef struct sobel5_ctx sobel5_ctx; /* opaque: device, streams, buffers */
 
@@ -148,6 +172,40 @@ sobel5_status sobel5_launch_band(const uint8_t* d_top, const uint8_t* d_in, cons
                                  const sobel5_taps* taps, int prefetch,
                                  const sobel5_planes* d_out, sobel5_diag* d_diag, void* stream);
 
+/* ---- detect path (sobel5_cli.cpp:127-189) ---------
+ * pad = 1 fuses pad_replicate(img, 2) (image_io.hpp:279-291) into the
+ * stencil's loads: the planes are then width x height (same size as the
+ * input) and equal run_stream(pad_replicate(img, 2).plane, ...); an empty
+ * image gives SOBEL5_EMPTY_PLANE.  pad = 0 is sobel5_launch_batch. */
+sobel5_status sobel5_launch_ex(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
+                               int width, int height, int n_frames, const sobel5_taps* taps,
+                               int prefetch, int pad, const sobel5_planes* d_out,
+                               int64_t out_frame_stride, sobel5_diag* d_diag, void* stream);
+
+/* Bytes of device scratch sobel5_detect / sobel5_quantize_plane need
+ * (16-byte aligned; normalize only). */
+size_t sobel5_detect_scratch_bytes(int n_frames);
+
+/* The detect export: u8 = quantize(g, save_mode) (image_io.hpp:233-256) of
+ * the (optionally padded) image; save_mode 0 = clamp_abs, 1 = normalize
+ * (the CLI default, sobel5_cli.cpp:177).  d_out->u8 is required; any other
+ * non-NULL plane of d_out is written too (the --dump-planes source).
+ * normalize runs pass 1 (planes + per-frame min/max of g), a threshold
+ * table, and pass 2 (u8 through the table); bit-exact with the reference's
+ * double arithmetic. */
+sobel5_status sobel5_detect(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
+                            int width, int height, int n_frames, const sobel5_taps* taps,
+                            int prefetch, int pad, int save_mode, const sobel5_planes* d_out,
+                            int64_t out_frame_stride, void* d_scratch, sobel5_diag* d_diag,
+                            void* stream);
+
+/* detail::quantize of a device plane (save_plane, image_io.hpp:258-268):
+ * kind 0 = RealPlane (double), 1 = SignedPlane (int32); pitch in elements,
+ * u8_pitch in bytes; save_mode as above. */
+sobel5_status sobel5_quantize_plane(const void* d_plane, int kind, int64_t pitch, int width,
+                                    int height, int save_mode, uint8_t* d_u8, int64_t u8_pitch,
+                                    void* d_scratch, void* stream);
+
 /* synth_random (synth.hpp:20-35) generated on the device, optionally masked
  * (SURVEY.md section 8d inputs).  Pixel i of row-major order is byte i%8 of
  * splitmix64 word i/8; row_offset lets a band generate its slice. */
@@ -194,6 +252,39 @@ const char* sobel5_ctx_last_error(const sobel5_ctx* ctx);
 sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
                               const sobel5_taps* taps, int prefetch, const sobel5_planes* h_out,
                               sobel5_diag* diag_out);
+
+/* ---- the classic 3x3 two-direction operator ---------
+ * run_stream_3x3 (pipeline.hpp:551-573) / sobel3_2d (oracle.hpp:58-70):
+ * gx, gy int32 and g double (plus optional g32 / u8 clamp_abs) of a valid
+ * (W-2) x (H-2) output, or W x H with pad = 1 (pad_replicate(img, 1)).
+ * d_out->gd and ->gdt must be NULL.  Images below 3x3 give
+ * SOBEL5_IMAGE_TOO_SMALL (pipeline.hpp:553-556). */
+sobel5_status sobel3_launch(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
+                            int width, int height, int n_frames, int prefetch, int pad,
+                            const sobel5_planes* d_out, int64_t out_frame_stride, void* stream);
+
+/* Detect with --op sobel3_2d (sobel5_cli.cpp:128-149): u8 = quantize(g). */
+sobel5_status sobel3_detect(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
+                            int width, int height, int n_frames, int prefetch, int pad,
+                            int save_mode, const sobel5_planes* d_out, int64_t out_frame_stride,
+                            void* d_scratch, void* stream);
+
+/* OpCounters of run_stream_3x3 (pipeline.hpp:488-547) for a plan. */
+sobel5_status sobel3_plan_counters(int height, const int* strip_out_w, int n_strips, int prefetch,
+                                   sobel5_counters* out);
+
+/* Host-buffer run_stream_3x3: tightly packed planes (pitch == width-2). */
+sobel5_status sobel3_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
+                              int prefetch, const sobel5_planes* h_out);
+
+/* Host-buffer detect (what the CLI's detect command needs): tightly packed
+ * W x H input, h_u8 receives the (out_w x out_h) edge map, h_planes
+ * (nullable, pitch == out_w) any planes to dump.  out = W x H with pad = 1,
+ * (W-4) x (H-4) otherwise. */
+sobel5_status sobel5_detect_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
+                                 const sobel5_taps* taps, int prefetch, int pad, int save_mode,
+                                 uint8_t* h_u8, const sobel5_planes* h_planes,
+                                 sobel5_diag* diag_out);
 
 #ifdef __cplusplus
 }

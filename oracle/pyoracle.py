@@ -93,6 +93,14 @@ class Oracle:
                                              C.c_int, C.POINTER(Counters)]
         L.oracle_fnv1a64.argtypes = [C.c_void_p, C.c_size_t]
         L.oracle_fnv1a64.restype = C.c_uint64
+        L.oracle_pad_replicate.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        L.oracle_pad_replicate.restype = C.c_int
+        for fn in ("oracle_normalize_f64", "oracle_normalize_i32", "oracle_clamp_abs_i32"):
+            getattr(L, fn).argtypes = [C.c_void_p, C.c_size_t, C.c_void_p]
+        L.oracle_sobel3_2d.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 3
+        L.oracle_sobel3_2d.restype = C.c_int
+        L.oracle_stream3_counters.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_int,
+                                              C.POINTER(Counters)]
 
     def make_stream_taps(self, a=1, b=2, m=6, n=4) -> Taps:
         t = Taps()
@@ -150,6 +158,46 @@ class Oracle:
         a = np.ascontiguousarray(a)
         return int(self.lib.oracle_fnv1a64(_p(a), a.nbytes))
 
+    # ---- detect path ----
+    def pad_replicate(self, img: np.ndarray, r: int = 2):
+        """Returns (status, padded) -- status 0, 20 EmptyPlane, 19 DimMismatch."""
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        out = np.empty((max(h + 2 * r, 0), max(w + 2 * r, 0)), np.uint8)
+        st = self.lib.oracle_pad_replicate(_p(img), w, h, r, _p(out))
+        return st, (out if st == 0 else None)
+
+    def quantize(self, plane: np.ndarray, mode: str) -> np.ndarray:
+        """detail::quantize of a RealPlane (float64) or SignedPlane (int32)."""
+        out = np.empty(plane.shape, np.uint8)
+        if plane.dtype == np.float64:
+            plane = np.ascontiguousarray(plane)
+            if mode == "clamp_abs":
+                self.lib.oracle_clamp_abs_f64(_p(plane), plane.size, _p(out))
+            else:
+                self.lib.oracle_normalize_f64(_p(plane), plane.size, _p(out))
+        else:
+            plane = np.ascontiguousarray(plane, np.int32)
+            fn = "oracle_clamp_abs_i32" if mode == "clamp_abs" else "oracle_normalize_i32"
+            getattr(self.lib, fn)(_p(plane), plane.size, _p(out))
+        return out
+
+    def sobel3_2d(self, img: np.ndarray):
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        if w < 3 or h < 3:
+            return 1, None
+        o = {k: np.empty((h - 2, w - 2), np.int32) for k in ("gx", "gy")}
+        o["g"] = np.empty((h - 2, w - 2), np.float64)
+        st = self.lib.oracle_sobel3_2d(_p(img), w, h, _p(o["gx"]), _p(o["gy"]), _p(o["g"]))
+        return st, o
+
+    def stream3_counters(self, h, strip_widths, prefetch=True):
+        sw = np.ascontiguousarray(strip_widths, np.int32)
+        c = Counters()
+        self.lib.oracle_stream3_counters(h, _p(sw), len(sw), int(prefetch), C.byref(c))
+        return {n: getattr(c, n) for n, _ in Counters._fields_}
+
 
 class Reference:
     """The reference's own headers, compiled (oracle/_ref/libsobel5_ref.so)."""
@@ -176,6 +224,12 @@ class Reference:
         L.ref_measure_run_stream.restype = C.c_double
         L.ref_measure_oracle.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
         L.ref_measure_oracle.restype = C.c_double
+        L.ref_pad_replicate.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p] + E
+        L.ref_quantize.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        L.ref_sobel3_2d.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 3 + E
+        L.ref_run_stream_3x3.argtypes = [C.c_void_p] + [C.c_int] * 5 + [C.c_void_p] * 4 + E
+        L.ref_measure_run_stream_3x3.argtypes = [C.c_void_p] + [C.c_int] * 6 + [C.c_void_p]
+        L.ref_measure_run_stream_3x3.restype = C.c_double
 
     @staticmethod
     def _err():
@@ -263,6 +317,53 @@ class Reference:
         sd = np.zeros(1, np.float64)
         mean = self.lib.ref_measure_run_stream(_p(img), w, h, lanes, int(prefetch), workers,
                                                iters, _p(sd))
+        return mean, float(sd[0])
+
+
+    # ---- detect path ----
+    def pad_replicate(self, img, r=2):
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape if img.size else (0, 0)
+        out = np.empty((max(h + 2 * r, 0), max(w + 2 * r, 0)), np.uint8)
+        e = self._err()
+        code = self.lib.ref_pad_replicate(_p(img), w, h, r, _p(out), e, 512)
+        return code, (out if code == 0 else None), e.value.decode()
+
+    def quantize(self, plane, mode):
+        out = np.empty(plane.shape, np.uint8)
+        kind = 0 if plane.dtype == np.float64 else 1
+        plane = np.ascontiguousarray(plane, np.float64 if kind == 0 else np.int32)
+        h, w = plane.shape
+        self.lib.ref_quantize(_p(plane), kind, w, h, 1 if mode == "normalize" else 0, _p(out))
+        return out
+
+    def sobel3_2d(self, img):
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        o = {k: np.empty((max(h - 2, 1), max(w - 2, 1)), np.int32) for k in ("gx", "gy")}
+        o["g"] = np.empty((max(h - 2, 1), max(w - 2, 1)), np.float64)
+        e = self._err()
+        code = self.lib.ref_sobel3_2d(_p(img), w, h, _p(o["gx"]), _p(o["gy"]), _p(o["g"]), e, 512)
+        return code, o, e.value.decode()
+
+    def run_stream_3x3(self, img, lanes=32, prefetch=True, workers=1):
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        o = {k: np.empty((max(h - 2, 1), max(w - 2, 1)), np.int32) for k in ("gx", "gy")}
+        o["g"] = np.empty((max(h - 2, 1), max(w - 2, 1)), np.float64)
+        cnt = np.zeros(8, np.uint64)
+        e = self._err()
+        code = self.lib.ref_run_stream_3x3(_p(img), w, h, lanes, int(prefetch), workers,
+                                           _p(o["gx"]), _p(o["gy"]), _p(o["g"]), _p(cnt), e, 512)
+        names = [n for n, _ in Counters._fields_]
+        return code, o, dict(zip(names, (int(x) for x in cnt))), e.value.decode()
+
+    def measure_run_stream_3x3(self, img, lanes=256, prefetch=True, workers=1, iters=1):
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        sd = np.zeros(1, np.float64)
+        mean = self.lib.ref_measure_run_stream_3x3(_p(img), w, h, lanes, int(prefetch), workers,
+                                                   iters, _p(sd))
         return mean, float(sd[0])
 
 

@@ -7,13 +7,16 @@
 // to make golden fixtures, and by bench.py --impl reference / cpu_baseline as
 // the reference's own CPU implementation of the path.
 //
-// Only header-only pieces without third-party dependencies are included
-// (image_io.hpp needs libpng, which is absent).
+// image_io.hpp #includes <png.h>; libpng is absent here, so the Makefile puts
+// a declaration-only stand-in (oracle/png_stub/png.h) on the include path.
+// Only its pure-C++ pieces are called (detail::quantize, pad_replicate);
+// the shim links with -Wl,--no-undefined, proving no libpng symbol is used.
 #include <cstring>
 #include <exception>
 #include <string>
 
 #include "sobel5/filter_algebra.hpp"
+#include "sobel5/image_io.hpp"
 #include "sobel5/metrics.hpp"
 #include "sobel5/oracle.hpp"
 #include "sobel5/pipeline.hpp"
@@ -275,6 +278,95 @@ double ref_measure_oracle(const std::uint8_t* img, int w, int h, int iters) {
         auto r = sobel5::sobel5_4d(in, sobel5::FilterParams{});
         (void)r;
     });
+    return rep.mean_s;
+}
+
+// ---- detect path pieces -------------------------
+
+// pad_replicate (image_io.hpp:279-291); out is (w+2r) x (h+2r).
+int ref_pad_replicate(const std::uint8_t* img, int w, int h, int r, std::uint8_t* out, char* err,
+                      int errlen) {
+    try {
+        sobel5::GrayPlane in = w > 0 && h > 0
+            ? sobel5::GrayPlane(w, h, std::vector<std::uint8_t>(img, img + std::size_t(w) * h))
+            : sobel5::GrayPlane();
+        const auto p = sobel5::pad_replicate(in, r);
+        std::memcpy(out, p.plane.data().data(), p.plane.size());
+        return 0;
+    } catch (const std::exception& e) {
+        return report(e, err, errlen);
+    }
+}
+
+// detail::quantize (image_io.hpp:233-256) of a RealPlane (kind 0) or a
+// SignedPlane (kind 1); mode 0 = clamp_abs, 1 = normalize.
+int ref_quantize(const void* plane, int kind, int w, int h, int mode, std::uint8_t* out) {
+    const auto m = mode ? sobel5::SaveMode::normalize : sobel5::SaveMode::clamp_abs;
+    const std::size_t n = std::size_t(w) * h;
+    sobel5::GrayPlane q;
+    if (kind == 0) {
+        const double* v = static_cast<const double*>(plane);
+        q = sobel5::detail::quantize(sobel5::RealPlane(w, h, std::vector<double>(v, v + n)), m);
+    } else {
+        const std::int32_t* v = static_cast<const std::int32_t*>(plane);
+        q = sobel5::detail::quantize(
+            sobel5::SignedPlane(w, h, std::vector<std::int32_t>(v, v + n)), m);
+    }
+    std::memcpy(out, q.data().data(), q.size());
+    return 0;
+}
+
+// sobel3_2d (oracle.hpp:58-70).
+int ref_sobel3_2d(const std::uint8_t* img, int w, int h, std::int32_t* gx, std::int32_t* gy,
+                  double* g, char* err, int errlen) {
+    try {
+        sobel5::GrayPlane in(w, h, std::vector<std::uint8_t>(img, img + std::size_t(w) * h));
+        const auto r = sobel5::sobel3_2d(in);
+        copy_plane(r.gx, gx);
+        copy_plane(r.gy, gy);
+        if (g) std::memcpy(g, r.g.data().data(), r.g.size() * sizeof(double));
+        return 0;
+    } catch (const std::exception& e) {
+        return report(e, err, errlen);
+    }
+}
+
+// run_stream_3x3 (pipeline.hpp:551-573) with plan_strips(w, lanes, 1).
+int ref_run_stream_3x3(const std::uint8_t* img, int w, int h, int lanes, int prefetch,
+                       int workers, std::int32_t* gx, std::int32_t* gy, double* g,
+                       std::uint64_t* counters8, char* err, int errlen) {
+    try {
+        sobel5::GrayPlane in(w, h, std::vector<std::uint8_t>(img, img + std::size_t(w) * h));
+        const auto plan = sobel5::plan_strips(w, lanes, 1);
+        const auto r = sobel5::run_stream_3x3(
+            in, plan, prefetch ? sobel5::Prefetch::on : sobel5::Prefetch::off, workers);
+        copy_plane(r.gx, gx);
+        copy_plane(r.gy, gy);
+        if (g) std::memcpy(g, r.g.data().data(), r.g.size() * sizeof(double));
+        if (counters8) {
+            const auto& c = r.counters;
+            const std::uint64_t v[8] = {c.row_conv5_f, c.row_conv5_h, c.row_conv5_k0,
+                                        c.row_conv5_k1, c.row_diff,   c.row_conv3_f,
+                                        c.row_conv3_h, c.mac};
+            std::memcpy(counters8, v, sizeof v);
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return report(e, err, errlen);
+    }
+}
+
+// The reference's timing harness around its run_stream_3x3.
+double ref_measure_run_stream_3x3(const std::uint8_t* img, int w, int h, int lanes, int prefetch,
+                                  int workers, int iters, double* stddev_s) {
+    sobel5::GrayPlane in(w, h, std::vector<std::uint8_t>(img, img + std::size_t(w) * h));
+    const auto plan = sobel5::plan_strips(w, lanes, 1);
+    const auto rep = sobel5::measure("fast-3x3", w, h, iters, workers, [&] {
+        auto r = sobel5::run_stream_3x3(
+            in, plan, prefetch ? sobel5::Prefetch::on : sobel5::Prefetch::off, workers);
+        (void)r;
+    });
+    if (stddev_s) *stddev_s = rep.stddev_s;
     return rep.mean_s;
 }
 

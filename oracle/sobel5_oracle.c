@@ -293,3 +293,114 @@ uint64_t oracle_fnv1a64(const void* data, size_t bytes) {
     }
     return hsh;
 }
+
+/* ---- detect-path pieces -------------------- */
+
+static int clampi(int v, int lo, int hi) { return v < lo ? lo : v > hi ? hi : v; }
+
+/* pad_replicate (image_io.hpp:279-291): (w+2r) x (h+2r), every border pixel
+ * the nearest edge pixel (std::clamp of both coordinates). Returns 0,
+ * 20 (EmptyPlane, :280) or 19 (DimMismatch for r < 0, :281). */
+int oracle_pad_replicate(const uint8_t* img, int w, int h, int r, uint8_t* out) {
+    if (w <= 0 || h <= 0) return 20;
+    if (r < 0) return 19;
+    const int pw = w + 2 * r, ph = h + 2 * r;
+    for (int y = 0; y < ph; ++y) {
+        const int sy = clampi(y - r, 0, h - 1);
+        for (int x = 0; x < pw; ++x) out[(size_t)y * pw + x] = img[(size_t)sy * w + clampi(x - r, 0, w - 1)];
+    }
+    return 0;
+}
+
+/* detail::quantize(plane, normalize) (image_io.hpp:242-255): lo/hi by a
+ * sequential std::min/std::max scan from element 0, then
+ * lround((v - lo) * 255.0 / span) in double, 0 when span <= 0. */
+static void normalize_doubles(const double* v, size_t n, uint8_t* out) {
+    if (n == 0) return;
+    double lo = v[0], hi = v[0];
+    for (size_t i = 1; i < n; ++i) {
+        lo = v[i] < lo ? v[i] : lo; /* std::min(lo, v): returns lo unless v < lo */
+        hi = hi < v[i] ? v[i] : hi; /* std::max(hi, v): returns hi unless hi < v */
+    }
+    const double span = hi - lo;
+    for (size_t i = 0; i < n; ++i) {
+        const double mapped = span > 0 ? (v[i] - lo) * 255.0 / span : 0.0;
+        out[i] = (uint8_t)lround(mapped);
+    }
+}
+
+void oracle_normalize_f64(const double* v, size_t n, uint8_t* out) { normalize_doubles(v, n, out); }
+
+void oracle_normalize_i32(const int32_t* v, size_t n, uint8_t* out) {
+    /* quantize<int32_t> converts each element with static_cast<double>
+     * (image_io.hpp:243-249); every int32 is exact in double */
+    if (n == 0) return;
+    double* d = (double*)malloc(n * sizeof(double));
+    for (size_t i = 0; i < n; ++i) d[i] = (double)v[i];
+    normalize_doubles(d, n, out);
+    free(d);
+}
+
+/* quantize<int32_t>(plane, clamp_abs) (image_io.hpp:235-240). */
+void oracle_clamp_abs_i32(const int32_t* v, size_t n, uint8_t* out) {
+    for (size_t i = 0; i < n; ++i) {
+        const double a = fabs((double)v[i]);
+        const double r = round(a);
+        out[i] = (uint8_t)(r < 255.0 ? r : 255.0);
+    }
+}
+
+/* sobel3_2d (oracle.hpp:58-70) with kernel3_x / kernel3_y
+ * (filter_algebra.hpp:33-39), valid mode, int64 accumulation cast to
+ * int32 (conv2d_valid, oracle.hpp:35-48), g = sqrt(gx*gx + gy*gy). */
+int oracle_sobel3_2d(const uint8_t* img, int w, int h, int32_t* gx, int32_t* gy, double* g) {
+    static const int32_t kx[3][3] = {{-1, 0, 1}, {-2, 0, 2}, {-1, 0, 1}};
+    static const int32_t ky[3][3] = {{-1, -2, -1}, {0, 0, 0}, {1, 2, 1}};
+    if (w < 3 || h < 3) return 1;
+    const int ow = w - 2, oh = h - 2;
+    for (int y = 0; y < oh; ++y)
+        for (int x = 0; x < ow; ++x) {
+            int64_t ax = 0, ay = 0;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) {
+                    const int64_t p = img[(size_t)(y + i) * w + x + j];
+                    ax += kx[i][j] * p;
+                    ay += ky[i][j] * p;
+                }
+            const size_t o = (size_t)y * ow + x;
+            if (gx) gx[o] = (int32_t)ax;
+            if (gy) gy[o] = (int32_t)ay;
+            if (g) {
+                const double dx = (double)(int32_t)ax, dy = (double)(int32_t)ay;
+                g[o] = sqrt(dx * dx + dy * dy);
+            }
+        }
+    return 0;
+}
+
+/* OpCounters of run_stream_3x3 (pipeline.hpp:488-547): per strip, one hpass
+ * (F and H row_conv3, mac += 5w) per primed row (3) and per later centre,
+ * and mac += 5w per centre. */
+void oracle_stream3_counters(int h, const int* strip_out_w, int n_strips, int prefetch,
+                             oracle_counters* c) {
+    memset(c, 0, sizeof *c);
+    for (int s = 0; s < n_strips; ++s) {
+        const uint64_t w = (uint64_t)strip_out_w[s];
+#define HPASS3()                \
+    do {                        \
+        c->row_conv3_f += 1;    \
+        c->row_conv3_h += 1;    \
+        c->mac += 5 * w;        \
+    } while (0)
+        for (int u = 0; u < 3; ++u) HPASS3(); /* :514 */
+        for (int64_t v = 1; v <= h - 2; ++v) {
+            if (prefetch) { /* :518-519 */
+                if (v + 2 <= h - 1) HPASS3();
+            } else if (v > 1) { /* :520-522 */
+                HPASS3();
+            }
+            c->mac += 5 * w; /* :545 */
+        }
+#undef HPASS3
+    }
+}

@@ -84,6 +84,25 @@ void oracle_synth_random(uint8_t* img, int w, int h, uint64_t seed);
 void oracle_stream_counters(int h, const int* strip_out_w, int n_strips, const oracle_taps* t,
                             int prefetch, oracle_counters* c);
 
+/* ---- detect path ---- */
+
+/* pad_replicate (image_io.hpp:279-291); out is (w+2r) x (h+2r).
+ * Returns 0, 20 = EmptyPlane, 19 = DimMismatch (r < 0). */
+int oracle_pad_replicate(const uint8_t* img, int w, int h, int r, uint8_t* out);
+
+/* detail::quantize(plane, SaveMode::normalize) (image_io.hpp:242-255). */
+void oracle_normalize_f64(const double* v, size_t n, uint8_t* out);
+void oracle_normalize_i32(const int32_t* v, size_t n, uint8_t* out);
+/* detail::quantize(SignedPlane, SaveMode::clamp_abs) (image_io.hpp:235-240). */
+void oracle_clamp_abs_i32(const int32_t* v, size_t n, uint8_t* out);
+
+/* sobel3_2d (oracle.hpp:58-70); out (w-2) x (h-2). Returns 0 or 1 (too small). */
+int oracle_sobel3_2d(const uint8_t* img, int w, int h, int32_t* gx, int32_t* gy, double* g);
+
+/* OpCounters of run_stream_3x3 (pipeline.hpp:488-547). */
+void oracle_stream3_counters(int h, const int* strip_out_w, int n_strips, int prefetch,
+                             oracle_counters* c);
+
 /* FNV-1a 64 over raw bytes (SURVEY.md Appendix A.3 hashing convention). */
 uint64_t oracle_fnv1a64(const void* data, size_t bytes);
 

@@ -66,14 +66,17 @@ PLANE_NAMES = ("gx", "gy", "gd", "gdt", "g", "g32", "u8")
 
 # sobel5_status
 OK, IMAGE_TOO_SMALL, DIM_MISMATCH, PARITY_VIOLATION, INVALID_ARG, CUDA_ERROR, \
-    OUT_OF_MEMORY, NON_POSITIVE_PARAM, PARAM_OVERFLOW, LANE_TOO_NARROW, NO_DEVICE = range(11)
+    OUT_OF_MEMORY, NON_POSITIVE_PARAM, PARAM_OVERFLOW, LANE_TOO_NARROW, NO_DEVICE, \
+    EMPTY_PLANE = range(12)
 
 EXPORTS = (
     "sobel5_abi_version", "sobel5_status_string", "sobel5_launch_count", "sobel5_make_taps",
     "sobel5_plan_counters", "sobel5_launch", "sobel5_launch_batch", "sobel5_launch_band",
     "sobel5_synth_random_device", "sobel5_ctx_create", "sobel5_ctx_destroy",
     "sobel5_ctx_last_error", "sobel5_run_host", "sobel5_selftest", "sobel5_ipc_export",
-    "sobel5_ipc_import", "sobel5_ipc_release",
+    "sobel5_ipc_import", "sobel5_ipc_release", "sobel5_launch_ex", "sobel5_detect",
+    "sobel5_detect_scratch_bytes", "sobel5_quantize_plane", "sobel5_detect_host",
+    "sobel3_launch", "sobel3_detect", "sobel3_plan_counters", "sobel3_run_host",
 )
 
 _lib = None
@@ -131,6 +134,29 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.sobel5_ipc_release.restype = i32
     L.sobel5_selftest.argtypes = [i32, C.c_uint32, C.c_uint32, vp, vp]
     L.sobel5_selftest.restype = i32
+    L.sobel5_launch_ex.argtypes = [vp, i64, i64, i32, i32, i32, C.POINTER(Taps), i32, i32,
+                                   C.POINTER(Planes), i64, vp, vp]
+    L.sobel5_launch_ex.restype = i32
+    L.sobel5_detect_scratch_bytes.argtypes = [i32]
+    L.sobel5_detect_scratch_bytes.restype = C.c_size_t
+    L.sobel5_detect.argtypes = [vp, i64, i64, i32, i32, i32, C.POINTER(Taps), i32, i32, i32,
+                                C.POINTER(Planes), i64, vp, vp, vp]
+    L.sobel5_detect.restype = i32
+    L.sobel5_quantize_plane.argtypes = [vp, i32, i64, i32, i32, i32, vp, i64, vp, vp]
+    L.sobel5_quantize_plane.restype = i32
+    L.sobel5_detect_host.argtypes = [vp, vp, i32, i32, C.POINTER(Taps), i32, i32, i32, vp,
+                                     C.POINTER(Planes), C.POINTER(Diag)]
+    L.sobel5_detect_host.restype = i32
+    L.sobel3_launch.argtypes = [vp, i64, i64, i32, i32, i32, i32, i32, C.POINTER(Planes), i64,
+                                vp]
+    L.sobel3_launch.restype = i32
+    L.sobel3_detect.argtypes = [vp, i64, i64, i32, i32, i32, i32, i32, i32, C.POINTER(Planes),
+                                i64, vp, vp]
+    L.sobel3_detect.restype = i32
+    L.sobel3_plan_counters.argtypes = [i32, vp, i32, i32, C.POINTER(Counters)]
+    L.sobel3_plan_counters.restype = i32
+    L.sobel3_run_host.argtypes = [vp, vp, i32, i32, i32, C.POINTER(Planes)]
+    L.sobel3_run_host.restype = i32
     _lib = L
     return L
 

@@ -42,6 +42,7 @@ class CudaError(Error): pass
 
 
 _STATUS_EXC = {
+    _abi.EMPTY_PLANE: EmptyPlane,
     _abi.IMAGE_TOO_SMALL: ImageTooSmall,
     _abi.DIM_MISMATCH: DimMismatch,
     _abi.PARITY_VIOLATION: ParityViolation,
@@ -252,6 +253,28 @@ class Context:
         return st, res, d
 
 
+    def detect_host(self, img: np.ndarray, taps: Taps, prefetch: Prefetch = Prefetch.on,
+                    pad: bool = True, save_mode: "SaveMode" = None, planes=()):
+        """sobel5_detect_host: returns (status, u8 edge map, dict of planes, Diag)."""
+        save_mode = SaveMode.normalize if save_mode is None else save_mode
+        img = np.ascontiguousarray(img, dtype=np.uint8)
+        h, w = img.shape if img.ndim == 2 else (0, 0)
+        ow, oh = (w, h) if pad else (max(w - 4, 0), max(h - 4, 0))
+        dt = {"gx": np.int32, "gy": np.int32, "gd": np.int32, "gdt": np.int32, "g": np.float64,
+              "g32": np.float32}
+        u8 = np.empty((oh, ow), np.uint8)
+        res = {k: np.empty((oh, ow), dt[k]) for k in planes}
+        pl = Planes(pitch=ow)
+        for k, v in res.items():
+            setattr(pl, k, v.ctypes.data)
+        d = Diag()
+        st = self._lib.sobel5_detect_host(self._h, img.ctypes.data if img.size else None, w, h,
+                                          C.byref(taps), int(prefetch), int(bool(pad)),
+                                          int(save_mode), u8.ctypes.data if u8.size else None,
+                                          C.byref(pl) if planes else None, C.byref(d))
+        return st, u8, res, d
+
+
 _default_ctx: Context | None = None
 
 
@@ -377,6 +400,214 @@ def synth_random_device(d_img, pitch: int, width: int, height: int, seed: int = 
     check(_abi.load().sobel5_synth_random_device(d_img.data_ptr(), pitch, width, height,
                                                  row_offset, seed, mask, s),
           "sobel5_synth_random_device")
+
+
+# ---- detect path ------------------------------------------
+
+
+class SaveMode(enum.IntEnum):
+    """image_io.hpp:225-228."""
+    clamp_abs = 0
+    normalize = 1
+
+
+@dataclass
+class PaddedPlane:
+    """pad_replicate's result (image_io.hpp:271-277).  ``plane`` is the
+    materialised (W+2r) x (H+2r) image, as in the reference; ``source`` keeps
+    the unpadded image so that run_stream / detect on a PaddedPlane of radius
+    2 send only the source to the GPU and pad inside the kernel's loads."""
+    plane: np.ndarray
+    radius: int
+    source: np.ndarray | None = None
+
+    def inner_width(self) -> int:
+        return self.plane.shape[1] - 2 * self.radius
+
+    def inner_height(self) -> int:
+        return self.plane.shape[0] - 2 * self.radius
+
+
+def pad_replicate(img: np.ndarray, radius: int) -> PaddedPlane:
+    """image_io.hpp:279-291 (host helper, same errors and messages)."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    if img.size == 0:
+        raise EmptyPlane("cannot pad an empty image")
+    if radius < 0:
+        raise DimMismatch("pad radius must be non-negative")
+    return PaddedPlane(np.pad(img, radius, mode="edge"), radius, img)
+
+
+def alloc_scratch(frames: int = 1, device="cuda"):
+    """Device scratch for normalize (sobel5_detect_scratch_bytes)."""
+    import torch
+    n = int(_abi.load().sobel5_detect_scratch_bytes(frames))
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
+def launch_ex(d_in, in_pitch: int, width: int, height: int, taps: Taps, prefetch: int,
+              pad: bool, planes: dict, pitch: int, frames: int = 1, in_frame_stride: int = 0,
+              out_frame_stride: int = 0, diag=None, stream=None) -> None:
+    """sobel5_launch_ex: valid mode, or pad_replicate(img, 2) fused (same size)."""
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    pl = planes_struct(planes, pitch)
+    check(_abi.load().sobel5_launch_ex(d_in.data_ptr(), in_pitch, in_frame_stride, width, height,
+                                       frames, C.byref(taps), int(prefetch), int(bool(pad)),
+                                       C.byref(pl), out_frame_stride,
+                                       None if diag is None else diag.data_ptr(), s),
+          "sobel5_launch_ex")
+
+
+def detect_device(d_in, in_pitch: int, width: int, height: int, taps: Taps, prefetch: int,
+                  pad: bool, save_mode: SaveMode, planes: dict, pitch: int, scratch=None,
+                  frames: int = 1, in_frame_stride: int = 0, out_frame_stride: int = 0,
+                  diag=None, stream=None) -> None:
+    """sobel5_detect: planes["u8"] = quantize(g, save_mode) of the (padded) image."""
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    pl = planes_struct(planes, pitch)
+    check(_abi.load().sobel5_detect(d_in.data_ptr(), in_pitch, in_frame_stride, width, height,
+                                    frames, C.byref(taps), int(prefetch), int(bool(pad)),
+                                    int(save_mode), C.byref(pl), out_frame_stride,
+                                    None if scratch is None else scratch.data_ptr(),
+                                    None if diag is None else diag.data_ptr(), s),
+          "sobel5_detect")
+
+
+def quantize_device(d_plane, pitch: int, width: int, height: int, save_mode: SaveMode, d_u8,
+                    u8_pitch: int, scratch=None, stream=None) -> None:
+    """sobel5_quantize_plane on a float64 (RealPlane) or int32 (SignedPlane) tensor."""
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    kind = 0 if d_plane.dtype == torch.float64 else 1
+    if kind == 1 and d_plane.dtype != torch.int32:
+        raise DimMismatch("quantize needs a float64 or int32 plane")
+    check(_abi.load().sobel5_quantize_plane(d_plane.data_ptr(), kind, pitch, width, height,
+                                            int(save_mode), d_u8.data_ptr(), u8_pitch,
+                                            None if scratch is None else scratch.data_ptr(), s),
+          "sobel5_quantize_plane")
+
+
+def quantize(plane: np.ndarray, mode: SaveMode) -> np.ndarray:
+    """detail::quantize (image_io.hpp:233-256) of a host plane, computed on the GPU."""
+    import torch
+    plane = np.ascontiguousarray(plane)
+    if plane.size == 0:
+        raise EmptyPlane("cannot save an empty plane")
+    if plane.dtype not in (np.float64, np.int32):
+        raise DimMismatch("quantize needs a float64 or int32 plane")
+    h, w = plane.shape
+    d = torch.from_numpy(plane).cuda()
+    u8 = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+    quantize_device(d, w, w, h, mode, u8, w, alloc_scratch(1))
+    torch.cuda.synchronize()
+    return u8.cpu().numpy()
+
+
+def detect(img, params_or_taps=None, pad: bool = True, save_mode: SaveMode = SaveMode.normalize,
+           prefetch: Prefetch = Prefetch.on, planes=(), ctx: Context | None = None):
+    """The CLI's detect command on the GPU (sobel5_cli.cpp:127-189): optional
+    pad_replicate(img, 2), run_stream, save_plane(g, save_mode).  Returns the
+    u8 edge map, plus a dict of the requested planes when ``planes`` is set."""
+    if isinstance(img, PaddedPlane):
+        if img.radius != 2 or img.source is None:
+            raise DimMismatch("detect pads by radius 2")
+        img, pad = img.source, True
+    taps = params_or_taps if isinstance(params_or_taps, Taps) else make_stream_taps(
+        params_or_taps or FilterParams())
+    ctx = ctx or default_context()
+    st, u8, res, d = ctx.detect_host(np.asarray(img, dtype=np.uint8), taps, prefetch, pad,
+                                     save_mode, planes)
+    if st == _abi.PARITY_VIOLATION:
+        raise ParityViolation(f"odd sum/difference pair ({d.sum}, {d.diff})")
+    if st == _abi.EMPTY_PLANE:
+        raise EmptyPlane("cannot pad an empty image")
+    if st == _abi.IMAGE_TOO_SMALL:
+        h, w = np.shape(img) if np.ndim(img) == 2 else (0, 0)
+        raise ImageTooSmall(f"streaming filter needs at least 5x5, got {w}x{h}")
+    check(st, f"detect ({ctx.last_error()})")
+    return (u8, res) if planes else u8
+
+
+# ---- the 3x3 operator (SURVEY.md 8f row 3) ------------------------------------------
+
+
+@dataclass
+class Stream3Result:
+    """pipeline.hpp:479-484."""
+    gx: np.ndarray
+    gy: np.ndarray
+    g: np.ndarray
+    counters: dict
+
+
+def plan_counters_3x3(height: int, plan: StripPlan, prefetch: Prefetch) -> dict:
+    widths = np.array([s.out_w for s in plan.strips], dtype=np.int32)
+    c = Counters()
+    check(_abi.load().sobel3_plan_counters(height, widths.ctypes.data_as(C.c_void_p),
+                                           len(widths), int(prefetch), C.byref(c)),
+          "plan_counters_3x3")
+    return {n: int(getattr(c, n)) for n, _ in Counters._fields_}
+
+
+def run_stream_3x3(img: np.ndarray, plan: StripPlan | None = None,
+                   prefetch: Prefetch = Prefetch.on, workers: int = 1,
+                   ctx: Context | None = None) -> Stream3Result:
+    """Drop-in for sobel5::run_stream_3x3 (pipeline.hpp:551-573); ``plan``
+    defaults to one full-width strip like the reference's second overload
+    (:571-573)."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    if img.ndim != 2:
+        raise DimMismatch("image must be 2-D")
+    h, w = img.shape
+    if w < 3 or h < 3:  # pipeline.hpp:553-556
+        raise ImageTooSmall(f"streaming filter needs at least 3x3, got {w}x{h}")
+    if plan is None:
+        plan = plan_strips(w, w, 1)
+    if plan.in_width != w or plan.radius != 1:  # pipeline.hpp:557-560
+        raise DimMismatch(f"strip plan covers {plan.in_width} columns at radius {plan.radius}, "
+                          f"image has {w}")
+    ctx = ctx or default_context()
+    ow, oh = w - 2, h - 2
+    res = {"gx": np.empty((oh, ow), np.int32), "gy": np.empty((oh, ow), np.int32),
+           "g": np.empty((oh, ow), np.float64)}
+    pl = Planes(pitch=ow)
+    for k, v in res.items():
+        setattr(pl, k, v.ctypes.data)
+    st = _abi.load().sobel3_run_host(ctx.handle, img.ctypes.data, w, h, int(prefetch),
+                                     C.byref(pl))
+    check(st, f"run_stream_3x3 ({ctx.last_error()})")
+    return Stream3Result(res["gx"], res["gy"], res["g"], plan_counters_3x3(h, plan, prefetch))
+
+
+def sobel3_2d(img: np.ndarray) -> Stream3Result:
+    """oracle.hpp:58-70 (identical results; computed by the streaming GPU path)."""
+    return run_stream_3x3(img)
+
+
+def launch3(d_in, in_pitch: int, width: int, height: int, prefetch: int, pad: bool,
+            planes: dict, pitch: int, frames: int = 1, in_frame_stride: int = 0,
+            out_frame_stride: int = 0, stream=None) -> None:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    pl = planes_struct(planes, pitch)
+    check(_abi.load().sobel3_launch(d_in.data_ptr(), in_pitch, in_frame_stride, width, height,
+                                    frames, int(prefetch), int(bool(pad)), C.byref(pl),
+                                    out_frame_stride, s), "sobel3_launch")
+
+
+def detect3_device(d_in, in_pitch: int, width: int, height: int, prefetch: int, pad: bool,
+                   save_mode: SaveMode, planes: dict, pitch: int, scratch=None, frames: int = 1,
+                   in_frame_stride: int = 0, out_frame_stride: int = 0, stream=None) -> None:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    pl = planes_struct(planes, pitch)
+    check(_abi.load().sobel3_detect(d_in.data_ptr(), in_pitch, in_frame_stride, width, height,
+                                    frames, int(prefetch), int(bool(pad)), int(save_mode),
+                                    C.byref(pl), out_frame_stride,
+                                    None if scratch is None else scratch.data_ptr(), s),
+          "sobel3_detect")
 
 
 def launch_count() -> int:

@@ -16,12 +16,15 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libsobel5_b200.so")
-SOURCES = ["sobel5_abi.cu", "sobel5_ctx.cu", "sobel5_ipc.cu"]
+SOURCES = ["sobel5_abi.cu", "sobel5_ctx.cu", "sobel5_ipc.cu", "sobel5_detect.cu",
+           "sobel5_k_plain.cu", "sobel5_k_seg.cu", "sobel5_k_pad.cu", "sobel5_k_generic.cu",
+           "sobel3_k.cu"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-                     "-shared", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+                     "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+OBJDIR = os.path.join(ROOT, "build", "obj")
 
 
 def nvcc() -> str:
@@ -42,15 +45,30 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Each translation unit compiles in its own nvcc process (in parallel),
+    then one nvcc link produces the shared library."""
     if not force and not _stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(OBJDIR, exist_ok=True)
+    nv = nvcc()
+
+    def compile_one(src):
+        obj = os.path.join(OBJDIR, src.replace(".cu", ".o"))
+        cmd = [nv] + NVCC_FLAGS + (["-Xptxas=-v"] if verbose else []) + [
+            "-c", os.path.join(CSRC, src), "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if verbose or r.returncode:
+            sys.stderr.write(r.stdout + r.stderr)
+        if r.returncode:
+            raise RuntimeError(f"nvcc failed on {src}")
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB + ".tmp"
-    cmd = [nvcc()] + NVCC_FLAGS + [os.path.join(CSRC, s) for s in SOURCES] + ["-o", tmp]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+    subprocess.run([nv] + ARCH + ["-shared", "-o", tmp] + objs, check=True)
     os.replace(tmp, LIB)
     return LIB
 

@@ -17,6 +17,7 @@
 
 #include "sobel5_gpu.h"
 #include "sobel5_packed.cuh"
+#include "sobel5_internal.h"
 #include "sobel5_stream.cuh"
 
 using namespace sobel5_b200;
@@ -83,7 +84,7 @@ int env_int(const char* name, int dflt) {
 
 // Output rows per CTA band.  Small bands cost 4/band extra halo rows of
 // horizontal work; large ones leave too few CTAs to fill 148 SMs.
-int choose_band(int out_w, int out_h, int frames) {
+int choose_band_impl(int out_w, int out_h, int frames) {
     const int forced = env_int("SOBEL5_BAND", 0);
     if (forced > 0) return forced;
     const int64_t cols = (out_w + kCtaCols - 1) / kCtaCols;
@@ -108,7 +109,7 @@ void fill_taps(KernelParams& kp, const sobel5_taps& t) {
 
 bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
-sobel5_status check_planes(const sobel5_planes* o, int out_w) {
+sobel5_status check_planes_impl(const sobel5_planes* o, int out_w) {
     if (!o) return SOBEL5_INVALID_ARG;
     if (o->pitch < out_w || o->pitch % 4 != 0) return SOBEL5_INVALID_ARG;
     const void* ps[7] = {o->gx, o->gy, o->gd, o->gdt, o->g, o->g32, o->u8};
@@ -117,71 +118,28 @@ sobel5_status check_planes(const sobel5_planes* o, int out_w) {
     return SOBEL5_OK;
 }
 
-template <int PF, class TAPS, int MAG>
-cudaError_t launch_one(const KernelParams& kp, dim3 grid, cudaStream_t s) {
-    sobel5_stream_kernel<PF, TAPS, MAG><<<grid, kCtaThreads, 0, s>>>(kp);
-    return cudaGetLastError();
-}
-
-template <int PF, bool SEG, int OUTS>
-cudaError_t launch_packed(const KernelParams& kp, dim3 grid, cudaStream_t s) {
-    sobel5_packed_default_kernel<PF, SEG, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
-    return cudaGetLastError();
-}
-
-// Prefetch depth of the packed kernel (rows of loads in flight ahead of the
-// row being processed); Prefetch::off maps to 0.
-int prefetch_depth(int prefetch) {
-    if (!prefetch) return 0;
-    return env_int("SOBEL5_PF", 1) >= 2 ? 2 : 1;
-}
-
-int out_set(const KernelParams& kp) {
-    return (kp.gx ? kOutGx : 0) | (kp.gy ? kOutGy : 0) | (kp.gd ? kOutGd : 0) |
-           (kp.gdt ? kOutGdt : 0) | (kp.g ? kOutG : 0) | (kp.g32 ? kOutG32 : 0) |
-           (kp.u8 ? kOutU8 : 0);
-}
-
-template <int PF, bool SEG>
-cudaError_t dispatch_outs(const KernelParams& kp, dim3 grid, cudaStream_t s) {
-    // compile-time output sets for the common contracts, runtime otherwise
-    switch (out_set(kp)) {
-        case kOutSR: return launch_packed<PF, SEG, kOutSR>(kp, grid, s);
-        case kOutSR | kOutU8: return launch_packed<PF, SEG, kOutSR | kOutU8>(kp, grid, s);
-        case kOutU8: return launch_packed<PF, SEG, kOutU8>(kp, grid, s);
-        case 15 | kOutG32: return launch_packed<PF, SEG, 15 | kOutG32>(kp, grid, s);
-        default: return launch_packed<PF, SEG, kOutRuntime>(kp, grid, s);
-    }
-}
-
-template <bool SEG>
-cudaError_t dispatch_packed(const KernelParams& kp, dim3 grid, int depth, cudaStream_t s) {
-    switch (depth) {
-        case 0: return dispatch_outs<0, SEG>(kp, grid, s);
-        case 1: return dispatch_outs<1, SEG>(kp, grid, s);
-        default: return dispatch_outs<2, SEG>(kp, grid, s);
-    }
-}
-
 cudaError_t dispatch(const KernelParams& kp, dim3 grid, int prefetch, bool dflt, MagMode mag,
                      cudaStream_t s) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (dflt && env_int("SOBEL5_GENERIC", 0) == 0) {
         // default taps: packed two-pixels-per-register kernel (sobel5_packed.cuh)
+        if (kp.pad) return launch_packed_pad(kp, grid, prefetch, s);
         const bool seg = kp.top_rows > 0 || kp.bot != nullptr;
-        return seg ? dispatch_packed<true>(kp, grid, prefetch_depth(prefetch), s)
-                   : dispatch_packed<false>(kp, grid, prefetch_depth(prefetch), s);
+        return seg ? launch_packed_seg(kp, grid, prefetch, s)
+                   : launch_packed_plain(kp, grid, prefetch, s);
     }
-    if (dflt) {
-        return prefetch ? launch_one<1, DefaultTaps, kMagU32>(kp, grid, s)
-                        : launch_one<0, DefaultTaps, kMagU32>(kp, grid, s);
-    }
-    if (mag == kMagU32)
-        return prefetch ? launch_one<1, KernelParams, kMagU32>(kp, grid, s)
-                        : launch_one<0, KernelParams, kMagU32>(kp, grid, s);
-    return prefetch ? launch_one<1, KernelParams, kMagF64>(kp, grid, s)
-                    : launch_one<0, KernelParams, kMagF64>(kp, grid, s);
+    return launch_generic(kp, grid, prefetch, dflt, mag, s);
 }
+
+}  // namespace
+
+namespace sobel5_b200 {
+
+bool taps_default(const sobel5_taps* t) { return taps_are_default(*t); }
+int choose_band(int out_w, int out_h, int frames) { return choose_band_impl(out_w, out_h, frames); }
+sobel5_status check_planes(const sobel5_planes* o, int out_w) { return check_planes_impl(o, out_w); }
+
+void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
 
 sobel5_status map_cuda(cudaError_t e) {
     if (e == cudaSuccess) return SOBEL5_OK;
@@ -190,25 +148,33 @@ sobel5_status map_cuda(cudaError_t e) {
     return SOBEL5_CUDA_ERROR;
 }
 
-// Common launch path for plain, batched and band launches.
+// Common launch path for plain, batched, band and detect launches.
 sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_t* bot,
                             int64_t in_pitch, int64_t in_frame_stride, int width, int mid_rows,
                             int frames, const sobel5_taps* taps, int prefetch,
                             const sobel5_planes* out, int64_t out_frame_stride,
-                            sobel5_diag* diag, void* stream) {
+                            sobel5_diag* diag, void* stream, const LaunchExtra& ex) {
     const int top_rows = top ? 2 : 0, bot_rows = bot ? 2 : 0;
     const int64_t rows = int64_t{top_rows} + mid_rows + bot_rows;
-    // run_stream validation order: size first (pipeline.hpp:454-456)
-    if (width < 5 || rows < 5) return SOBEL5_IMAGE_TOO_SMALL;
+    if (ex.pad) {
+        // pad_replicate(img, 2) (image_io.hpp:279-281): empty input throws
+        // EmptyPlane; the padded image is then >= 5x5
+        if (width < 1 || mid_rows < 1) return SOBEL5_EMPTY_PLANE;
+        if (top || bot) return SOBEL5_INVALID_ARG;
+    } else if (width < 5 || rows < 5) {
+        // run_stream validation order: size first (pipeline.hpp:454-456)
+        return SOBEL5_IMAGE_TOO_SMALL;
+    }
     if (!taps || !mid || frames < 1) return SOBEL5_INVALID_ARG;
     if (in_pitch < round_up(width, 4) || in_pitch % 16 != 0) return SOBEL5_INVALID_ARG;
     if (!aligned(mid, 16) || (top && !aligned(top, 16)) || (bot && !aligned(bot, 16)))
         return SOBEL5_INVALID_ARG;
     if (frames > 1 && (in_frame_stride % 16 != 0 || out_frame_stride % 4 != 0))
         return SOBEL5_INVALID_ARG;
-    const int out_w = width - 4;
-    const int out_h = static_cast<int>(rows - 4);
+    const int out_w = ex.pad ? width : width - 4;
+    const int out_h = static_cast<int>(ex.pad ? rows : rows - 4);
     if (sobel5_status st = check_planes(out, out_w); st != SOBEL5_OK) return st;
+    if (ex.u8_norm && (!ex.norm || !out->u8)) return SOBEL5_INVALID_ARG;
     if (rows > (int64_t{1} << 30) || frames > 65535) return SOBEL5_INVALID_ARG;
 
     KernelParams kp{};
@@ -233,7 +199,11 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     kp.pitch = out->pitch;
     kp.out_frame_stride = out_frame_stride;
     kp.diag = diag;
-    kp.need_mag = (out->g || out->g32 || out->u8) ? 1 : 0;
+    kp.need_mag = (out->g || out->g32 || out->u8 || ex.minmax) ? 1 : 0;
+    kp.pad = ex.pad;
+    kp.minmax = ex.minmax;
+    kp.norm = ex.norm;
+    kp.u8_norm = ex.u8_norm;
     fill_taps(kp, *taps);
 
     const dim3 grid(static_cast<unsigned>((out_w + kCtaCols - 1) / kCtaCols),
@@ -248,6 +218,32 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
                                    static_cast<cudaStream_t>(stream));
     return map_cuda(e);
 }
+
+}  // namespace sobel5_b200
+
+namespace {
+
+// Device-side synth_random (synth.hpp:11-35), random-access form:
+// pixel i = byte (i mod 8) of splitmix64 output word floor(i/8), where word
+// k is mix(seed + (k+1) * 0x9E3779B97F4A7C15).
+__device__ __forceinline__ uint64_t splitmix64_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+__global__ void synth_random_kernel(uint8_t* img, int64_t pitch, int width, int height,
+                                    int64_t row_offset, uint64_t seed, uint8_t mask) {
+    const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    if (x >= width || y >= height) return;
+    const uint64_t i = static_cast<uint64_t>(row_offset + y) * static_cast<uint64_t>(width) +
+                       static_cast<uint64_t>(x);
+    const uint64_t word = splitmix64_mix(seed + (i / 8 + 1) * 0x9E3779B97F4A7C15ULL);
+    img[static_cast<int64_t>(y) * pitch + x] =
+        static_cast<uint8_t>((word >> (8 * (i % 8))) & 0xff) & mask;
+}
+
 
 __global__ void selftest_kernel(int which, uint32_t lo, uint32_t hi,
                                 unsigned long long* count) {
@@ -290,6 +286,7 @@ const char* sobel5_status_string(int status) {
         case SOBEL5_PARAM_OVERFLOW: return "filter weight magnitude exceeds 2^15";
         case SOBEL5_LANE_TOO_NARROW: return "lane width too narrow";
         case SOBEL5_NO_DEVICE: return "no CUDA device";
+        case SOBEL5_EMPTY_PLANE: return "cannot pad an empty image";
         default: return "unknown status";
     }
 }
@@ -377,7 +374,7 @@ sobel5_status sobel5_launch(const uint8_t* d_in, int64_t in_pitch, int width, in
                             const sobel5_taps* taps, int prefetch, const sobel5_planes* d_out,
                             sobel5_diag* d_diag, void* stream) {
     return launch_common(nullptr, d_in, nullptr, in_pitch, 0, width, height, 1, taps, prefetch,
-                         d_out, 0, d_diag, stream);
+                         d_out, 0, d_diag, stream, LaunchExtra{});
 }
 
 sobel5_status sobel5_launch_batch(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
@@ -385,7 +382,8 @@ sobel5_status sobel5_launch_batch(const uint8_t* d_in, int64_t in_pitch, int64_t
                                   int prefetch, const sobel5_planes* d_out,
                                   int64_t out_frame_stride, sobel5_diag* d_diag, void* stream) {
     return launch_common(nullptr, d_in, nullptr, in_pitch, in_frame_stride, width, height,
-                         n_frames, taps, prefetch, d_out, out_frame_stride, d_diag, stream);
+                         n_frames, taps, prefetch, d_out, out_frame_stride, d_diag, stream,
+                         LaunchExtra{});
 }
 
 sobel5_status sobel5_launch_band(const uint8_t* d_top, const uint8_t* d_in, const uint8_t* d_bot,
@@ -393,7 +391,7 @@ sobel5_status sobel5_launch_band(const uint8_t* d_top, const uint8_t* d_in, cons
                                  const sobel5_taps* taps, int prefetch,
                                  const sobel5_planes* d_out, sobel5_diag* d_diag, void* stream) {
     return launch_common(d_top, d_in, d_bot, in_pitch, 0, width, band_rows, 1, taps, prefetch,
-                         d_out, 0, d_diag, stream);
+                         d_out, 0, d_diag, stream, LaunchExtra{});
 }
 
 sobel5_status sobel5_selftest(int which, uint32_t lo, uint32_t hi, uint64_t* d_count,

@@ -1,0 +1,281 @@
+// sobel5_detect.cu -- the CLI detect path on the device (SURVEY.md 8f rows
+// 1-2): optional replicate padding fused into the stencil's loads, then the
+// edge-map export of g (image_io.hpp:233-256) in either SaveMode, plus the
+// standalone quantize of a device plane (save_plane, image_io.hpp:258-268).
+//
+// Reference flow (sobel5_cli.cpp:127-189): img = pad_replicate(img, r)
+// (:133) -> run_stream (:160-167) -> save_plane(g, normalize) (:177).
+// Here: normalize needs the frame's min/max of g before any pixel can be
+// mapped, so it is two passes over the input (the second recomputes the
+// stencil instead of round-tripping g through HBM):
+//   init   : minmax keys <- (+inf, -inf)
+//   pass 1 : stencil, optional planes, per-frame min/max of g (warp reduce +
+//            one atomic per warp)
+//   table  : per frame, the exact threshold table of S -> u8 (256 threads)
+//   pass 2 : stencil, u8 = normalize(g) through the table
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "sobel5_gpu.h"
+#include "sobel5_internal.h"
+#include "sobel5_packed.cuh"
+
+using namespace sobel5_b200;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+
+size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+sobel5_minmax* scratch_minmax(void* s) { return static_cast<sobel5_minmax*>(s); }
+sobel5_norm_table* scratch_table(void* s, int frames) {
+    return reinterpret_cast<sobel5_norm_table*>(static_cast<char*>(s) +
+                                                align_up(sizeof(sobel5_minmax) * frames));
+}
+
+__global__ void minmax_init_kernel(sobel5_minmax* mm, int frames) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < frames) {
+        mm[i].lo_key = ~0ull;
+        mm[i].hi_key = 0ull;
+    }
+}
+
+// One block per frame.  lo / hi from the keys; for integer sums of squares
+// (exact_s) thread k in 1..255 binary-searches the smallest S in
+// [S_lo, S_hi] whose normalized value is >= k (the map is monotone).
+__global__ void norm_table_kernel(const sobel5_minmax* mm, sobel5_norm_table* tab, int exact_s) {
+    const sobel5_minmax m = mm[blockIdx.x];
+    sobel5_norm_table* t = tab + blockIdx.x;
+    const bool any = m.lo_key <= m.hi_key;
+    const double lo = any ? dkey_value(m.lo_key) : 0.0;
+    const double hi = any ? dkey_value(m.hi_key) : 0.0;
+    const double span = hi - lo;  // image_io.hpp:248
+    const int k = threadIdx.x;
+    if (k == 0) {
+        t->lo = lo;
+        t->span = span;
+        t->lo_f = static_cast<float>(lo);
+        t->scale_f = span > 0.0 ? static_cast<float>(255.0 / span) : 0.0f;
+        t->exact_s = static_cast<uint32_t>(exact_s);
+        t->thr[0] = 0u;
+        t->thr[256] = 0xffffffffu;
+    }
+    if (k >= 1 && k <= 255) {
+        uint32_t thr = 0xffffffffu;
+        if (exact_s && any) {
+            // g = sqrt(S) correctly rounded and S < 2^31: S = rint(g * g)
+            const uint32_t s_lo = static_cast<uint32_t>(llrint(lo * lo));
+            const uint32_t s_hi = static_cast<uint32_t>(llrint(hi * hi));
+            auto u_of = [&](uint32_t S) { return normalize_u8(sqrt_u30(S), lo, span); };
+            if (u_of(s_hi) >= static_cast<uint32_t>(k)) {
+                uint32_t a = s_lo, b = s_hi;  // u(b) >= k
+                while (a < b) {
+                    const uint32_t c = a + (b - a) / 2;
+                    if (u_of(c) >= static_cast<uint32_t>(k)) b = c;
+                    else a = c + 1;
+                }
+                thr = a;
+            }
+        }
+        t->thr[k] = thr;
+    }
+}
+
+// ---- standalone quantize of a device plane (detail::quantize) ------------
+
+template <class T>
+__device__ __forceinline__ double as_double(T v) {
+    return static_cast<double>(v);
+}
+
+template <class T>
+__global__ void plane_minmax_kernel(const T* plane, int64_t pitch, int width, int height,
+                                    sobel5_minmax* mm) {
+    unsigned long long lo = ~0ull, hi = 0ull;
+    const int64_t n = static_cast<int64_t>(width) * height;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t y = i / width, x = i - y * width;
+        const double v = as_double(plane[y * pitch + x]);
+        if (v != v) continue;  // NaN never occurs for Sobel planes
+        const unsigned long long k = dkey(v);
+        lo = min(lo, k);
+        hi = max(hi, k);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0 && lo <= hi) {
+        atomicMin(reinterpret_cast<unsigned long long*>(&mm->lo_key), lo);
+        atomicMax(reinterpret_cast<unsigned long long*>(&mm->hi_key), hi);
+    }
+}
+
+// clamp_abs (image_io.hpp:235-240) or normalize (:242-255), per element.
+template <class T>
+__global__ void plane_map_kernel(const T* plane, int64_t pitch, int width, int height, int mode,
+                                 const sobel5_norm_table* tab, uint8_t* out, int64_t out_pitch) {
+    const double lo = mode ? tab->lo : 0.0, span = mode ? tab->span : 0.0;
+    const int64_t n = static_cast<int64_t>(width) * height;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t y = i / width, x = i - y * width;
+        const double v = as_double(plane[y * pitch + x]);
+        uint32_t u;
+        if (mode) {
+            u = normalize_u8(v, lo, span);
+        } else {
+            const double r = round(fabs(v));
+            u = r < 255.0 ? static_cast<uint32_t>(r) : 255u;
+        }
+        out[y * out_pitch + x] = static_cast<uint8_t>(u);
+    }
+}
+
+sobel5_status run_init(sobel5_minmax* mm, int frames, cudaStream_t s) {
+    minmax_init_kernel<<<(frames + 127) / 128, 128, 0, s>>>(mm, frames);
+    count_launch();
+    return map_cuda(cudaGetLastError());
+}
+
+}  // namespace
+
+extern "C" {
+
+sobel5_status sobel5_launch_ex(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
+                               int width, int height, int n_frames, const sobel5_taps* taps,
+                               int prefetch, int pad, const sobel5_planes* d_out,
+                               int64_t out_frame_stride, sobel5_diag* d_diag, void* stream) {
+    LaunchExtra ex;
+    ex.pad = pad ? 1 : 0;
+    return launch_common(nullptr, d_in, nullptr, in_pitch, in_frame_stride, width, height,
+                         n_frames, taps, prefetch, d_out, out_frame_stride, d_diag, stream, ex);
+}
+
+size_t sobel5_detect_scratch_bytes(int n_frames) {
+    if (n_frames < 1) return 0;
+    return align_up(sizeof(sobel5_minmax) * n_frames) + sizeof(sobel5_norm_table) * n_frames;
+}
+
+sobel5_status sobel5_detect(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
+                            int width, int height, int n_frames, const sobel5_taps* taps,
+                            int prefetch, int pad, int save_mode, const sobel5_planes* d_out,
+                            int64_t out_frame_stride, void* d_scratch, sobel5_diag* d_diag,
+                            void* stream) {
+    if (!d_out || !d_out->u8 || (save_mode != 0 && save_mode != 1) || n_frames < 1)
+        return SOBEL5_INVALID_ARG;
+    LaunchExtra ex;
+    ex.pad = pad ? 1 : 0;
+    if (save_mode == 0)  // clamp_abs: one fused launch
+        return launch_common(nullptr, d_in, nullptr, in_pitch, in_frame_stride, width, height,
+                             n_frames, taps, prefetch, d_out, out_frame_stride, d_diag, stream, ex);
+    if (!d_scratch || reinterpret_cast<uintptr_t>(d_scratch) % 16 != 0) return SOBEL5_INVALID_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    sobel5_minmax* mm = scratch_minmax(d_scratch);
+    sobel5_norm_table* tab = scratch_table(d_scratch, n_frames);
+    // validate before any launch: a dry check through pass 2's arguments
+    sobel5_planes p2{};
+    p2.u8 = d_out->u8;
+    p2.pitch = d_out->pitch;
+    // pass 1: requested planes (u8 excluded) + min/max of g
+    sobel5_planes p1 = *d_out;
+    p1.u8 = nullptr;
+    if (sobel5_status st = run_init(mm, n_frames, s); st != SOBEL5_OK) return st;
+    LaunchExtra e1 = ex;
+    e1.minmax = mm;
+    sobel5_status st = launch_common(nullptr, d_in, nullptr, in_pitch, in_frame_stride, width,
+                                     height, n_frames, taps, prefetch, &p1, out_frame_stride,
+                                     d_diag, stream, e1);
+    if (st != SOBEL5_OK) return st;
+    // thresholds: exact for integer sums of squares (the packed default-taps
+    // kernel); the generic kernel maps g with the direct double formula
+    const bool dflt = taps && taps_default(taps);
+    norm_table_kernel<<<n_frames, 256, 0, s>>>(mm, tab, dflt ? 1 : 0);
+    count_launch();
+    if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return map_cuda(e);
+    LaunchExtra e2 = ex;
+    e2.norm = tab;
+    e2.u8_norm = 1;
+    return launch_common(nullptr, d_in, nullptr, in_pitch, in_frame_stride, width, height,
+                         n_frames, taps, prefetch, &p2, out_frame_stride, nullptr, stream, e2);
+}
+
+sobel5_status sobel3_detect(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
+                            int width, int height, int n_frames, int prefetch, int pad,
+                            int save_mode, const sobel5_planes* d_out, int64_t out_frame_stride,
+                            void* d_scratch, void* stream) {
+    if (!d_out || !d_out->u8 || (save_mode != 0 && save_mode != 1) || n_frames < 1)
+        return SOBEL5_INVALID_ARG;
+    LaunchExtra ex;
+    ex.pad = pad ? 1 : 0;
+    if (save_mode == 0)
+        return sobel3_common(d_in, in_pitch, in_frame_stride, width, height, n_frames, prefetch,
+                             d_out, out_frame_stride, stream, ex);
+    if (!d_scratch || reinterpret_cast<uintptr_t>(d_scratch) % 16 != 0) return SOBEL5_INVALID_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    sobel5_minmax* mm = scratch_minmax(d_scratch);
+    sobel5_norm_table* tab = scratch_table(d_scratch, n_frames);
+    sobel5_planes p1 = *d_out;
+    p1.u8 = nullptr;
+    sobel5_planes p2{};
+    p2.u8 = d_out->u8;
+    p2.pitch = d_out->pitch;
+    if (sobel5_status st = run_init(mm, n_frames, s); st != SOBEL5_OK) return st;
+    LaunchExtra e1 = ex;
+    e1.minmax = mm;
+    sobel5_status st = sobel3_common(d_in, in_pitch, in_frame_stride, width, height, n_frames,
+                                     prefetch, &p1, out_frame_stride, stream, e1);
+    if (st != SOBEL5_OK) return st;
+    norm_table_kernel<<<n_frames, 256, 0, s>>>(mm, tab, 1);
+    count_launch();
+    if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return map_cuda(e);
+    LaunchExtra e2 = ex;
+    e2.norm = tab;
+    e2.u8_norm = 1;
+    return sobel3_common(d_in, in_pitch, in_frame_stride, width, height, n_frames, prefetch, &p2,
+                         out_frame_stride, stream, e2);
+}
+
+sobel5_status sobel5_quantize_plane(const void* d_plane, int kind, int64_t pitch, int width,
+                                    int height, int save_mode, uint8_t* d_u8, int64_t u8_pitch,
+                                    void* d_scratch, void* stream) {
+    // save_plane (image_io.hpp:258-268): an empty plane throws EmptyPlane
+    if (width < 1 || height < 1) return SOBEL5_EMPTY_PLANE;
+    if (!d_plane || !d_u8 || (kind != 0 && kind != 1) || (save_mode != 0 && save_mode != 1) ||
+        pitch < width || u8_pitch < width)
+        return SOBEL5_INVALID_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int blocks = 148 * 8;
+    sobel5_norm_table* tab = nullptr;
+    if (save_mode == 1) {
+        if (!d_scratch || reinterpret_cast<uintptr_t>(d_scratch) % 16 != 0)
+            return SOBEL5_INVALID_ARG;
+        sobel5_minmax* mm = scratch_minmax(d_scratch);
+        tab = scratch_table(d_scratch, 1);
+        if (sobel5_status st = run_init(mm, 1, s); st != SOBEL5_OK) return st;
+        if (kind == 0)
+            plane_minmax_kernel<<<blocks, 256, 0, s>>>(static_cast<const double*>(d_plane), pitch,
+                                                       width, height, mm);
+        else
+            plane_minmax_kernel<<<blocks, 256, 0, s>>>(static_cast<const int32_t*>(d_plane), pitch,
+                                                       width, height, mm);
+        norm_table_kernel<<<1, 256, 0, s>>>(mm, tab, 0);
+        count_launch(2);
+        if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return map_cuda(e);
+    }
+    if (kind == 0)
+        plane_map_kernel<<<blocks, 256, 0, s>>>(static_cast<const double*>(d_plane), pitch, width,
+                                                height, save_mode, tab, d_u8, u8_pitch);
+    else
+        plane_map_kernel<<<blocks, 256, 0, s>>>(static_cast<const int32_t*>(d_plane), pitch, width,
+                                                height, save_mode, tab, d_u8, u8_pitch);
+    count_launch();
+    return map_cuda(cudaGetLastError());
+}
+
+}  // extern "C"

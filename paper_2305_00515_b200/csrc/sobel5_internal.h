@@ -1,0 +1,52 @@
+// sobel5_internal.h -- library-internal launch interface shared by the
+// translation units (kernels are instantiated in separate .cu files so the
+// build compiles them in parallel).  Not part of the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "sobel5_gpu.h"
+#include "sobel5_stream.cuh"
+
+namespace sobel5_b200 {
+
+// Packed default-taps kernel (sobel5_packed.cuh), one launcher per geometry.
+cudaError_t launch_packed_plain(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
+cudaError_t launch_packed_seg(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
+cudaError_t launch_packed_pad(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
+
+// Generic-taps kernel (sobel5_stream.cuh).
+cudaError_t launch_generic(const KernelParams& kp, dim3 grid, int pf, bool default_taps,
+                           MagMode mag, cudaStream_t s);
+
+// Extra options of a launch beyond the plain StreamResult planes.
+struct LaunchExtra {
+    int pad = 0;                               // fused pad_replicate(img, 2)
+    sobel5_minmax* minmax = nullptr;           // normalize pass 1
+    const sobel5_norm_table* norm = nullptr;   // normalize pass 2
+    int u8_norm = 0;
+};
+
+// Common launch path (validation in the reference's order, geometry, kernel
+// selection) for plain, batched, band and detect launches.
+sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_t* bot,
+                            int64_t in_pitch, int64_t in_frame_stride, int width, int mid_rows,
+                            int frames, const sobel5_taps* taps, int prefetch,
+                            const sobel5_planes* out, int64_t out_frame_stride,
+                            sobel5_diag* diag, void* stream, const LaunchExtra& ex);
+
+sobel5_status map_cuda(cudaError_t e);
+int choose_band(int out_w, int out_h, int frames);  // output rows per CTA
+sobel5_status check_planes(const sobel5_planes* o, int out_w);
+
+// 3x3 operator (sobel3_packed.cuh, sobel3_k.cu).
+sobel5_status sobel3_common(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
+                            int width, int height, int frames, int prefetch,
+                            const sobel5_planes* out, int64_t out_frame_stride, void* stream,
+                            const LaunchExtra& ex);
+bool taps_default(const sobel5_taps* t);  // equal to make_stream_taps(1, 2, 6, 4)
+void count_launch(int n = 1);
+
+}  // namespace sobel5_b200

@@ -1,0 +1,34 @@
+// sobel5_k_plain.cu -- instantiations of the packed default-taps kernel for
+// plain images and batches (valid mode), one per output contract.
+#include "sobel5_internal.h"
+#include "sobel5_packed.cuh"
+
+namespace sobel5_b200 {
+
+namespace {
+template <int PF, int OUTS>
+cudaError_t go(const KernelParams& kp, dim3 grid, cudaStream_t s) {
+    sobel5_packed_default_kernel<PF, kGeomPlain, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
+    return cudaGetLastError();
+}
+
+template <int PF>
+cudaError_t outs(const KernelParams& kp, dim3 grid, cudaStream_t s) {
+    // compile-time output sets for the common contracts, runtime otherwise
+    switch (packed_out_set(kp)) {
+        case kOutSR: return go<PF, kOutSR>(kp, grid, s);
+        case kOutSR | kOutU8: return go<PF, kOutSR | kOutU8>(kp, grid, s);
+        case kOutU8: return go<PF, kOutU8>(kp, grid, s);
+        case 15 | kOutG32: return go<PF, 15 | kOutG32>(kp, grid, s);
+        case kOutMinMax: return go<PF, kOutMinMax>(kp, grid, s);
+        case kOutU8 | kOutNorm: return go<PF, kOutU8 | kOutNorm>(kp, grid, s);
+        default: return go<PF, kOutRuntime>(kp, grid, s);
+    }
+}
+}  // namespace
+
+cudaError_t launch_packed_plain(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s) {
+    return pf ? outs<1>(kp, grid, s) : outs<0>(kp, grid, s);
+}
+
+}  // namespace sobel5_b200

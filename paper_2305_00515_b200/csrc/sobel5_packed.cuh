@@ -40,8 +40,17 @@ namespace sobel5_b200 {
 // Output-set bits (template OUTS); kOutRuntime checks the plane pointers.
 enum : int {
     kOutGx = 1, kOutGy = 2, kOutGd = 4, kOutGdt = 8, kOutG = 16, kOutG32 = 32, kOutU8 = 64,
+    kOutMinMax = 128, kOutNorm = 256,
     kOutSR = 31, kOutRuntime = -1
 };
+
+// Output-set bits of a launch (selects the compile-time instantiation).
+inline int packed_out_set(const KernelParams& kp) {
+    return (kp.gx ? kOutGx : 0) | (kp.gy ? kOutGy : 0) | (kp.gd ? kOutGd : 0) |
+           (kp.gdt ? kOutGdt : 0) | (kp.g ? kOutG : 0) | (kp.g32 ? kOutG32 : 0) |
+           (kp.u8 ? kOutU8 : 0) | (kp.minmax ? kOutMinMax : 0) |
+           (kp.u8 && kp.u8_norm ? kOutNorm : 0);
+}
 
 // Double magnitude of an exact integer sum of squares S < 2^32: IEEE sqrt
 // (__dsqrt_rn), bit-identical to std::sqrt((double)S).  A float-seeded
@@ -70,12 +79,37 @@ __device__ __forceinline__ int32_t lane_hi(uint32_t v) {
     return static_cast<int32_t>(v + 0x8000u) >> 16;
 }
 
+// Exact normalize export of an integer sum of squares (image_io.hpp:242-255,
+// pass 2): u = lround((sqrt(S) - lo) * 255 / span) is non-decreasing in S
+// (each IEEE step is monotone), so it equals max{k : thr[k] <= S} for the
+// thresholds built by norm_table_kernel (sobel5_detect.cu).  A float estimate
+// seeds the lookup; two table probes confirm it, else an 8-step binary
+// search decides, so the result is exact whatever the seed.
+__device__ __forceinline__ uint32_t u8_normalize_s(uint32_t S, const uint32_t* thr, float lo_f,
+                                                   float scale_f) {
+    const float f = __uint2float_rn(S);
+    const float est = (f * rsqrtf(fmaxf(f, 1.0f)) - lo_f) * scale_f;
+    int e = min(255, max(0, __float2int_rn(est)));
+    if (thr[e] <= S && S < thr[e + 1]) return static_cast<uint32_t>(e);
+    // seed off by more than the table says (tiny spans): binary search
+    e = 0;
+#pragma unroll
+    for (int step = 128; step >= 1; step >>= 1)
+        if (thr[e + step] <= S) e += step;
+    return static_cast<uint32_t>(e);
+}
+
 // Default taps, packed.  PF = number of input rows whose loads are in flight
 // ahead of the row being processed (0 = Prefetch::off, >= 1 = on).
-// SEG = stacked three-segment input (row bands with halos) vs plain image.
-template <int PF, bool SEG, int OUTS>
+// GEOM = Geom (plain image / stacked row band / fused replicate padding).
+// OUTS = output-set bits; kOutMinMax adds the per-frame min/max of g
+// (normalize pass 1), kOutNorm makes the u8 plane the normalize export
+// (pass 2) instead of clamp_abs.
+template <int PF, int GEOM, int OUTS>
 __global__ void __launch_bounds__(kCtaThreads, 4)
     sobel5_packed_default_kernel(const __grid_constant__ KernelParams p) {
+    constexpr bool SEG = GEOM == kGeomSeg;
+    constexpr bool PAD = GEOM == kGeomPad;
     // which planes this instantiation writes (compile-time unless kOutRuntime)
     constexpr bool RT = OUTS == kOutRuntime;
     const bool w_gx = RT ? p.gx != nullptr : (OUTS & kOutGx) != 0;
@@ -85,34 +119,58 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
     const bool w_g = RT ? p.g != nullptr : (OUTS & kOutG) != 0;
     const bool w_g32 = RT ? p.g32 != nullptr : (OUTS & kOutG32) != 0;
     const bool w_u8 = RT ? p.u8 != nullptr : (OUTS & kOutU8) != 0;
+    const bool w_mm = RT ? p.minmax != nullptr : (OUTS & kOutMinMax) != 0;
+    const bool u8_norm = RT ? p.u8_norm != 0 : (OUTS & kOutNorm) != 0;
     const bool need_g = w_g || w_g32;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int x0 = (blockIdx.x * kCtaWarps + warp) * kWarpCols + lane * 4;
-    if ((x0 - lane * 4) >= p.out_w) return;
+    const int warp_x0 = (blockIdx.x * kCtaWarps + warp) * kWarpCols;
+    const int x0 = warp_x0 + lane * 4;
+
+    // normalize pass 2: the frame's threshold table, staged in shared memory
+    __shared__ uint32_t s_thr[257];
+    float n_lo = 0.f, n_scale = 0.f;
+    if (RT || (OUTS & kOutNorm)) {
+        if (u8_norm) {
+            const sobel5_norm_table* t = p.norm + blockIdx.z;
+            for (int i = threadIdx.x; i < 257; i += kCtaThreads) s_thr[i] = t->thr[i];
+            n_lo = t->lo_f;
+            n_scale = t->scale_f;
+            __syncthreads();
+        }
+    }
+    if (warp_x0 >= p.out_w) return;  // whole warp right of the image
     const int oy0 = blockIdx.y * p.band;
     const int n_out = min(p.band, p.out_h - oy0);
     const int n_in = n_out + 4;
     const int64_t in_frame = static_cast<int64_t>(blockIdx.z) * p.in_frame_stride;
     const int64_t out_frame = static_cast<int64_t>(blockIdx.z) * p.out_frame_stride;
     const bool load_a = x0 < p.width;
-    const bool load_b = lane == 31 && x0 + 4 < p.width;
+    // the one extra word: lane 31's right neighbour; in pad mode lane 0's left
+    const int xoff = (PAD && lane == 0) ? -4 : 4;
+    const bool load_b = (lane == 31 && x0 + 4 < p.width) || (PAD && lane == 0 && x0 > 0);
     const bool full = x0 + 3 < p.out_w;
+    const PadEdge pe = PAD ? pad_edge_setup(p.width, warp_x0) : PadEdge{0, 0, 0, 0u};
 
     // row pointer for plain images: advanced by one pitch per row
     const uint8_t* plain = p.mid + in_frame + static_cast<int64_t>(oy0) * p.in_pitch + x0;
     auto row_ptr = [&](int r) -> const uint8_t* {
         if (SEG) return stacked_row(p, in_frame, oy0 + r) + x0;
+        if (PAD) {  // padded row oy0 + r is image row clamp(oy0 + r - 2, 0, H - 1)
+            const int y = min(max(oy0 + r - 2, 0), p.mid_rows - 1);
+            return p.mid + in_frame + static_cast<int64_t>(y) * p.in_pitch + x0;
+        }
         return plain + static_cast<int64_t>(r) * p.in_pitch;
     };
     auto load_row = [&](int r, uint32_t& a, uint32_t& b) {
         const uint8_t* rp = row_ptr(r);
         a = load_a ? ld_row_word(rp) : 0u;
-        b = load_b ? ld_row_word(rp + 4) : 0u;
+        b = load_b ? ld_row_word(rp + xoff) : 0u;
     };
 
     // pending accumulators [slot = output row mod 5][pair]
     uint32_t ax[5][2], ay[5][2], an[5][2], aq[5][2];
+    uint32_t s_min = 0xffffffffu, s_max = 0u;
 
     // Prefetch ring: with PF > 0 the loads of the next 5 input rows are in
     // flight while a row is processed.  The ring slot is the unrolled row
@@ -129,9 +187,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
             if (k < n_in) load_row(k, qa[k], qb[k]);
             else qa[k] = qb[k] = 0u;
         }
-        cur_a = qa[0];
-        const uint32_t sh0 = __shfl_down_sync(0xffffffffu, cur_a, 1);
-        cur_b = lane != 31 ? sh0 : qb[0];
+        row_window<PAD>(qa[0], qb[0], lane, x0, p.width, pe, cur_a, cur_b);
     }
 
     for (int base = 0; base < n_in; base += 5) {
@@ -144,10 +200,9 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                 wa = cur_a;
                 wb = cur_b;
             } else {
-                load_row(r, wa, wb);
-                // warp-shuffle column sharing
-                const uint32_t sh = __shfl_down_sync(0xffffffffu, wa, 1);
-                if (lane != 31) wb = sh;
+                uint32_t o, x;
+                load_row(r, o, x);
+                row_window<PAD>(o, x, lane, x0, p.width, pe, wa, wb);
             }
 
             // E_k = byte k | byte k+2 << 16
@@ -165,9 +220,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                 if (r + 5 < n_in) load_row(r + 5, qa[s], qb[s]);
                 // warp-shuffle column sharing for row r+1
                 const int sn = (s + 1) % 5;
-                cur_a = qa[sn];
-                const uint32_t shn = __shfl_down_sync(0xffffffffu, cur_a, 1);
-                cur_b = lane != 31 ? shn : qb[sn];
+                row_window<PAD>(qa[sn], qb[sn], lane, x0, p.width, pe, cur_a, cur_b);
             }
 
             uint32_t F[2], H[2], D[2], K0[2], K1[2];
@@ -255,7 +308,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                         }
                     }
                 }
-                if (need_g || w_u8) {
+                if (need_g || w_u8 || w_mm) {
                     // exact: every square < 2^28 and the sum < 2^30, so
                     // double(S) equals the reference's double sum of squares
                     uint32_t S[4];
@@ -265,6 +318,15 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                                static_cast<uint32_t>(gy[j] * gy[j]) +
                                static_cast<uint32_t>(gd[j] * gd[j]) +
                                static_cast<uint32_t>(gdt[j] * gdt[j]);
+                    if (w_mm) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            if (full || x0 + j < p.out_w) {
+                                s_min = min(s_min, S[j]);
+                                s_max = max(s_max, S[j]);
+                            }
+                        }
+                    }
                     double g[4] = {0.0, 0.0, 0.0, 0.0};
                     if (need_g) {
 #pragma unroll
@@ -273,7 +335,9 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                     uint32_t u[4] = {0u, 0u, 0u, 0u};
                     if (w_u8) {
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) u[j] = u8_from_s(S[j]);
+                        for (int j = 0; j < 4; ++j)
+                            u[j] = u8_norm ? u8_normalize_s(S[j], s_thr, n_lo, n_scale)
+                                           : u8_from_s(S[j]);
                     }
                     if (full) {
                         if (w_g) {
@@ -297,6 +361,17 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                     }
                 }
             }
+        }
+    }
+    if (w_mm) {  // normalize pass 1: frame min / max of g = sqrt(S), monotone in S
+        s_min = __reduce_min_sync(0xffffffffu, s_min);
+        s_max = __reduce_max_sync(0xffffffffu, s_max);
+        if (lane == 0 && s_min <= s_max) {
+            sobel5_minmax* mm = p.minmax + blockIdx.z;
+            atomicMin(reinterpret_cast<unsigned long long*>(&mm->lo_key),
+                      dkey(sqrt_u30(s_min)));
+            atomicMax(reinterpret_cast<unsigned long long*>(&mm->hi_key),
+                      dkey(sqrt_u30(s_max)));
         }
     }
 }

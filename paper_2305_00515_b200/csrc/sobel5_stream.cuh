@@ -70,6 +70,11 @@ struct KernelParams {
     int64_t out_frame_stride;
     sobel5_diag* diag;
     int need_mag;
+    // detect path: replicate padding, normalize export
+    int pad;                     // 1: pad_replicate(img, 2) fused (same-size output)
+    sobel5_minmax* minmax;       // per frame: min/max of g (pass 1 of normalize)
+    const sobel5_norm_table* norm;  // per frame: normalize thresholds (pass 2)
+    int u8_norm;                 // u8 plane = normalize(g) instead of clamp_abs(g)
     // taps (kernel parameter space -> constant-bank operands)
     int32_t f[5], h[5], k0[5], k1[5], gx_v[5], gy_v[5], gdm_f[5], gdm_d[5];
 };
@@ -162,6 +167,76 @@ struct TapSource<DefaultTaps> {
     __device__ static constexpr int32_t gdm_d(int i) { return pick5(i, 10, 0, -12, 0, 10); }
 };
 
+// Geometry of the input rows / columns seen by a kernel instantiation.
+enum Geom : int {
+    kGeomPlain = 0,  // valid mode over one (or a batch of) plain image(s)
+    kGeomSeg = 1,    // valid mode over a stacked [top halo; band; bottom halo]
+    kGeomPad = 2,    // pad_replicate(img, 2) fused: same-size output (image_io.hpp:279-291)
+};
+
+// The 8-byte window (wa = input columns c..c+3, wb = c+4..c+7) a lane needs
+// for its 4 output columns, from its own row word `own` and the one extra
+// word `xtra` that lane 31 (right neighbour word) and, in pad mode, lane 0
+// (left neighbour word) load themselves.  The other neighbour words come
+// from warp shuffles (the paper's column sharing).
+//   valid : c = x0       -> wa = own, wb = right
+//   pad   : c = x0 - 2   -> wa = (left:own) bytes 2..5, wb = (own:right) bytes 2..5,
+//           columns outside [0, width) replaced by the edge pixel (std::clamp
+//           of the column, image_io.hpp:286).
+struct PadEdge {
+    int active;     // warp-uniform: some lane's window reaches past width-1
+    int src_lane;   // lane holding column width-1 ...
+    int from_xtra;  // ... in its extra word (lane 31's right word) or its own
+    uint32_t sel;   // byte_perm selector replicating that byte
+};
+
+__device__ __forceinline__ PadEdge pad_edge_setup(int width, int warp_x0) {
+    PadEdge e;
+    // lane 31's window ends at column warp_x0 + 131 at most
+    e.active = warp_x0 + kWarpCols + 3 >= width;
+    // column width-1 relative to the warp: 0..130 whenever active (>= 128 is
+    // in lane 31's right neighbour word, owned by the next warp)
+    const int c = width - 1 - warp_x0;
+    e.from_xtra = c >= kWarpCols;
+    e.src_lane = min(31, c >> 2);
+    e.sel = static_cast<uint32_t>(c & 3) * 0x1111u;
+    return e;
+}
+
+// R = pad radius (2 for the 5x5 operator, 1 for the 3x3 one): the window
+// starts at column c = x0 - R.
+template <bool PAD, int R = 2>
+__device__ __forceinline__ void row_window(uint32_t own, uint32_t xtra, int lane, int x0, int width,
+                                           const PadEdge& pe, uint32_t& wa, uint32_t& wb) {
+    static_assert(R == 1 || R == 2, "pad radius");
+    const uint32_t dn = __shfl_down_sync(0xffffffffu, own, 1);
+    const uint32_t right = lane != 31 ? dn : xtra;
+    if (!PAD) {
+        wa = own;
+        wb = right;
+        return;
+    }
+    constexpr uint32_t kSel = R == 2 ? 0x5432u : 0x6543u;  // bytes 4-R .. 7-R of (lo:hi)
+    const uint32_t up = __shfl_up_sync(0xffffffffu, own, 1);
+    const uint32_t left = lane != 0 ? up : (x0 > 0 ? xtra : __byte_perm(own, 0u, 0x0000));
+    wa = __byte_perm(left, own, kSel);
+    wb = __byte_perm(own, right, kSel);
+    if (pe.active) {  // warp-uniform: the right image edge is in this warp's reach
+        const uint32_t ew = __shfl_sync(0xffffffffu, pe.from_xtra ? xtra : own, pe.src_lane);
+        const uint32_t rep = __byte_perm(ew, 0u, pe.sel);
+        const int nv = width - (x0 - R);  // valid window bytes (> R for live lanes)
+        if (nv < 4) {
+            const uint32_t m = 0xffffffffu << (8 * nv);
+            wa = (wa & ~m) | (rep & m);
+        }
+        if (nv < 8) {
+            const int k = nv - 4;
+            const uint32_t m = k <= 0 ? 0xffffffffu : 0xffffffffu << (8 * k);
+            wb = (wb & ~m) | (rep & m);
+        }
+    }
+}
+
 // Row pointer of stacked input row `row` (0-based, stacked coordinates).
 __device__ __forceinline__ const uint8_t* stacked_row(const KernelParams& p, int64_t frame_off,
                                                       int row) {
@@ -172,37 +247,75 @@ __device__ __forceinline__ const uint8_t* stacked_row(const KernelParams& p, int
     return p.bot + frame_off + static_cast<int64_t>(row) * p.in_pitch;
 }
 
+// Order-preserving key of a double (sobel5_minmax, include/sobel5_gpu.h).
+__host__ __device__ __forceinline__ unsigned long long dkey_bits(unsigned long long b) {
+    return b ^ ((b >> 63) ? ~0ull : (1ull << 63));
+}
+__device__ __forceinline__ unsigned long long dkey(double v) {
+    return dkey_bits(static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+__device__ __forceinline__ double dkey_value(unsigned long long k) {
+    const unsigned long long b = (k >> 63) ? (k ^ (1ull << 63)) : ~k;
+    return __longlong_as_double(static_cast<long long>(b));
+}
+
+// normalize export of a double magnitude (image_io.hpp:249-253), exact
+// reference operation order: lround((v - lo) * 255.0 / span), 0 if span <= 0.
+__device__ __forceinline__ uint32_t normalize_u8(double g, double lo, double span) {
+    if (!(span > 0.0)) return 0u;
+    const double mapped = __ddiv_rn(__dmul_rn(__dsub_rn(g, lo), 255.0), span);
+    return static_cast<uint32_t>(static_cast<long long>(round(mapped)));
+}
+
 // The fused streaming kernel.
 //   PF     : 0 = load each row when it is consumed (Prefetch::off);
 //            1 = the next row's load is issued before the current row is
 //                processed (Prefetch::on, the paper's Eq. 9 mod-6 ring);
 //   TAPS   : KernelParams (runtime taps) or DefaultTaps (compile-time);
-//   MAG    : MagMode.
-template <int PF, class TAPS, int MAG>
+//   MAG    : MagMode;
+//   PAD    : fused pad_replicate(img, 2) (same-size output) vs valid mode.
+template <int PF, class TAPS, int MAG, bool PAD>
 __global__ void __launch_bounds__(kCtaThreads)
     sobel5_stream_kernel(const __grid_constant__ KernelParams p) {
     const TapSource<TAPS> T{p};
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int x0 = (blockIdx.x * kCtaWarps + warp) * kWarpCols + lane * 4;
-    if ((x0 - lane * 4) >= p.out_w) return;  // whole warp right of the image
+    const int warp_x0 = (blockIdx.x * kCtaWarps + warp) * kWarpCols;
+    const int x0 = warp_x0 + lane * 4;
+    if (warp_x0 >= p.out_w) return;  // whole warp right of the image
     const int oy0 = blockIdx.y * p.band;
     const int n_out = min(p.band, p.out_h - oy0);
     const int n_in = n_out + 4;
     const int64_t in_frame = static_cast<int64_t>(blockIdx.z) * p.in_frame_stride;
     const int64_t out_frame = static_cast<int64_t>(blockIdx.z) * p.out_frame_stride;
     const bool load_a = x0 < p.width;
-    const bool load_b = lane == 31 && x0 + 4 < p.width;
+    const int xoff = (PAD && lane == 0) ? -4 : 4;
+    const bool load_b = (lane == 31 && x0 + 4 < p.width) || (PAD && lane == 0 && x0 > 0);
     const bool full = x0 + 3 < p.out_w;
+    const PadEdge pe = PAD ? pad_edge_setup(p.width, warp_x0) : PadEdge{0, 0, 0, 0u};
+    double n_lo = 0.0, n_span = 0.0;
+    if (p.u8_norm) {
+        n_lo = p.norm[blockIdx.z].lo;
+        n_span = p.norm[blockIdx.z].span;
+    }
+    unsigned long long g_min = ~0ull, g_max = 0ull;  // order keys of g
+
+    auto row_ptr = [&](int r) -> const uint8_t* {
+        if (PAD) {
+            const int y = min(max(oy0 + r - 2, 0), p.mid_rows - 1);
+            return p.mid + in_frame + static_cast<int64_t>(y) * p.in_pitch;
+        }
+        return stacked_row(p, in_frame, oy0 + r);
+    };
 
     // Pending vertical accumulators, slot = (output row) mod 5.
     uint32_t acc_x[5][4], acc_y[5][4], acc_p[5][4], acc_m[5][4];
 
     uint32_t nxt_a = 0, nxt_b = 0;
     if (PF) {
-        const uint8_t* rp = stacked_row(p, in_frame, oy0);
+        const uint8_t* rp = row_ptr(0);
         nxt_a = load_a ? ld_row_word(rp + x0) : 0u;
-        nxt_b = load_b ? ld_row_word(rp + x0 + 4) : 0u;
+        nxt_b = load_b ? ld_row_word(rp + x0 + xoff) : 0u;
     }
 
     for (int base = 0; base < n_in; base += 5) {
@@ -210,23 +323,23 @@ __global__ void __launch_bounds__(kCtaThreads)
         for (int s = 0; s < 5; ++s) {
             const int r = base + s;
             if (r >= n_in) break;
-            uint32_t wa, wb;
+            uint32_t oa, ob;
             if (PF) {
-                wa = nxt_a;
-                wb = nxt_b;
+                oa = nxt_a;
+                ob = nxt_b;
                 if (r + 1 < n_in) {
-                    const uint8_t* rp = stacked_row(p, in_frame, oy0 + r + 1);
+                    const uint8_t* rp = row_ptr(r + 1);
                     nxt_a = load_a ? ld_row_word(rp + x0) : 0u;
-                    nxt_b = load_b ? ld_row_word(rp + x0 + 4) : 0u;
+                    nxt_b = load_b ? ld_row_word(rp + x0 + xoff) : 0u;
                 }
             } else {
-                const uint8_t* rp = stacked_row(p, in_frame, oy0 + r);
-                wa = load_a ? ld_row_word(rp + x0) : 0u;
-                wb = load_b ? ld_row_word(rp + x0 + 4) : 0u;
+                const uint8_t* rp = row_ptr(r);
+                oa = load_a ? ld_row_word(rp + x0) : 0u;
+                ob = load_b ? ld_row_word(rp + x0 + xoff) : 0u;
             }
-            // Column sharing: the 4 pixels right of this lane's word.
-            const uint32_t sh = __shfl_down_sync(0xffffffffu, wa, 1);
-            if (lane != 31) wb = sh;
+            // Column sharing: the neighbour words come by warp shuffle.
+            uint32_t wa, wb;
+            row_window<PAD>(oa, ob, lane, x0, p.width, pe, wa, wb);
 
             uint32_t px[8];
 #pragma unroll
@@ -352,6 +465,17 @@ __global__ void __launch_bounds__(kCtaThreads)
                             S = __dadd_rn(S, __dmul_rn(dt, dt));
                             g[j] = __dsqrt_rn(S);
                         }
+                        if (p.minmax && x0 + j < p.out_w) {
+                            const unsigned long long b = dkey(g[j]);
+                            g_min = min(g_min, b);
+                            g_max = max(g_max, b);
+                        }
+                    }
+                    uint32_t u[4] = {0u, 0u, 0u, 0u};
+                    if (p.u8) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            u[j] = p.u8_norm ? normalize_u8(g[j], n_lo, n_span) : clamp_abs_u8(g[j]);
                     }
                     if (full) {
                         if (p.g) {
@@ -362,19 +486,15 @@ __global__ void __launch_bounds__(kCtaThreads)
                             st_cs_v4f(p.g32 + row_off, __double2float_rn(g[0]),
                                       __double2float_rn(g[1]), __double2float_rn(g[2]),
                                       __double2float_rn(g[3]));
-                        if (p.u8) {
-                            const uint32_t q = clamp_abs_u8(g[0]) | (clamp_abs_u8(g[1]) << 8) |
-                                               (clamp_abs_u8(g[2]) << 16) |
-                                               (clamp_abs_u8(g[3]) << 24);
-                            st_cs_u32(p.u8 + row_off, q);
-                        }
+                        if (p.u8)
+                            st_cs_u32(p.u8 + row_off, u[0] | (u[1] << 8) | (u[2] << 16) | (u[3] << 24));
                     } else {
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
                             if (x0 + j < p.out_w) {
                                 if (p.g) p.g[row_off + j] = g[j];
                                 if (p.g32) p.g32[row_off + j] = __double2float_rn(g[j]);
-                                if (p.u8) p.u8[row_off + j] = static_cast<uint8_t>(clamp_abs_u8(g[j]));
+                                if (p.u8) p.u8[row_off + j] = static_cast<uint8_t>(u[j]);
                             }
                         }
                     }
@@ -382,27 +502,17 @@ __global__ void __launch_bounds__(kCtaThreads)
             }
         }
     }
-}
-
-// Device-side synth_random (synth.hpp:11-35), random-access form:
-// pixel i = byte (i mod 8) of splitmix64 output word floor(i/8), where word
-// k is mix(seed + (k+1) * 0x9E3779B97F4A7C15).
-__device__ __forceinline__ uint64_t splitmix64_mix(uint64_t z) {
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-    return z ^ (z >> 31);
-}
-
-__global__ void synth_random_kernel(uint8_t* img, int64_t pitch, int width, int height,
-                                    int64_t row_offset, uint64_t seed, uint8_t mask) {
-    const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y;
-    if (x >= width || y >= height) return;
-    const uint64_t i = static_cast<uint64_t>(row_offset + y) * static_cast<uint64_t>(width) +
-                       static_cast<uint64_t>(x);
-    const uint64_t word = splitmix64_mix(seed + (i / 8 + 1) * 0x9E3779B97F4A7C15ULL);
-    img[static_cast<int64_t>(y) * pitch + x] =
-        static_cast<uint8_t>((word >> (8 * (i % 8))) & 0xff) & mask;
+    if (p.minmax) {  // normalize pass 1: frame min / max of g
+        for (int o = 16; o > 0; o >>= 1) {
+            g_min = min(g_min, __shfl_xor_sync(0xffffffffu, g_min, o));
+            g_max = max(g_max, __shfl_xor_sync(0xffffffffu, g_max, o));
+        }
+        if (lane == 0 && g_min <= g_max) {
+            sobel5_minmax* mm = p.minmax + blockIdx.z;
+            atomicMin(reinterpret_cast<unsigned long long*>(&mm->lo_key), g_min);
+            atomicMax(reinterpret_cast<unsigned long long*>(&mm->hi_key), g_max);
+        }
+    }
 }
 
 }  // namespace sobel5_b200

@@ -37,7 +37,7 @@ def lib():
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "sobel5_gpu.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(sobel5_[a-z0-9_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(sobel[35]_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol(lib):
