@@ -257,6 +257,7 @@ def main():
     ow, oh = w - 4, h - 4
     planes_names = CONTRACT_PLANES[a.contract]
     taps = api.make_stream_taps()
+    taps_default = True  # (1, 2, 6, 4): the packed kernel (sobel5_packed.cuh)
     stream = torch.cuda.current_stream(dev)
     s_ptr = stream.cuda_stream
 
@@ -347,30 +348,58 @@ def main():
         except Exception:
             traffic = None
 
-    # ---- variants (same workload, other output contracts / prefetch off) ----
+    # ---- variants (same workload, other output contracts / paths) ----
+    # Each is timed like the headline (CUDA events around n launches on the
+    # launching stream, inputs rotated over > L2); bytes are algorithmic
+    # (input read once + outputs written once).
     variants = {}
     if rank == 0 and frames == 1 and a.workload != "32k-bands":
-        for name, contract, pf in (("u8", "u8", 1), ("sr32", "sr32", 1), ("sr_prefetch_off",
-                                                                          "sr", 0)):
-            if contract == a.contract and pf == a.prefetch:
-                continue
-            vo, vp = api.alloc_planes(ow, oh, CONTRACT_PLANES[contract], dev)
+        scratch = api.alloc_scratch(1, dev, out_h=h, pitch=api.round_up(w, 32))
+
+        def variant(name, planes_names_v, out_w_v, out_h_v, out_bytes_px, call, passes=1):
+            vo, vp = api.alloc_planes(out_w_v, out_h_v, planes_names_v, dev)
             for i in range(5):
-                api.launch(ins[i % n_in], pitch, w, h, taps, pf, vo, vp, stream=s_ptr)
+                call(ins[i % n_in], vo, vp)
             torch.cuda.synchronize()
             v0, v1 = torch.cuda.Event(True), torch.cuda.Event(True)
             v0.record(stream)
             n = 50
             for i in range(n):
-                api.launch(ins[i % n_in], pitch, w, h, taps, pf, vo, vp, stream=s_ptr)
+                call(ins[i % n_in], vo, vp)
             v1.record(stream)
             torch.cuda.synchronize()
             vms = v0.elapsed_time(v1) / n
-            vb = w * h + ow * oh * OUT_BYTES[contract]
+            vb = w * h + out_w_v * out_h_v * out_bytes_px
             variants[name] = {"gpx_s": w * h / vms / 1e6, "us": vms * 1e3,
                               "hbm_gbs": vb / vms / 1e6, "frac": vb / vms / 1e6 / hbm_peak,
-                              "alg_bytes": vb}
+                              "alg_bytes": vb, "kernel_passes": passes}
             del vo
+
+        for name, contract, pf in (("u8", "u8", 1), ("sr32", "sr32", 1),
+                                   ("sr_prefetch_off", "sr", 0)):
+            if contract == a.contract and pf == a.prefetch:
+                continue
+            variant(name, CONTRACT_PLANES[contract], ow, oh, OUT_BYTES[contract],
+                    lambda d, vo, vp, pf=pf: api.launch(d, pitch, w, h, taps, pf, vo, vp,
+                                                        stream=s_ptr))
+        # detect path: replicate padding fused, same-size
+        # u8 edge map; normalize = 2 stencil passes + threshold table
+        variant("detect_pad_clamp_abs", ("u8",), w, h, 1,
+                lambda d, vo, vp: api.detect_device(d, pitch, w, h, taps, 1, True,
+                                                    api.SaveMode.clamp_abs, vo, vp, scratch,
+                                                    stream=s_ptr))
+        variant("detect_pad_normalize", ("u8",), w, h, 1,
+                lambda d, vo, vp: api.detect_device(d, pitch, w, h, taps, 1, True,
+                                                    api.SaveMode.normalize, vo, vp, scratch,
+                                                    stream=s_ptr), passes=2)
+        variant("sr_pad", CONTRACT_PLANES["sr"], w, h, OUT_BYTES["sr"],
+                lambda d, vo, vp: api.launch_ex(d, pitch, w, h, taps, 1, True, vo, vp,
+                                                stream=s_ptr))
+        # 3x3 operator: Stream3Result gx+gy (int32) + g (f64)
+        variant("sobel3_sr", ("gx", "gy", "g"), w - 2, h - 2, 16,
+                lambda d, vo, vp: api.launch3(d, pitch, w, h, 1, False, vo, vp, stream=s_ptr))
+        variant("sobel3_u8", ("u8",), w - 2, h - 2, 1,
+                lambda d, vo, vp: api.launch3(d, pitch, w, h, 1, False, vo, vp, stream=s_ptr))
         torch.cuda.empty_cache()
 
     # ---- e2e through the C ABI host entry with pinned buffers ----
@@ -432,7 +461,9 @@ def main():
                          "frac": achieved / hbm_peak, "traffic": traffic,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
                          if peak_kind == "measured" else "fallback (B200_PROFILING.md)",
-                         "alg_bytes_per_launch": alg_bytes, "kernel": "sobel5_stream_kernel",
+                         "alg_bytes_per_launch": alg_bytes,
+                         "kernel": "sobel5_packed_default_kernel" if taps_default
+                         else "sobel5_stream_kernel",
                          "kernel_us": ms_step * 1e3},
             "gpu_launches": launches,
             "clocks": clocks.summary(),

@@ -182,17 +182,22 @@ sobel5_status sobel5_launch_ex(const uint8_t* d_in, int64_t in_pitch, int64_t in
                                int prefetch, int pad, const sobel5_planes* d_out,
                                int64_t out_frame_stride, sobel5_diag* d_diag, void* stream);
 
-/* Bytes of device scratch sobel5_detect / sobel5_quantize_plane need
- * (16-byte aligned; normalize only). */
-size_t sobel5_detect_scratch_bytes(int n_frames);
+/* Bytes of device scratch the normalize export needs (256-byte aligned):
+ * per-frame min/max and threshold table plus a uint32 plane of the exact
+ * integer g^2 with the output planes' pitch / frame stride (elements).
+ * sobel5_quantize_plane needs sobel5_detect_scratch_bytes(0, 0, 0, 1). */
+size_t sobel5_detect_scratch_bytes(int out_h, int64_t pitch, int64_t out_frame_stride,
+                                   int n_frames);
 
 /* The detect export: u8 = quantize(g, save_mode) (image_io.hpp:233-256) of
  * the (optionally padded) image; save_mode 0 = clamp_abs, 1 = normalize
  * (the CLI default, sobel5_cli.cpp:177).  d_out->u8 is required; any other
  * non-NULL plane of d_out is written too (the --dump-planes source).
- * normalize runs pass 1 (planes + per-frame min/max of g), a threshold
- * table, and pass 2 (u8 through the table); bit-exact with the reference's
- * double arithmetic. */
+ * normalize runs pass 1 (stencil: planes, per-frame min/max of g and, for
+ * integer magnitudes, the g^2 plane into scratch), a threshold table, and
+ * pass 2 (u8 from the g^2 plane through the table; non-integer magnitudes
+ * re-run the stencil instead); bit-exact with the reference's double
+ * arithmetic. */
 sobel5_status sobel5_detect(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
                             int width, int height, int n_frames, const sobel5_taps* taps,
                             int prefetch, int pad, int save_mode, const sobel5_planes* d_out,

@@ -137,7 +137,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.sobel5_launch_ex.argtypes = [vp, i64, i64, i32, i32, i32, C.POINTER(Taps), i32, i32,
                                    C.POINTER(Planes), i64, vp, vp]
     L.sobel5_launch_ex.restype = i32
-    L.sobel5_detect_scratch_bytes.argtypes = [i32]
+    L.sobel5_detect_scratch_bytes.argtypes = [i32, i64, i64, i32]
     L.sobel5_detect_scratch_bytes.restype = C.c_size_t
     L.sobel5_detect.argtypes = [vp, i64, i64, i32, i32, i32, C.POINTER(Taps), i32, i32, i32,
                                 C.POINTER(Planes), i64, vp, vp, vp]

@@ -438,10 +438,12 @@ def pad_replicate(img: np.ndarray, radius: int) -> PaddedPlane:
     return PaddedPlane(np.pad(img, radius, mode="edge"), radius, img)
 
 
-def alloc_scratch(frames: int = 1, device="cuda"):
-    """Device scratch for normalize (sobel5_detect_scratch_bytes)."""
+def alloc_scratch(frames: int = 1, device="cuda", out_h: int = 0, pitch: int = 0,
+                  out_frame_stride: int = 0):
+    """Device scratch for normalize (sobel5_detect_scratch_bytes): per-frame
+    min/max + tables, plus the g^2 plane for an out_h x pitch output."""
     import torch
-    n = int(_abi.load().sobel5_detect_scratch_bytes(frames))
+    n = int(_abi.load().sobel5_detect_scratch_bytes(out_h, pitch, out_frame_stride, frames))
     return torch.empty(n, dtype=torch.uint8, device=device)
 
 
@@ -500,7 +502,7 @@ def quantize(plane: np.ndarray, mode: SaveMode) -> np.ndarray:
     h, w = plane.shape
     d = torch.from_numpy(plane).cuda()
     u8 = torch.empty((h, w), dtype=torch.uint8, device="cuda")
-    quantize_device(d, w, w, h, mode, u8, w, alloc_scratch(1))
+    quantize_device(d, w, w, h, mode, u8, w, alloc_scratch(1))  # min/max + table only
     torch.cuda.synchronize()
     return u8.cpu().numpy()
 

@@ -28,6 +28,7 @@ cudaError_t outs(const KernelParams& kp, dim3 grid, cudaStream_t s) {
         case kOut3: return go<PF, PAD, kOut3>(kp, grid, s);
         case kOutU8: return go<PF, PAD, kOutU8>(kp, grid, s);
         case kOutMinMax: return go<PF, PAD, kOutMinMax>(kp, grid, s);
+        case kOutMinMax | kOutS32: return go<PF, PAD, kOutMinMax | kOutS32>(kp, grid, s);
         case kOutU8 | kOutNorm: return go<PF, PAD, kOutU8 | kOutNorm>(kp, grid, s);
         default: return go<PF, PAD, kOutRuntime>(kp, grid, s);
     }
@@ -76,6 +77,7 @@ sobel5_status sobel3_common(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
     kp.minmax = ex.minmax;
     kp.norm = ex.norm;
     kp.u8_norm = ex.u8_norm;
+    kp.s32 = ex.s32;
     unsigned gy = static_cast<unsigned>((out_h + kp.band - 1) / kp.band);
     if (gy > 65535u) {
         kp.band = (out_h + 65534) / 65535;

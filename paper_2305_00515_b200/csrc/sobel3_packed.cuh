@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
     const bool w_u8 = RT ? p.u8 != nullptr : (OUTS & kOutU8) != 0;
     const bool w_mm = RT ? p.minmax != nullptr : (OUTS & kOutMinMax) != 0;
     const bool u8_norm = RT ? p.u8_norm != 0 : (OUTS & kOutNorm) != 0;
+    const bool w_s = RT ? p.s32 != nullptr : (OUTS & kOutS32) != 0;
     const bool need_g = w_g || w_g32;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -63,17 +64,23 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
     const bool full = x0 + 3 < p.out_w;
     const PadEdge pe = PAD ? pad_edge_setup(p.width, warp_x0) : PadEdge{0, 0, 0, 0u};
 
-    auto row_ptr = [&](int r) -> const uint8_t* {
-        int y = oy0 + r;
-        if (PAD) y = min(max(y - 1, 0), p.mid_rows - 1);  // image_io.hpp:285
-        return p.mid + in_frame + static_cast<int64_t>(y) * p.in_pitch + x0;
-    };
+    // rows load in order: a running pointer (valid mode) or the clamped row
+    // of pad_replicate(img, 1) (image_io.hpp:285)
+    const uint8_t* plain = p.mid + in_frame + static_cast<int64_t>(oy0) * p.in_pitch + x0;
     auto load_row = [&](int r, uint32_t& a, uint32_t& b) {
-        const uint8_t* rp = row_ptr(r);
+        const uint8_t* rp;
+        if (PAD) {
+            const int y = min(max(oy0 + r - 1, 0), p.mid_rows - 1);
+            rp = p.mid + in_frame + static_cast<int64_t>(y) * p.in_pitch + x0;
+        } else {
+            rp = plain;
+            plain += p.in_pitch;
+        }
         a = load_a ? ld_row_word(rp) : 0u;
         b = load_b ? ld_row_word(rp + xoff) : 0u;
     };
 
+    int64_t out_off = out_frame + static_cast<int64_t>(oy0) * p.pitch + x0;
     constexpr int kRing = 6;  // multiple of the 3-row accumulator window
     uint32_t ax[3][2], ay[3][2];
     uint32_t qa[kRing], qb[kRing];
@@ -124,7 +131,6 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                 ay[s2][q] += hh;
             }
             if (r >= 2) {
-                const int v = r - 2;
                 int32_t gx[4], gy[4];
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
@@ -133,7 +139,8 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                     gy[q] = lane_lo(ay[s2][q]);
                     gy[q + 2] = lane_hi(ay[s2][q]);
                 }
-                const int64_t row_off = out_frame + static_cast<int64_t>(oy0 + v) * p.pitch + x0;
+                const int64_t row_off = out_off;
+                out_off += p.pitch;
                 uint32_t S[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
@@ -145,6 +152,15 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                             s_min = min(s_min, S[j]);
                             s_max = max(s_max, S[j]);
                         }
+                }
+                if (w_s) {
+                    if (full) {
+                        *reinterpret_cast<uint4*>(p.s32 + row_off) = make_uint4(S[0], S[1], S[2], S[3]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (x0 + j < p.out_w) p.s32[row_off + j] = S[j];
+                    }
                 }
                 double g[4] = {0.0, 0.0, 0.0, 0.0};
                 if (need_g) {
@@ -165,7 +181,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                         st_cs_v4f(p.g32 + row_off, __double2float_rn(g[0]), __double2float_rn(g[1]),
                                   __double2float_rn(g[2]), __double2float_rn(g[3]));
                     if (w_u8)
-                        st_cs_u32(p.u8 + row_off, u[0] | (u[1] << 8) | (u[2] << 16) | (u[3] << 24));
+                        st_cs_u32(p.u8 + row_off, pack_u8x4(u[0], u[1], u[2], u[3]));
                 } else {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {

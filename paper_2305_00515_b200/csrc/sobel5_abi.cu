@@ -175,6 +175,9 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     const int out_h = static_cast<int>(ex.pad ? rows : rows - 4);
     if (sobel5_status st = check_planes(out, out_w); st != SOBEL5_OK) return st;
     if (ex.u8_norm && (!ex.norm || !out->u8)) return SOBEL5_INVALID_ARG;
+    // the S plane exists only for integer magnitudes (packed default taps)
+    if (ex.s32 && !(taps_are_default(*taps) && env_int("SOBEL5_GENERIC", 0) == 0))
+        return SOBEL5_INVALID_ARG;
     if (rows > (int64_t{1} << 30) || frames > 65535) return SOBEL5_INVALID_ARG;
 
     KernelParams kp{};
@@ -204,6 +207,7 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     kp.minmax = ex.minmax;
     kp.norm = ex.norm;
     kp.u8_norm = ex.u8_norm;
+    kp.s32 = ex.s32;
     fill_taps(kp, *taps);
 
     const dim3 grid(static_cast<unsigned>((out_w + kCtaCols - 1) / kCtaCols),

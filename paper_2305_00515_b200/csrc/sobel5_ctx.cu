@@ -246,7 +246,8 @@ sobel5_status sobel5_detect_host(sobel5_ctx* ctx, const uint8_t* h_in, int width
                   static_cast<size_t>(dpitch) * out_h * kElem[i]));
         *dslots[i] = ctx->d_plane[i];
     }
-    CK(ensure(&ctx->d_scratch, &ctx->d_scratch_bytes, sobel5_detect_scratch_bytes(1)));
+    CK(ensure(&ctx->d_scratch, &ctx->d_scratch_bytes,
+              sobel5_detect_scratch_bytes(out_h, dpitch, 0, 1)));
     CK(cudaMemsetAsync(ctx->d_diag, 0, sizeof(sobel5_diag), ctx->s_comp));
     CK(cudaMemcpy2DAsync(ctx->d_in, in_pitch, h_in, width, width, height, cudaMemcpyHostToDevice,
                          ctx->s_comp));

@@ -15,8 +15,10 @@
 //   pass 2 : stencil, u8 = normalize(g) through the table
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "sobel5_gpu.h"
 #include "sobel5_internal.h"
@@ -30,10 +32,18 @@ constexpr size_t kAlign = 256;
 
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
+// Scratch layout: [minmax x frames][norm_table x frames][S plane (u32, the
+// output planes' pitch and frame stride)].
+size_t head_bytes(int frames) {
+    return align_up(align_up(sizeof(sobel5_minmax) * frames) + sizeof(sobel5_norm_table) * frames);
+}
 sobel5_minmax* scratch_minmax(void* s) { return static_cast<sobel5_minmax*>(s); }
 sobel5_norm_table* scratch_table(void* s, int frames) {
     return reinterpret_cast<sobel5_norm_table*>(static_cast<char*>(s) +
                                                 align_up(sizeof(sobel5_minmax) * frames));
+}
+uint32_t* scratch_s32(void* s, int frames) {
+    return reinterpret_cast<uint32_t*>(static_cast<char*>(s) + head_bytes(frames));
 }
 
 __global__ void minmax_init_kernel(sobel5_minmax* mm, int frames) {
@@ -72,16 +82,47 @@ __global__ void norm_table_kernel(const sobel5_minmax* mm, sobel5_norm_table* ta
             const uint32_t s_hi = static_cast<uint32_t>(llrint(hi * hi));
             auto u_of = [&](uint32_t S) { return normalize_u8(sqrt_u30(S), lo, span); };
             if (u_of(s_hi) >= static_cast<uint32_t>(k)) {
-                uint32_t a = s_lo, b = s_hi;  // u(b) >= k
-                while (a < b) {
-                    const uint32_t c = a + (b - a) / 2;
-                    if (u_of(c) >= static_cast<uint32_t>(k)) b = c;
-                    else a = c + 1;
-                }
+                // lround(m) >= k  <=>  m >= k - 1/2 (m >= 0): the real-valued
+                // threshold seeds a short walk on the exact double map
+                const double g = lo + (k - 0.5) * span / 255.0;
+                double seed = ceil(g * g);
+                seed = fmin(fmax(seed, static_cast<double>(s_lo)), static_cast<double>(s_hi));
+                uint32_t a = static_cast<uint32_t>(seed);
+                while (a > s_lo && u_of(a - 1) >= static_cast<uint32_t>(k)) --a;
+                while (u_of(a) < static_cast<uint32_t>(k)) ++a;  // terminates: u(s_hi) >= k
                 thr = a;
             }
         }
         t->thr[k] = thr;
+    }
+}
+
+// Normalize pass 2 of the detect path (integer magnitudes): u8 from the S
+// plane written by pass 1, 4 pixels per thread (16-byte load, 4-byte store).
+__global__ void norm_map_kernel(const uint32_t* __restrict__ s32, int64_t pitch,
+                                int64_t frame_stride, int out_w, int out_h,
+                                const sobel5_norm_table* __restrict__ tab, uint8_t* __restrict__ u8) {
+    __shared__ uint32_t s_thr[257];
+    const sobel5_norm_table* t = tab + blockIdx.z;
+    for (int i = threadIdx.x; i < 257; i += blockDim.x) s_thr[i] = t->thr[i];
+    const float lo_f = t->lo_f, scale_f = t->scale_f;
+    __syncthreads();
+    const int x = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (x >= out_w) return;
+    const int64_t base = static_cast<int64_t>(blockIdx.z) * frame_stride + x;
+    for (int y = blockIdx.y; y < out_h; y += gridDim.y) {
+        const int64_t o = base + static_cast<int64_t>(y) * pitch;
+        const uint4 S = __ldcs(reinterpret_cast<const uint4*>(s32 + o));
+        const uint32_t u0 = u8_normalize_s(S.x, s_thr, lo_f, scale_f);
+        const uint32_t u1 = u8_normalize_s(S.y, s_thr, lo_f, scale_f);
+        const uint32_t u2 = u8_normalize_s(S.z, s_thr, lo_f, scale_f);
+        const uint32_t u3 = u8_normalize_s(S.w, s_thr, lo_f, scale_f);
+        if (x + 3 < out_w) {
+            st_cs_u32(u8 + o, pack_u8x4(u0, u1, u2, u3));
+        } else {
+            const uint32_t u[4] = {u0, u1, u2, u3};
+            for (int j = 0; j < 4 && x + j < out_w; ++j) u8[o + j] = static_cast<uint8_t>(u[j]);
+        }
     }
 }
 
@@ -143,6 +184,56 @@ sobel5_status run_init(sobel5_minmax* mm, int frames, cudaStream_t s) {
     return map_cuda(cudaGetLastError());
 }
 
+int env_int_(const char* name) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : 0;
+}
+
+// normalize export (image_io.hpp:242-255) around a stencil launcher:
+//   exact (integer S): init, pass 1 = stencil + planes + S plane + min/max,
+//     table, pass 2 = S plane -> u8 (memory-bound map, no stencil rerun);
+//   otherwise: init, pass 1 = stencil + planes + min/max, table (lo, span),
+//     pass 2 = stencil again with the direct double formula.
+template <class Launch>
+sobel5_status detect_normalize(void* scratch, int frames, bool exact, const sobel5_planes* d_out,
+                               int64_t out_frame_stride, void* stream, Launch&& launch,
+                               const LaunchExtra& ex, sobel5_diag* d_diag, int out_w, int out_h) {
+    if (out_w < 1 || out_h < 1) {
+        // let the launcher report the reference's error for the size
+        sobel5_planes none = *d_out;
+        return launch(&none, ex, d_diag);
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    sobel5_minmax* mm = scratch_minmax(scratch);
+    sobel5_norm_table* tab = scratch_table(scratch, frames);
+    sobel5_planes p1 = *d_out;
+    p1.u8 = nullptr;
+    sobel5_planes p2{};
+    p2.u8 = d_out->u8;
+    p2.pitch = d_out->pitch;
+    if (sobel5_status st = run_init(mm, frames, s); st != SOBEL5_OK) return st;
+    LaunchExtra e1 = ex;
+    e1.minmax = mm;
+    if (exact) e1.s32 = scratch_s32(scratch, frames);
+    if (sobel5_status st = launch(&p1, e1, d_diag); st != SOBEL5_OK) return st;
+    norm_table_kernel<<<frames, 256, 0, s>>>(mm, tab, exact ? 1 : 0);
+    count_launch();
+    if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return map_cuda(e);
+    if (exact) {
+        const dim3 grid(static_cast<unsigned>((out_w + 4 * 128 - 1) / (4 * 128)),
+                        static_cast<unsigned>(std::min(out_h, 65535)),
+                        static_cast<unsigned>(frames));
+        norm_map_kernel<<<grid, 128, 0, s>>>(e1.s32, d_out->pitch, out_frame_stride, out_w, out_h,
+                                             tab, d_out->u8);
+        count_launch();
+        return map_cuda(cudaGetLastError());
+    }
+    LaunchExtra e2 = ex;
+    e2.norm = tab;
+    e2.u8_norm = 1;
+    return launch(&p2, e2, nullptr);
+}
+
 }  // namespace
 
 extern "C" {
@@ -157,9 +248,11 @@ sobel5_status sobel5_launch_ex(const uint8_t* d_in, int64_t in_pitch, int64_t in
                          n_frames, taps, prefetch, d_out, out_frame_stride, d_diag, stream, ex);
 }
 
-size_t sobel5_detect_scratch_bytes(int n_frames) {
-    if (n_frames < 1) return 0;
-    return align_up(sizeof(sobel5_minmax) * n_frames) + sizeof(sobel5_norm_table) * n_frames;
+size_t sobel5_detect_scratch_bytes(int out_h, int64_t pitch, int64_t out_frame_stride,
+                                   int n_frames) {
+    if (n_frames < 1 || out_h < 0 || pitch < 0) return 0;
+    const int64_t plane = (n_frames - 1) * out_frame_stride + static_cast<int64_t>(out_h) * pitch;
+    return head_bytes(n_frames) + static_cast<size_t>(plane) * sizeof(uint32_t);
 }
 
 sobel5_status sobel5_detect(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
@@ -174,35 +267,15 @@ sobel5_status sobel5_detect(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
     if (save_mode == 0)  // clamp_abs: one fused launch
         return launch_common(nullptr, d_in, nullptr, in_pitch, in_frame_stride, width, height,
                              n_frames, taps, prefetch, d_out, out_frame_stride, d_diag, stream, ex);
-    if (!d_scratch || reinterpret_cast<uintptr_t>(d_scratch) % 16 != 0) return SOBEL5_INVALID_ARG;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    sobel5_minmax* mm = scratch_minmax(d_scratch);
-    sobel5_norm_table* tab = scratch_table(d_scratch, n_frames);
-    // validate before any launch: a dry check through pass 2's arguments
-    sobel5_planes p2{};
-    p2.u8 = d_out->u8;
-    p2.pitch = d_out->pitch;
-    // pass 1: requested planes (u8 excluded) + min/max of g
-    sobel5_planes p1 = *d_out;
-    p1.u8 = nullptr;
-    if (sobel5_status st = run_init(mm, n_frames, s); st != SOBEL5_OK) return st;
-    LaunchExtra e1 = ex;
-    e1.minmax = mm;
-    sobel5_status st = launch_common(nullptr, d_in, nullptr, in_pitch, in_frame_stride, width,
-                                     height, n_frames, taps, prefetch, &p1, out_frame_stride,
-                                     d_diag, stream, e1);
-    if (st != SOBEL5_OK) return st;
-    // thresholds: exact for integer sums of squares (the packed default-taps
-    // kernel); the generic kernel maps g with the direct double formula
-    const bool dflt = taps && taps_default(taps);
-    norm_table_kernel<<<n_frames, 256, 0, s>>>(mm, tab, dflt ? 1 : 0);
-    count_launch();
-    if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return map_cuda(e);
-    LaunchExtra e2 = ex;
-    e2.norm = tab;
-    e2.u8_norm = 1;
-    return launch_common(nullptr, d_in, nullptr, in_pitch, in_frame_stride, width, height,
-                         n_frames, taps, prefetch, &p2, out_frame_stride, nullptr, stream, e2);
+    if (!d_scratch || reinterpret_cast<uintptr_t>(d_scratch) % 256 != 0) return SOBEL5_INVALID_ARG;
+    const bool exact = taps && taps_default(taps) && env_int_("SOBEL5_GENERIC") == 0;
+    return detect_normalize(
+        d_scratch, n_frames, exact, d_out, out_frame_stride, stream,
+        [&](const sobel5_planes* planes, const LaunchExtra& e, sobel5_diag* dg) {
+            return launch_common(nullptr, d_in, nullptr, in_pitch, in_frame_stride, width, height,
+                                 n_frames, taps, prefetch, planes, out_frame_stride, dg, stream, e);
+        },
+        ex, d_diag, pad ? width : width - 4, pad ? height : height - 4);
 }
 
 sobel5_status sobel3_detect(const uint8_t* d_in, int64_t in_pitch, int64_t in_frame_stride,
@@ -216,29 +289,14 @@ sobel5_status sobel3_detect(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
     if (save_mode == 0)
         return sobel3_common(d_in, in_pitch, in_frame_stride, width, height, n_frames, prefetch,
                              d_out, out_frame_stride, stream, ex);
-    if (!d_scratch || reinterpret_cast<uintptr_t>(d_scratch) % 16 != 0) return SOBEL5_INVALID_ARG;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    sobel5_minmax* mm = scratch_minmax(d_scratch);
-    sobel5_norm_table* tab = scratch_table(d_scratch, n_frames);
-    sobel5_planes p1 = *d_out;
-    p1.u8 = nullptr;
-    sobel5_planes p2{};
-    p2.u8 = d_out->u8;
-    p2.pitch = d_out->pitch;
-    if (sobel5_status st = run_init(mm, n_frames, s); st != SOBEL5_OK) return st;
-    LaunchExtra e1 = ex;
-    e1.minmax = mm;
-    sobel5_status st = sobel3_common(d_in, in_pitch, in_frame_stride, width, height, n_frames,
-                                     prefetch, &p1, out_frame_stride, stream, e1);
-    if (st != SOBEL5_OK) return st;
-    norm_table_kernel<<<n_frames, 256, 0, s>>>(mm, tab, 1);
-    count_launch();
-    if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return map_cuda(e);
-    LaunchExtra e2 = ex;
-    e2.norm = tab;
-    e2.u8_norm = 1;
-    return sobel3_common(d_in, in_pitch, in_frame_stride, width, height, n_frames, prefetch, &p2,
-                         out_frame_stride, stream, e2);
+    if (!d_scratch || reinterpret_cast<uintptr_t>(d_scratch) % 256 != 0) return SOBEL5_INVALID_ARG;
+    return detect_normalize(
+        d_scratch, n_frames, true, d_out, out_frame_stride, stream,
+        [&](const sobel5_planes* planes, const LaunchExtra& e, sobel5_diag*) {
+            return sobel3_common(d_in, in_pitch, in_frame_stride, width, height, n_frames,
+                                 prefetch, planes, out_frame_stride, stream, e);
+        },
+        ex, nullptr, pad ? width : width - 2, pad ? height : height - 2);
 }
 
 sobel5_status sobel5_quantize_plane(const void* d_plane, int kind, int64_t pitch, int width,

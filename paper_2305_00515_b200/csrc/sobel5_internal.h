@@ -27,6 +27,7 @@ struct LaunchExtra {
     sobel5_minmax* minmax = nullptr;           // normalize pass 1
     const sobel5_norm_table* norm = nullptr;   // normalize pass 2
     int u8_norm = 0;
+    uint32_t* s32 = nullptr;                   // exact g^2 plane (normalize pass 1)
 };
 
 // Common launch path (validation in the reference's order, geometry, kernel

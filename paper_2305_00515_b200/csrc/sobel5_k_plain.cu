@@ -21,6 +21,7 @@ cudaError_t outs(const KernelParams& kp, dim3 grid, cudaStream_t s) {
         case kOutU8: return go<PF, kOutU8>(kp, grid, s);
         case 15 | kOutG32: return go<PF, 15 | kOutG32>(kp, grid, s);
         case kOutMinMax: return go<PF, kOutMinMax>(kp, grid, s);
+        case kOutMinMax | kOutS32: return go<PF, kOutMinMax | kOutS32>(kp, grid, s);
         case kOutU8 | kOutNorm: return go<PF, kOutU8 | kOutNorm>(kp, grid, s);
         default: return go<PF, kOutRuntime>(kp, grid, s);
     }

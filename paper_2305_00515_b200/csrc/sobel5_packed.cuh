@@ -40,7 +40,7 @@ namespace sobel5_b200 {
 // Output-set bits (template OUTS); kOutRuntime checks the plane pointers.
 enum : int {
     kOutGx = 1, kOutGy = 2, kOutGd = 4, kOutGdt = 8, kOutG = 16, kOutG32 = 32, kOutU8 = 64,
-    kOutMinMax = 128, kOutNorm = 256,
+    kOutMinMax = 128, kOutNorm = 256, kOutS32 = 512,
     kOutSR = 31, kOutRuntime = -1
 };
 
@@ -49,7 +49,7 @@ inline int packed_out_set(const KernelParams& kp) {
     return (kp.gx ? kOutGx : 0) | (kp.gy ? kOutGy : 0) | (kp.gd ? kOutGd : 0) |
            (kp.gdt ? kOutGdt : 0) | (kp.g ? kOutG : 0) | (kp.g32 ? kOutG32 : 0) |
            (kp.u8 ? kOutU8 : 0) | (kp.minmax ? kOutMinMax : 0) |
-           (kp.u8 && kp.u8_norm ? kOutNorm : 0);
+           (kp.u8 && kp.u8_norm ? kOutNorm : 0) | (kp.s32 ? kOutS32 : 0);
 }
 
 // Double magnitude of an exact integer sum of squares S < 2^32: IEEE sqrt
@@ -63,13 +63,24 @@ __device__ __forceinline__ double sqrt_u30(uint32_t S) {
 
 // clamp_abs(sqrt(S)) for an integer S, without the double: sqrt(S) is never
 // within 4.9e-4 of k + 0.5 (the nearest case is S = 255*256), and the float
-// estimate S * rsqrt(S) is within 7e-5 of sqrt(S) below 65281 (checked for
-// every S by test_u8_from_s_exhaustive).
+// estimate S * rsqrt(S) (MUFU.RSQ) is within 7e-5 of sqrt(S) below 65281
+// (checked for every 32-bit S on the device by test_u8_from_s_exhaustive).
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// Branch-free: S is clamped to 65280 first (sqrt(65280) = 255.4995 -> 255),
+// which is the saturation of clamp_abs for every larger S.
 __device__ __forceinline__ uint32_t u8_from_s(uint32_t S) {
-    if (S > 65280u) return 255u;  // sqrt(65281) > 255.5
-    const float f = __uint2float_rn(S);
-    const float y = f * rsqrtf(fmaxf(f, 1.0f));
+    const float f = __uint2float_rn(min(S, 65280u));
+    const float y = f * rsqrt_approx(fmaxf(f, 1.0f));
     return static_cast<uint32_t>(__float2int_rn(y));
+}
+
+// Four bytes (each < 256) packed little-endian with two byte permutes.
+__device__ __forceinline__ uint32_t pack_u8x4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
 
 __device__ __forceinline__ int32_t lane_lo(uint32_t v) {
@@ -121,6 +132,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
     const bool w_u8 = RT ? p.u8 != nullptr : (OUTS & kOutU8) != 0;
     const bool w_mm = RT ? p.minmax != nullptr : (OUTS & kOutMinMax) != 0;
     const bool u8_norm = RT ? p.u8_norm != 0 : (OUTS & kOutNorm) != 0;
+    const bool w_s = RT ? p.s32 != nullptr : (OUTS & kOutS32) != 0;
     const bool need_g = w_g || w_g32;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -152,21 +164,29 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
     const bool full = x0 + 3 < p.out_w;
     const PadEdge pe = PAD ? pad_edge_setup(p.width, warp_x0) : PadEdge{0, 0, 0, 0u};
 
-    // row pointer for plain images: advanced by one pitch per row
+    // Plain images: rows are loaded strictly in order, so one running
+    // pointer advanced by the pitch replaces the 64-bit address arithmetic
+    // per row (it is never dereferenced past the band's last row).
     const uint8_t* plain = p.mid + in_frame + static_cast<int64_t>(oy0) * p.in_pitch + x0;
     auto row_ptr = [&](int r) -> const uint8_t* {
         if (SEG) return stacked_row(p, in_frame, oy0 + r) + x0;
-        if (PAD) {  // padded row oy0 + r is image row clamp(oy0 + r - 2, 0, H - 1)
-            const int y = min(max(oy0 + r - 2, 0), p.mid_rows - 1);
-            return p.mid + in_frame + static_cast<int64_t>(y) * p.in_pitch + x0;
-        }
-        return plain + static_cast<int64_t>(r) * p.in_pitch;
+        // PAD: padded row oy0 + r is image row clamp(oy0 + r - 2, 0, H - 1)
+        const int y = min(max(oy0 + r - 2, 0), p.mid_rows - 1);
+        return p.mid + in_frame + static_cast<int64_t>(y) * p.in_pitch + x0;
     };
     auto load_row = [&](int r, uint32_t& a, uint32_t& b) {
-        const uint8_t* rp = row_ptr(r);
+        const uint8_t* rp;
+        if (!SEG && !PAD) {
+            rp = plain;
+            plain += p.in_pitch;
+        } else {
+            rp = row_ptr(r);
+        }
         a = load_a ? ld_row_word(rp) : 0u;
         b = load_b ? ld_row_word(rp + xoff) : 0u;
     };
+    // element offset of the next output row (running, one pitch per row)
+    int64_t out_off = out_frame + static_cast<int64_t>(oy0) * p.pitch + x0;
 
     // pending accumulators [slot = output row mod 5][pair]
     uint32_t ax[5][2], ay[5][2], an[5][2], aq[5][2];
@@ -275,7 +295,6 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
 
             if (r >= 4) {
                 const int sl = (s + 1) % 5;
-                const int v = r - 4;
                 int32_t gx[4], gy[4], gd[4], gdt[4];
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
@@ -291,7 +310,8 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                     gdt[q] = lane_lo(vt);
                     gdt[q + 2] = lane_hi(vt);
                 }
-                const int64_t row_off = out_frame + static_cast<int64_t>(oy0 + v) * p.pitch + x0;
+                const int64_t row_off = out_off;
+                out_off += p.pitch;
                 if (full) {
                     if (w_gx) st_cs_v4(p.gx + row_off, gx[0], gx[1], gx[2], gx[3]);
                     if (w_gy) st_cs_v4(p.gy + row_off, gy[0], gy[1], gy[2], gy[3]);
@@ -308,7 +328,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                         }
                     }
                 }
-                if (need_g || w_u8 || w_mm) {
+                if (need_g || w_u8 || w_mm || w_s) {
                     // exact: every square < 2^28 and the sum < 2^30, so
                     // double(S) equals the reference's double sum of squares
                     uint32_t S[4];
@@ -325,6 +345,15 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                                 s_min = min(s_min, S[j]);
                                 s_max = max(s_max, S[j]);
                             }
+                        }
+                    }
+                    if (w_s) {  // kept in L2 where it fits: pass 2 reads it next
+                        if (full) {
+                            *reinterpret_cast<uint4*>(p.s32 + row_off) = make_uint4(S[0], S[1], S[2], S[3]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                if (x0 + j < p.out_w) p.s32[row_off + j] = S[j];
                         }
                     }
                     double g[4] = {0.0, 0.0, 0.0, 0.0};
@@ -347,8 +376,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                             st_cs_v4f(p.g32 + row_off, __double2float_rn(g[0]),
                                       __double2float_rn(g[1]), __double2float_rn(g[2]),
                                       __double2float_rn(g[3]));
-                        if (w_u8) st_cs_u32(p.u8 + row_off, u[0] | (u[1] << 8) | (u[2] << 16) |
-                                                               (u[3] << 24));
+                        if (w_u8) st_cs_u32(p.u8 + row_off, pack_u8x4(u[0], u[1], u[2], u[3]));
                     } else {
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {

@@ -75,6 +75,7 @@ struct KernelParams {
     sobel5_minmax* minmax;       // per frame: min/max of g (pass 1 of normalize)
     const sobel5_norm_table* norm;  // per frame: normalize thresholds (pass 2)
     int u8_norm;                 // u8 plane = normalize(g) instead of clamp_abs(g)
+    uint32_t* s32;               // exact integer g^2 (normalize pass 1 of the detect path)
     // taps (kernel parameter space -> constant-bank operands)
     int32_t f[5], h[5], k0[5], k1[5], gx_v[5], gy_v[5], gdm_f[5], gdm_d[5];
 };

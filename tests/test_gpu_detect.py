@@ -96,7 +96,7 @@ def _detect(api, img, pad, mode, planes=(), taps=None, prefetch=1):
     d, pitch = to_dev(api, img)
     out, op = api.alloc_planes(ow, oh, tuple(planes) + ("u8",))
     out["u8"].fill_(0x5A)
-    scratch = api.alloc_scratch(1)
+    scratch = api.alloc_scratch(1, out_h=oh, pitch=op)
     api.detect_device(d, pitch, w, h, taps or api.make_stream_taps(), prefetch, pad, mode, out,
                       op, scratch)
     torch.cuda.synchronize()
@@ -156,7 +156,7 @@ def test_detect_batch_per_frame_normalize(api, oracle):
     frames = np.stack([rand_img(h, w, 100 + i, [0xFF, 0x07, 0x01, 0x3F][i]) for i in range(n)])
     d, pitch = to_dev(api, frames)
     out, op = api.alloc_planes(w, h, ("u8",), frames=n)
-    scratch = api.alloc_scratch(n)
+    scratch = api.alloc_scratch(n, out_h=h, pitch=op, out_frame_stride=h * op)
     api.detect_device(d, pitch, w, h, api.make_stream_taps(), 1, True, api.SaveMode.normalize,
                       out, op, scratch, frames=n, in_frame_stride=h * pitch,
                       out_frame_stride=h * op)

@@ -103,7 +103,7 @@ def test_sobel3_detect(api, oracle, pad, mode):
         d, pitch = to_dev(api, img)
         out, op = api.alloc_planes(ow, oh, ("g", "u8"))
         api.detect3_device(d, pitch, w, h, 1, pad, api.SaveMode[mode], out, op,
-                           api.alloc_scratch(1))
+                           api.alloc_scratch(1, out_h=oh, pitch=op))
         torch.cuda.synchronize()
         ref = ref3(oracle, img, pad)
         np.testing.assert_array_equal(out["g"][:, :ow].cpu().numpy(), ref["g"])
