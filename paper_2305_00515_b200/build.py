@@ -56,7 +56,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(OBJDIR, src.replace(".cu", ".o"))
-        cmd = [nv] + NVCC_FLAGS + (["-Xptxas=-v"] if verbose else []) + [
+        extra = os.environ.get("SOBEL5_NVCC_EXTRA", "").split()
+        cmd = [nv] + NVCC_FLAGS + extra + (["-Xptxas=-v"] if verbose else []) + [
             "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or r.returncode:

@@ -78,6 +78,27 @@ __device__ __forceinline__ uint32_t u8_from_s(uint32_t S) {
     return static_cast<uint32_t>(__float2int_rn(y));
 }
 
+// ---- TMA bulk stores (cp.async.bulk global <- shared, bulk-group completion)
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(static_cast<uint32_t>(__cvta_generic_to_shared(ssrc))), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {  // <= N groups still reading smem
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+// generic-proxy smem writes -> visible to the async proxy (the bulk copy)
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // Four bytes (each < 256) packed little-endian with two byte permutes.
 __device__ __forceinline__ uint32_t pack_u8x4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
@@ -117,7 +138,7 @@ __device__ __forceinline__ uint32_t u8_normalize_s(uint32_t S, const uint32_t* t
 // (normalize pass 1), kOutNorm makes the u8 plane the normalize export
 // (pass 2) instead of clamp_abs.
 template <int PF, int GEOM, int OUTS>
-__global__ void __launch_bounds__(kCtaThreads, 4)
+__global__ void __launch_bounds__(kCtaThreads, kMinCtasPerSm)
     sobel5_packed_default_kernel(const __grid_constant__ KernelParams p) {
     constexpr bool SEG = GEOM == kGeomSeg;
     constexpr bool PAD = GEOM == kGeomPad;
@@ -138,6 +159,31 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
     const int warp = threadIdx.x >> 5;
     const int warp_x0 = (blockIdx.x * kCtaWarps + warp) * kWarpCols;
     const int x0 = warp_x0 + lane * 4;
+
+    // TMA bulk stores of the wide planes (compile-time output sets only)
+    // Opt-in (-DSOBEL5_TMA_STORE, best with -DSOBEL5_CTA_WARPS=1 so the bulk
+    // addresses are warp-uniform): measured no faster than register stores
+    // in this kernel (145 vs 144 us at 8K SR) although a store-only probe
+    // gains 12% (profiles/r1/store_probes.txt), so register stores are the
+    // default.
+#ifdef SOBEL5_TMA_STORE
+    constexpr bool TMA = !RT && (OUTS & (kOutGx | kOutGy | kOutGd | kOutGdt | kOutG | kOutG32)) != 0;
+#else
+    constexpr bool TMA = false;
+#endif
+    constexpr int kOffGx = 0;
+    constexpr int kOffGy = kOffGx + ((OUTS & kOutGx) ? 512 : 0);
+    constexpr int kOffGd = kOffGy + ((OUTS & kOutGy) ? 512 : 0);
+    constexpr int kOffGdt = kOffGd + ((OUTS & kOutGd) ? 512 : 0);
+    constexpr int kOffG = kOffGdt + ((OUTS & kOutGdt) ? 512 : 0);
+    constexpr int kOffG32 = kOffG + ((OUTS & kOutG) ? 1024 : 0);
+    constexpr int kStageBytes = kOffG32 + ((OUTS & kOutG32) ? 512 : 0);
+#ifndef SOBEL5_STAGE_BUFS
+#define SOBEL5_STAGE_BUFS 3
+#endif
+    constexpr int kBufs = SOBEL5_STAGE_BUFS;  // rows of staging per warp in flight
+    __shared__ __align__(128) unsigned char s_stage[TMA ? kCtaWarps * kBufs * kStageBytes : 16];
+    int stage_row = 0;
 
     // normalize pass 2: the frame's threshold table, staged in shared memory
     __shared__ uint32_t s_thr[257];
@@ -162,6 +208,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
     const int xoff = (PAD && lane == 0) ? -4 : 4;
     const bool load_b = (lane == 31 && x0 + 4 < p.width) || (PAD && lane == 0 && x0 > 0);
     const bool full = x0 + 3 < p.out_w;
+    const bool warp_full = warp_x0 + kWarpCols <= p.out_w;  // warp-uniform
     const PadEdge pe = PAD ? pad_edge_setup(p.width, warp_x0) : PadEdge{0, 0, 0, 0u};
 
     // Plain images: rows are loaded strictly in order, so one running
@@ -312,26 +359,12 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                 }
                 const int64_t row_off = out_off;
                 out_off += p.pitch;
-                if (full) {
-                    if (w_gx) st_cs_v4(p.gx + row_off, gx[0], gx[1], gx[2], gx[3]);
-                    if (w_gy) st_cs_v4(p.gy + row_off, gy[0], gy[1], gy[2], gy[3]);
-                    if (w_gd) st_cs_v4(p.gd + row_off, gd[0], gd[1], gd[2], gd[3]);
-                    if (w_gdt) st_cs_v4(p.gdt + row_off, gdt[0], gdt[1], gdt[2], gdt[3]);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        if (x0 + j < p.out_w) {
-                            if (w_gx) p.gx[row_off + j] = gx[j];
-                            if (w_gy) p.gy[row_off + j] = gy[j];
-                            if (w_gd) p.gd[row_off + j] = gd[j];
-                            if (w_gdt) p.gdt[row_off + j] = gdt[j];
-                        }
-                    }
-                }
+                uint32_t S[4] = {0u, 0u, 0u, 0u};
+                double g[4] = {0.0, 0.0, 0.0, 0.0};
+                uint32_t u[4] = {0u, 0u, 0u, 0u};
                 if (need_g || w_u8 || w_mm || w_s) {
                     // exact: every square < 2^28 and the sum < 2^30, so
                     // double(S) equals the reference's double sum of squares
-                    uint32_t S[4];
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
                         S[j] = static_cast<uint32_t>(gx[j] * gx[j]) +
@@ -347,50 +380,95 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
                             }
                         }
                     }
-                    if (w_s) {  // kept in L2 where it fits: pass 2 reads it next
-                        if (full) {
-                            *reinterpret_cast<uint4*>(p.s32 + row_off) = make_uint4(S[0], S[1], S[2], S[3]);
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                if (x0 + j < p.out_w) p.s32[row_off + j] = S[j];
-                        }
-                    }
-                    double g[4] = {0.0, 0.0, 0.0, 0.0};
                     if (need_g) {
 #pragma unroll
                         for (int j = 0; j < 4; ++j) g[j] = sqrt_u30(S[j]);
                     }
-                    uint32_t u[4] = {0u, 0u, 0u, 0u};
                     if (w_u8) {
 #pragma unroll
                         for (int j = 0; j < 4; ++j)
                             u[j] = u8_norm ? u8_normalize_s(S[j], s_thr, n_lo, n_scale)
                                            : u8_from_s(S[j]);
                     }
-                    if (full) {
-                        if (w_g) {
-                            st_cs_v4d(p.g + row_off, g[0], g[1], g[2], g[3]);
-                        }
-                        if (w_g32)
-                            st_cs_v4f(p.g32 + row_off, __double2float_rn(g[0]),
-                                      __double2float_rn(g[1]), __double2float_rn(g[2]),
-                                      __double2float_rn(g[3]));
-                        if (w_u8) st_cs_u32(p.u8 + row_off, pack_u8x4(u[0], u[1], u[2], u[3]));
-                    } else {
+                }
+                if (TMA && warp_full) {
+                    // Stage the warp's row of every wide plane in shared
+                    // memory; lane 0 writes each as one bulk copy (TMA,
+                    // cp.async.bulk.global.shared::cta).
+                    unsigned char* st = s_stage + (warp * kBufs + stage_row % kBufs) * kStageBytes;
+                    if (stage_row >= kBufs) {
+                        if (lane == 0) bulk_wait_read<kBufs - 1>();
+                        __syncwarp();
+                    }
+                    if (w_gx) reinterpret_cast<int4*>(st + kOffGx)[lane] = make_int4(gx[0], gx[1], gx[2], gx[3]);
+                    if (w_gy) reinterpret_cast<int4*>(st + kOffGy)[lane] = make_int4(gy[0], gy[1], gy[2], gy[3]);
+                    if (w_gd) reinterpret_cast<int4*>(st + kOffGd)[lane] = make_int4(gd[0], gd[1], gd[2], gd[3]);
+                    if (w_gdt)
+                        reinterpret_cast<int4*>(st + kOffGdt)[lane] = make_int4(gdt[0], gdt[1], gdt[2], gdt[3]);
+                    if (w_g) {
+                        reinterpret_cast<double2*>(st + kOffG)[2 * lane] = make_double2(g[0], g[1]);
+                        reinterpret_cast<double2*>(st + kOffG)[2 * lane + 1] = make_double2(g[2], g[3]);
+                    }
+                    if (w_g32)
+                        reinterpret_cast<float4*>(st + kOffG32)[lane] =
+                            make_float4(__double2float_rn(g[0]), __double2float_rn(g[1]),
+                                        __double2float_rn(g[2]), __double2float_rn(g[3]));
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        // from warp-uniform values only (uniform datapath, no
+                        // per-lane address to convert)
+                        const int64_t wo = out_frame + static_cast<int64_t>(oy0 + r - 4) * p.pitch +
+                                           warp_x0;
+                        if (w_gx) bulk_store(p.gx + wo, st + kOffGx, 512);
+                        if (w_gy) bulk_store(p.gy + wo, st + kOffGy, 512);
+                        if (w_gd) bulk_store(p.gd + wo, st + kOffGd, 512);
+                        if (w_gdt) bulk_store(p.gdt + wo, st + kOffGdt, 512);
+                        if (w_g) bulk_store(p.g + wo, st + kOffG, 1024);
+                        if (w_g32) bulk_store(p.g32 + wo, st + kOffG32, 512);
+                        bulk_commit();
+                    }
+                    ++stage_row;
+                } else if (full) {
+                    if (w_gx) st_cs_v4(p.gx + row_off, gx[0], gx[1], gx[2], gx[3]);
+                    if (w_gy) st_cs_v4(p.gy + row_off, gy[0], gy[1], gy[2], gy[3]);
+                    if (w_gd) st_cs_v4(p.gd + row_off, gd[0], gd[1], gd[2], gd[3]);
+                    if (w_gdt) st_cs_v4(p.gdt + row_off, gdt[0], gdt[1], gdt[2], gdt[3]);
+                    if (w_g) st_cs_v4d(p.g + row_off, g[0], g[1], g[2], g[3]);
+                    if (w_g32)
+                        st_cs_v4f(p.g32 + row_off, __double2float_rn(g[0]), __double2float_rn(g[1]),
+                                  __double2float_rn(g[2]), __double2float_rn(g[3]));
+                } else {
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            if (x0 + j < p.out_w) {
-                                if (w_g) p.g[row_off + j] = g[j];
-                                if (w_g32) p.g32[row_off + j] = __double2float_rn(g[j]);
-                                if (w_u8) p.u8[row_off + j] = static_cast<uint8_t>(u[j]);
-                            }
+                    for (int j = 0; j < 4; ++j) {
+                        if (x0 + j < p.out_w) {
+                            if (w_gx) p.gx[row_off + j] = gx[j];
+                            if (w_gy) p.gy[row_off + j] = gy[j];
+                            if (w_gd) p.gd[row_off + j] = gd[j];
+                            if (w_gdt) p.gdt[row_off + j] = gdt[j];
+                            if (w_g) p.g[row_off + j] = g[j];
+                            if (w_g32) p.g32[row_off + j] = __double2float_rn(g[j]);
+                        }
+                    }
+                }
+                // narrow planes: register stores
+                if (full) {
+                    if (w_u8) st_cs_u32(p.u8 + row_off, pack_u8x4(u[0], u[1], u[2], u[3]));
+                    if (w_s)  // kept in L2 where it fits: the normalize map reads it next
+                        *reinterpret_cast<uint4*>(p.s32 + row_off) = make_uint4(S[0], S[1], S[2], S[3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (x0 + j < p.out_w) {
+                            if (w_u8) p.u8[row_off + j] = static_cast<uint8_t>(u[j]);
+                            if (w_s) p.s32[row_off + j] = S[j];
                         }
                     }
                 }
             }
         }
     }
+    if (TMA && warp_full && lane == 0) bulk_wait_all();  // smem must outlive the copies
     if (w_mm) {  // normalize pass 1: frame min / max of g = sqrt(S), monotone in S
         s_min = __reduce_min_sync(0xffffffffu, s_min);
         s_max = __reduce_max_sync(0xffffffffu, s_max);

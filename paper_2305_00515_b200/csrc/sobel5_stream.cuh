@@ -35,9 +35,13 @@
 namespace sobel5_b200 {
 
 constexpr int kWarpCols = 128;          // output columns per warp (4 per lane)
-constexpr int kCtaWarps = 4;            // warps per CTA, side by side
+#ifndef SOBEL5_CTA_WARPS
+#define SOBEL5_CTA_WARPS 4
+#endif
+constexpr int kCtaWarps = SOBEL5_CTA_WARPS;  // warps per CTA, side by side
 constexpr int kCtaCols = kWarpCols * kCtaWarps;
 constexpr int kCtaThreads = 32 * kCtaWarps;
+constexpr int kMinCtasPerSm = 16 / kCtaWarps;  // 16 resident warps per SM (<= 128 registers)
 
 enum MagMode : int {
     kMagU32 = 0,  // exact integer sum of squares fits uint32 (host-proven bound)

@@ -1,0 +1,38 @@
+"""Store-path probes (tools/probes/store_probe3.cu) at the 8K SR geometry."""
+import os, subprocess
+import numpy as np, torch
+from cuda.bindings import driver as cu
+HERE = os.path.dirname(os.path.abspath(__file__))
+cub = "/tmp/p3.cubin"
+subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-cubin", "-o", cub,
+                os.path.join(HERE, "store_probe3.cu")], check=True)
+torch.zeros(1, device="cuda")
+err, mod = cu.cuModuleLoad(cub.encode())
+def fn(name):
+    e, f = cu.cuModuleGetFunction(mod, name.encode()); assert e == cu.CUresult.CUDA_SUCCESS, (name, e); return f
+def launch(f, grid, block, args):
+    vals = [np.array(v, dtype=t) for v, t in args]
+    ptrs = np.array([v.ctypes.data for v in vals], dtype=np.uint64)
+    e, = cu.cuLaunchKernel(f, *grid, *block, 0, torch.cuda.current_stream().cuda_stream, ptrs.ctypes.data, 0)
+    assert e == cu.CUresult.CUDA_SUCCESS, e
+def timeit(g, n=40):
+    for _ in range(3): g()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    torch.cuda.synchronize(); e0.record()
+    for _ in range(n): g()
+    e1.record(); torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n * 1e3
+W, H = 7676, 4316
+pitch = (W + 31) // 32 * 32
+byts = W * H * 24
+pl = [torch.empty((H, pitch * 4), dtype=torch.uint8, device="cuda") for _ in range(4)]
+g = torch.empty((H, pitch * 8), dtype=torch.uint8, device="cuda")
+for name in ("reg_planes", "tma_warp", "tma_cta"):
+    f = fn(f"_Z{len(name)}{name}PcS_S_S_S_liii")
+    for band in (16, 32, 64):
+        args = [(p.data_ptr(), np.uint64) for p in pl] + [(g.data_ptr(), np.uint64), (pitch, np.int64),
+                (W, np.int32), (H, np.int32), (band, np.int32)]
+        us = timeit(lambda: launch(f, ((W + 511) // 512, (H + band - 1) // band, 1), (128, 1, 1), args))
+        print(f"{name:11s} band={band:3d}: {us:6.1f} us {byts/us/1e3:5.0f} GB/s", flush=True)
+t = torch.empty(byts // 4, dtype=torch.int32, device="cuda")
+us = timeit(lambda: t.fill_(3)); print(f"torch fill_: {us:.1f} us {byts/us/1e3:.0f} GB/s")
