@@ -11,3 +11,4 @@
 #include "sobel5_b200/core.hpp"
 #include "sobel5_b200/params.hpp"
 #include "sobel5_b200/stream.hpp"
+#include "sobel5_b200/detect.hpp"

@@ -348,6 +348,7 @@ inline void raise(sobel5_status st, const std::string& where, const sobel5_diag*
         case SOBEL5_DIM_MISMATCH: throw DimMismatch(where + ": " + sobel5_status_string(st));
         case SOBEL5_NON_POSITIVE_PARAM: throw NonPositiveParam(where + ": " + sobel5_status_string(st));
         case SOBEL5_PARAM_OVERFLOW: throw ParamOverflow(where + ": " + sobel5_status_string(st));
+        case SOBEL5_EMPTY_PLANE: throw EmptyPlane("cannot pad an empty image");
         default: throw DeviceError(where + ": " + sobel5_status_string(st));
     }
 }

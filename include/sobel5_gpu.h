@@ -291,6 +291,11 @@ sobel5_status sobel5_detect_host(sobel5_ctx* ctx, const uint8_t* h_in, int width
                                  uint8_t* h_u8, const sobel5_planes* h_planes,
                                  sobel5_diag* diag_out);
 
+/* Host-buffer detail::quantize (save_plane's export, image_io.hpp:233-268):
+ * tightly packed plane (kind 0 double, 1 int32), h_u8 same size. */
+sobel5_status sobel5_quantize_host(sobel5_ctx* ctx, const void* h_plane, int kind, int width,
+                                   int height, int save_mode, uint8_t* h_u8);
+
 #ifdef __cplusplus
 }
 #endif

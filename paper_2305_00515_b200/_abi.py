@@ -77,6 +77,7 @@ EXPORTS = (
     "sobel5_ipc_import", "sobel5_ipc_release", "sobel5_launch_ex", "sobel5_detect",
     "sobel5_detect_scratch_bytes", "sobel5_quantize_plane", "sobel5_detect_host",
     "sobel3_launch", "sobel3_detect", "sobel3_plan_counters", "sobel3_run_host",
+    "sobel5_quantize_host",
 )
 
 _lib = None
@@ -157,6 +158,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.sobel3_plan_counters.restype = i32
     L.sobel3_run_host.argtypes = [vp, vp, i32, i32, i32, C.POINTER(Planes)]
     L.sobel3_run_host.restype = i32
+    L.sobel5_quantize_host.argtypes = [vp, vp, i32, i32, i32, i32, vp]
+    L.sobel5_quantize_host.restype = i32
     _lib = L
     return L
 

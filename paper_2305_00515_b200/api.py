@@ -493,18 +493,18 @@ def quantize_device(d_plane, pitch: int, width: int, height: int, save_mode: Sav
 
 def quantize(plane: np.ndarray, mode: SaveMode) -> np.ndarray:
     """detail::quantize (image_io.hpp:233-256) of a host plane, computed on the GPU."""
-    import torch
     plane = np.ascontiguousarray(plane)
     if plane.size == 0:
         raise EmptyPlane("cannot save an empty plane")
     if plane.dtype not in (np.float64, np.int32):
         raise DimMismatch("quantize needs a float64 or int32 plane")
     h, w = plane.shape
-    d = torch.from_numpy(plane).cuda()
-    u8 = torch.empty((h, w), dtype=torch.uint8, device="cuda")
-    quantize_device(d, w, w, h, mode, u8, w, alloc_scratch(1))  # min/max + table only
-    torch.cuda.synchronize()
-    return u8.cpu().numpy()
+    out = np.empty((h, w), np.uint8)
+    ctx = default_context()
+    kind = 0 if plane.dtype == np.float64 else 1
+    check(_abi.load().sobel5_quantize_host(ctx.handle, plane.ctypes.data, kind, w, h, int(mode),
+                                           out.ctypes.data), f"quantize ({ctx.last_error()})")
+    return out
 
 
 def detect(img, params_or_taps=None, pad: bool = True, save_mode: SaveMode = SaveMode.normalize,

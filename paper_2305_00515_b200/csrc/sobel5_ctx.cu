@@ -345,4 +345,27 @@ sobel5_status sobel3_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     return SOBEL5_OK;
 }
 
+sobel5_status sobel5_quantize_host(sobel5_ctx* ctx, const void* h_plane, int kind, int width,
+                                   int height, int save_mode, uint8_t* h_u8) {
+    if (!ctx) return SOBEL5_INVALID_ARG;
+    if (width < 1 || height < 1) return SOBEL5_EMPTY_PLANE;  // image_io.hpp:259/265
+    if (!h_plane || !h_u8 || (kind != 0 && kind != 1)) return SOBEL5_INVALID_ARG;
+    CK(cudaSetDevice(ctx->device));
+    const size_t es = kind == 0 ? sizeof(double) : sizeof(int32_t);
+    const size_t n = static_cast<size_t>(width) * height;
+    // the plane goes through the g slot (8 B/elem covers both kinds), u8 through u8
+    CK(ensure(&ctx->d_plane[4], &ctx->d_plane_bytes[4], n * 8));
+    CK(ensure(&ctx->d_plane[6], &ctx->d_plane_bytes[6], n));
+    CK(ensure(&ctx->d_scratch, &ctx->d_scratch_bytes, sobel5_detect_scratch_bytes(0, 0, 0, 1)));
+    CK(cudaMemcpyAsync(ctx->d_plane[4], h_plane, n * es, cudaMemcpyHostToDevice, ctx->s_comp));
+    const sobel5_status st =
+        sobel5_quantize_plane(ctx->d_plane[4], kind, width, width, height, save_mode,
+                              static_cast<uint8_t*>(ctx->d_plane[6]), width, ctx->d_scratch,
+                              ctx->s_comp);
+    if (st != SOBEL5_OK) return st;
+    CK(cudaMemcpyAsync(h_u8, ctx->d_plane[6], n, cudaMemcpyDeviceToHost, ctx->s_comp));
+    CK(cudaStreamSynchronize(ctx->s_comp));
+    return SOBEL5_OK;
+}
+
 }  // extern "C"

@@ -247,10 +247,97 @@ static void gpu_checks() {
     CHECK(s4.gx == full.gx && s4.g == full.g);
 }
 
+// sobel3_2d brute force (oracle.hpp:58-70) -- the 3x3 checker
+static void corr3(const GrayPlane& img, SignedPlane& gx, SignedPlane& gy, RealPlane& g) {
+    static const int kx[3][3] = {{-1, 0, 1}, {-2, 0, 2}, {-1, 0, 1}};
+    static const int ky[3][3] = {{-1, -2, -1}, {0, 0, 0}, {1, 2, 1}};
+    gx = SignedPlane(img.width() - 2, img.height() - 2);
+    gy = SignedPlane(img.width() - 2, img.height() - 2);
+    g = RealPlane(img.width() - 2, img.height() - 2);
+    for (int y = 0; y < gx.height(); ++y)
+        for (int x = 0; x < gx.width(); ++x) {
+            long long a = 0, b = 0;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) {
+                    a += kx[i][j] * img.at(y + i, x + j);
+                    b += ky[i][j] * img.at(y + i, x + j);
+                }
+            gx.at(y, x) = static_cast<std::int32_t>(a);
+            gy.at(y, x) = static_cast<std::int32_t>(b);
+            g.at(y, x) = std::sqrt(static_cast<double>(a) * a + static_cast<double>(b) * b);
+        }
+}
+
+// the reference's quantize (image_io.hpp:233-256) written out as the checker
+template <class T>
+static GrayPlane quantize_ref(const Plane<T>& p, bool normalize) {
+    GrayPlane out(p.width(), p.height());
+    double lo = static_cast<double>(p.data()[0]), hi = lo;
+    for (auto v : p.data()) {
+        lo = std::min(lo, static_cast<double>(v));
+        hi = std::max(hi, static_cast<double>(v));
+    }
+    const double span = hi - lo;
+    for (std::size_t i = 0; i < p.size(); ++i) {
+        const double v = static_cast<double>(p.data()[i]);
+        out.data()[i] = normalize ? static_cast<std::uint8_t>(std::lround(span > 0 ? (v - lo) * 255.0 / span : 0.0))
+                                  : static_cast<std::uint8_t>(std::min(255.0, std::round(std::fabs(v))));
+    }
+    return out;
+}
+
+static void gpu_checks_next_rows() {
+    // run_stream_3x3 / sobel3_2d vs brute force, counters closed form
+    std::mt19937 rng(3);
+    bool eq3 = true;
+    for (int trial = 0; trial < 16; ++trial) {
+        const int w = 3 + static_cast<int>(rng() % 300), h = 3 + static_cast<int>(rng() % 90);
+        const GrayPlane img = synth_random(w, h, 500 + static_cast<std::uint64_t>(trial));
+        SignedPlane ex, ey;
+        RealPlane eg;
+        corr3(img, ex, ey, eg);
+        const auto r = run_stream_3x3(img, plan_strips(w, 16, 1), trial % 2 ? Prefetch::on : Prefetch::off);
+        eq3 &= r.gx == ex && r.gy == ey && r.g == eg;
+        const auto o = sobel3_2d(img);
+        eq3 &= o.gx == ex && o.g == eg;
+    }
+    CHECK(eq3);
+    const auto c3 = run_stream_3x3(synth_random(100, 50, 1), plan_strips(100, 32, 1), Prefetch::on).counters;
+    CHECK(c3.row_conv3_f == 4 * 50 && c3.row_conv3_h == 4 * 50 && c3.mac == 5ull * (50 + 48) * 98);
+    CHECK(throws<ImageTooSmall>([] { run_stream_3x3(GrayPlane(9, 2)); }) ==
+          "streaming filter needs at least 3x3, got 9x2");
+
+    // detect = quantize(run_stream(pad_replicate(img, 2).plane).g, mode)
+    const GrayPlane img = synth_random(131, 77, 9);
+    GrayPlane low = img;
+    for (auto& v : low.data()) v &= 7;
+    for (const GrayPlane* src : {&img, static_cast<const GrayPlane*>(&low)}) {
+        const PaddedPlane pp = pad_replicate(*src, 2);
+        CHECK(pp.inner_width() == src->width() && pp.plane.width() == src->width() + 4);
+        const auto full = run_stream(pp.plane, FilterParams{}, plan_strips(pp.plane.width(), 32, 2), Prefetch::on);
+        for (SaveMode m : {SaveMode::clamp_abs, SaveMode::normalize}) {
+            const GrayPlane want = quantize_ref(full.g, m == SaveMode::normalize);
+            CHECK(gpu::detect(*src, FilterParams{}, true, m) == want);
+            CHECK(detail::quantize(full.g, m) == want);
+        }
+        CHECK(detail::quantize(full.gx, SaveMode::normalize) == quantize_ref(full.gx, true));
+        CHECK(detail::quantize(full.gd, SaveMode::clamp_abs) == quantize_ref(full.gd, false));
+    }
+    CHECK(throws<EmptyPlane>([] { pad_replicate(GrayPlane(), 2); }) == "cannot pad an empty image");
+    CHECK(throws<EmptyPlane>([] { gpu::detect(GrayPlane()); }) == "cannot pad an empty image");
+    SignedPlane ties(4, 1);
+    ties.data() = {0, 1, 2, 1};
+    const GrayPlane tq = detail::quantize(ties, SaveMode::normalize);
+    CHECK(tq.data()[1] == 128 && tq.data()[2] == 255);
+}
+
 int main(int argc, char** argv) {
     const bool gpu = argc > 1 && std::strcmp(argv[1], "--gpu") == 0;
     host_checks();
-    if (gpu) gpu_checks();
+    if (gpu) {
+        gpu_checks();
+        gpu_checks_next_rows();
+    }
     std::printf("%s: %d checks, %d failed\n", gpu ? "host+gpu" : "host", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }

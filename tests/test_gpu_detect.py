@@ -228,3 +228,18 @@ def test_detect_golden_fixtures(api):
         for mode in ("clamp_abs", "normalize"):
             u8 = api.detect(img, pad=True, save_mode=api.SaveMode[mode])
             np.testing.assert_array_equal(u8, z[f"{n}__{mode}"], err_msg=f"{n} {mode}")
+
+
+@pytest.mark.parametrize("mode", ["clamp_abs", "normalize"])
+def test_quantize_device_pitched(api, oracle, mode):
+    """sobel5_quantize_plane on pitched device planes (the dump-planes path)."""
+    import torch
+    rng = np.random.default_rng(12)
+    plane = rng.integers(-5000, 5000, (33, 70)).astype(np.int32)
+    d = torch.zeros((33, 96), dtype=torch.int32, device="cuda")
+    d[:, :70] = torch.from_numpy(plane).cuda()
+    u8 = torch.full((33, 80), 0x5A, dtype=torch.uint8, device="cuda")
+    api.quantize_device(d, 96, 70, 33, api.SaveMode[mode], u8, 80, api.alloc_scratch(1))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(u8[:, :70].cpu().numpy(), oracle.quantize(plane, mode))
+    assert (u8[:, 70:].cpu().numpy() == 0x5A).all()
