@@ -65,7 +65,7 @@ sobel5_status sobel3_common(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
     kp.width = width;
     kp.out_w = out_w;
     kp.out_h = out_h;
-    kp.band = choose_band(out_w, out_h, frames);
+    kp.band = choose_band(out_w, out_h, frames, !(out->gx || out->gy || out->g || out->g32));
     kp.gx = out->gx;
     kp.gy = out->gy;
     kp.g = out->g;

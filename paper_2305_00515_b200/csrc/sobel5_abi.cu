@@ -84,15 +84,18 @@ int env_int(const char* name, int dflt) {
 
 // Output rows per CTA band.  Small bands cost 4/band extra halo rows of
 // horizontal work; large ones leave too few CTAs to fill 148 SMs.
-int choose_band_impl(int out_w, int out_h, int frames) {
+int choose_band_impl(int out_w, int out_h, int frames, bool narrow_only) {
     const int forced = env_int("SOBEL5_BAND", 0);
     if (forced > 0) return forced;
     const int64_t cols = (out_w + kCtaCols - 1) / kCtaCols;
     int band = 64;
     // keep >= ~16 CTAs per SM (4 resident x 4 waves) so the last partial
-    // wave costs little; measured on B200 at 8K: band 16 154.5 us, 32
-    // 159.3 us, 64 161.0 us (tools/sweep.py)
-    while (band > 16 && cols * frames * ((out_h + band - 1) / band) < 148 * 16) band /= 2;
+    // wave costs little; measured on B200 at 8K SR: band 16 141.9 us, 32
+    // 146.9 us, 64 149.6 us (tools/sweep.py).  Contracts without wide planes
+    // (u8, detect passes) are issue-bound and prefer 32 (halo rows are 4/band
+    // of the row work): 8K u8 57.5 us at 32 vs 59.7 at 16 and 64.
+    const int floor_band = narrow_only ? 32 : 16;
+    while (band > floor_band && cols * frames * ((out_h + band - 1) / band) < 148 * 16) band /= 2;
     return band;
 }
 
@@ -136,7 +139,9 @@ cudaError_t dispatch(const KernelParams& kp, dim3 grid, int prefetch, bool dflt,
 namespace sobel5_b200 {
 
 bool taps_default(const sobel5_taps* t) { return taps_are_default(*t); }
-int choose_band(int out_w, int out_h, int frames) { return choose_band_impl(out_w, out_h, frames); }
+int choose_band(int out_w, int out_h, int frames, bool narrow_only) {
+    return choose_band_impl(out_w, out_h, frames, narrow_only);
+}
 sobel5_status check_planes(const sobel5_planes* o, int out_w) { return check_planes_impl(o, out_w); }
 
 void count_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
@@ -191,7 +196,8 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     kp.width = width;
     kp.out_w = out_w;
     kp.out_h = out_h;
-    kp.band = choose_band(out_w, out_h, frames);
+    kp.band = choose_band(out_w, out_h, frames,
+                          !(out->gx || out->gy || out->gd || out->gdt || out->g || out->g32));
     kp.gx = out->gx;
     kp.gy = out->gy;
     kp.gd = out->gd;

@@ -39,7 +39,7 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
                             sobel5_diag* diag, void* stream, const LaunchExtra& ex);
 
 sobel5_status map_cuda(cudaError_t e);
-int choose_band(int out_w, int out_h, int frames);  // output rows per CTA
+int choose_band(int out_w, int out_h, int frames, bool narrow_only);  // output rows per CTA
 sobel5_status check_planes(const sobel5_planes* o, int out_w);
 
 // 3x3 operator (sobel3_packed.cuh, sobel3_k.cu).

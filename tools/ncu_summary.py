@@ -5,8 +5,9 @@ def page(p, extra=()):
     out = subprocess.run(["ncu", "-i", rep, "--page", p, "--csv", *extra], capture_output=True, text=True).stdout
     return list(csv.reader(io.StringIO(out)))
 raw = page("raw")
-hdr, vals = raw[0], raw[2]
+hdr, units, vals = raw[0], raw[1], raw[2]
 d = dict(zip(hdr, vals))
+u = dict(zip(hdr, units))
 keys = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "smsp__inst_executed.sum", "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
@@ -17,7 +18,7 @@ keys = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]
 for k in keys:
-    print(f"{k:60s} {d.get(k)}")
+    print(f"{k:60s} {d.get(k)} {u.get(k, '')}")
 if len(sys.argv) > 2:
     src = page("source", ("--print-source", "sass"))
     h = src[1]; data = src[2:]
