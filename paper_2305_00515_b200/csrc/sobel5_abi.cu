@@ -17,6 +17,7 @@
 
 #include "sobel5_gpu.h"
 #include "sobel5_packed.cuh"
+#include <algorithm>
 #include "sobel5_internal.h"
 #include "sobel5_stream.cuh"
 
