@@ -78,6 +78,26 @@ MagMode choose_mag(const sobel5_taps& t) {
     return S < ((unsigned __int128)1 << 32) ? kMagU32 : kMagF64;
 }
 
+// The packed (two pixels per register) kernel is exact for ANY taps whose
+// extracted quantities -- gx, gy and the P / M diagonal sums -- stay within
+// int16 for every uint8 input: all arithmetic before the extraction is mod
+// 2^32 (a ring homomorphism), so only the final values must fit a lane.
+bool taps_fit_packed(const sobel5_taps& t) {
+    int64_t kx[25], ky[25], kp[25], km[25];
+    const int64_t dd[5] = {0, -1, 0, 1, 0};
+    for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < 5; ++j) {
+            kx[i * 5 + j] = int64_t{t.gx_v[i]} * t.f[j];
+            ky[i * 5 + j] = int64_t{t.gy_v[i]} * t.h[j];
+            km[i * 5 + j] = int64_t{t.gdm_f[i]} * t.f[j] - int64_t{t.gdm_d[i]} * dd[j];
+            const int64_t kpr[5] = {t.k0[j], t.k1[j], 0, -int64_t{t.k1[j]}, -int64_t{t.k0[j]}};
+            kp[i * 5 + j] = kpr[i];
+        }
+    constexpr int64_t lim = 32767;
+    return response_bound(kx) <= lim && response_bound(ky) <= lim && response_bound(kp) <= lim &&
+           response_bound(km) <= lim;
+}
+
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
     return v && *v ? std::atoi(v) : dflt;
@@ -122,6 +142,19 @@ sobel5_status check_planes_impl(const sobel5_planes* o, int out_w) {
     return SOBEL5_OK;
 }
 
+bool taps_fit_packed_p(const KernelParams& kp) {
+    sobel5_taps t{};
+    std::memcpy(t.f, kp.f, sizeof t.f);
+    std::memcpy(t.h, kp.h, sizeof t.h);
+    std::memcpy(t.k0, kp.k0, sizeof t.k0);
+    std::memcpy(t.k1, kp.k1, sizeof t.k1);
+    std::memcpy(t.gx_v, kp.gx_v, sizeof t.gx_v);
+    std::memcpy(t.gy_v, kp.gy_v, sizeof t.gy_v);
+    std::memcpy(t.gdm_f, kp.gdm_f, sizeof t.gdm_f);
+    std::memcpy(t.gdm_d, kp.gdm_d, sizeof t.gdm_d);
+    return taps_fit_packed(t);
+}
+
 cudaError_t dispatch(const KernelParams& kp, dim3 grid, int prefetch, bool dflt, MagMode mag,
                      cudaStream_t s) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -132,6 +165,13 @@ cudaError_t dispatch(const KernelParams& kp, dim3 grid, int prefetch, bool dflt,
         return seg ? launch_packed_seg(kp, grid, prefetch, s)
                    : launch_packed_plain(kp, grid, prefetch, s);
     }
+    if (env_int("SOBEL5_GENERIC", 0) == 0 && taps_fit_packed_p(kp)) {
+        // any other taps within the int16 bound: packed kernel, runtime taps
+        if (kp.pad) return launch_packed_rt_pad(kp, grid, prefetch, s);
+        const bool seg = kp.top_rows > 0 || kp.bot != nullptr;
+        return seg ? launch_packed_rt_seg(kp, grid, prefetch, s)
+                   : launch_packed_rt_plain(kp, grid, prefetch, s);
+    }
     return launch_generic(kp, grid, prefetch, dflt, mag, s);
 }
 
@@ -140,6 +180,9 @@ cudaError_t dispatch(const KernelParams& kp, dim3 grid, int prefetch, bool dflt,
 namespace sobel5_b200 {
 
 bool taps_default(const sobel5_taps* t) { return taps_are_default(*t); }
+bool taps_packed(const sobel5_taps* t) {
+    return env_int("SOBEL5_GENERIC", 0) == 0 && (taps_are_default(*t) || taps_fit_packed(*t));
+}
 int choose_band(int out_w, int out_h, int frames, bool narrow_only) {
     return choose_band_impl(out_w, out_h, frames, narrow_only);
 }
@@ -181,9 +224,8 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     const int out_h = static_cast<int>(ex.pad ? rows : rows - 4);
     if (sobel5_status st = check_planes(out, out_w); st != SOBEL5_OK) return st;
     if (ex.u8_norm && (!ex.norm || !out->u8)) return SOBEL5_INVALID_ARG;
-    // the S plane exists only for integer magnitudes (packed default taps)
-    if (ex.s32 && !(taps_are_default(*taps) && env_int("SOBEL5_GENERIC", 0) == 0))
-        return SOBEL5_INVALID_ARG;
+    // the S plane exists only for the packed kernels (exact integer S)
+    if (ex.s32 && !taps_packed(taps)) return SOBEL5_INVALID_ARG;
     if (rows > (int64_t{1} << 30) || frames > 65535) return SOBEL5_INVALID_ARG;
 
     KernelParams kp{};

@@ -184,11 +184,6 @@ sobel5_status run_init(sobel5_minmax* mm, int frames, cudaStream_t s) {
     return map_cuda(cudaGetLastError());
 }
 
-int env_int_(const char* name) {
-    const char* v = std::getenv(name);
-    return v && *v ? std::atoi(v) : 0;
-}
-
 // normalize export (image_io.hpp:242-255) around a stencil launcher:
 //   exact (integer S): init, pass 1 = stencil + planes + S plane + min/max,
 //     table, pass 2 = S plane -> u8 (memory-bound map, no stencil rerun);
@@ -268,7 +263,7 @@ sobel5_status sobel5_detect(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
         return launch_common(nullptr, d_in, nullptr, in_pitch, in_frame_stride, width, height,
                              n_frames, taps, prefetch, d_out, out_frame_stride, d_diag, stream, ex);
     if (!d_scratch || reinterpret_cast<uintptr_t>(d_scratch) % 256 != 0) return SOBEL5_INVALID_ARG;
-    const bool exact = taps && taps_default(taps) && env_int_("SOBEL5_GENERIC") == 0;
+    const bool exact = taps && taps_packed(taps);
     return detect_normalize(
         d_scratch, n_frames, exact, d_out, out_frame_stride, stream,
         [&](const sobel5_planes* planes, const LaunchExtra& e, sobel5_diag* dg) {

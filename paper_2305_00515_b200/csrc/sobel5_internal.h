@@ -17,6 +17,11 @@ cudaError_t launch_packed_plain(const KernelParams& kp, dim3 grid, int pf, cudaS
 cudaError_t launch_packed_seg(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
 cudaError_t launch_packed_pad(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
 
+// Packed kernel with runtime taps (any taps within the int16 bound).
+cudaError_t launch_packed_rt_plain(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
+cudaError_t launch_packed_rt_seg(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
+cudaError_t launch_packed_rt_pad(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
+
 // Generic-taps kernel (sobel5_stream.cuh).
 cudaError_t launch_generic(const KernelParams& kp, dim3 grid, int pf, bool default_taps,
                            MagMode mag, cudaStream_t s);
@@ -48,6 +53,7 @@ sobel5_status sobel3_common(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
                             const sobel5_planes* out, int64_t out_frame_stride, void* stream,
                             const LaunchExtra& ex);
 bool taps_default(const sobel5_taps* t);  // equal to make_stream_taps(1, 2, 6, 4)
+bool taps_packed(const sobel5_taps* t);   // a packed kernel (exact integer S) serves these taps
 void count_launch(int n = 1);
 
 }  // namespace sobel5_b200

@@ -137,7 +137,7 @@ __device__ __forceinline__ uint32_t u8_normalize_s(uint32_t S, const uint32_t* t
 // OUTS = output-set bits; kOutMinMax adds the per-frame min/max of g
 // (normalize pass 1), kOutNorm makes the u8 plane the normalize export
 // (pass 2) instead of clamp_abs.
-template <int PF, int GEOM, int OUTS>
+template <int PF, int GEOM, int OUTS, bool RTAPS = false>
 __global__ void __launch_bounds__(kCtaThreads, kMinCtasPerSm)
     sobel5_packed_default_kernel(const __grid_constant__ KernelParams p) {
     constexpr bool SEG = GEOM == kGeomSeg;
@@ -295,67 +295,155 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtasPerSm)
             for (int q = 0; q < 2; ++q) {
                 const uint32_t p0 = e[q], p1 = e[q + 1], p2 = e[q + 2], p3 = e[q + 3],
                                p4 = e[q + 4];
-                const uint32_t s04 = p0 + p4, s13 = p1 + p3;
-                const uint32_t d = p3 - p1, d04 = p4 - p0;
+                const uint32_t d = p3 - p1;  // row_diff (pipeline.hpp:124-127)
                 D[q] = d;
-                F[q] = d04 + 2u * d;
-                H[q] = s04 + 4u * s13 + 6u * p2;
-                K0[q] = 3u * (s04 + s13) + p2;
-                K1[q] = s04 + 6u * s13 + 8u * p2;
+                if constexpr (RTAPS) {
+                    // row_conv5 (pipeline.hpp:117-122) with the caller's taps;
+                    // the multiplies act on both packed pixels at once
+                    const uint32_t pv[5] = {p0, p1, p2, p3, p4};
+                    uint32_t f = 0u, hh = 0u, k0 = 0u, k1 = 0u;
+#pragma unroll
+                    for (int t = 0; t < 5; ++t) {
+                        f += static_cast<uint32_t>(p.f[t]) * pv[t];
+                        hh += static_cast<uint32_t>(p.h[t]) * pv[t];
+                        k0 += static_cast<uint32_t>(p.k0[t]) * pv[t];
+                        k1 += static_cast<uint32_t>(p.k1[t]) * pv[t];
+                    }
+                    F[q] = f;
+                    H[q] = hh;
+                    K0[q] = k0;
+                    K1[q] = k1;
+                } else {
+                    const uint32_t s04 = p0 + p4, s13 = p1 + p3;
+                    const uint32_t d04 = p4 - p0;
+                    F[q] = d04 + 2u * d;
+                    H[q] = s04 + 4u * s13 + 6u * p2;
+                    K0[q] = 3u * (s04 + s13) + p2;
+                    K1[q] = s04 + 6u * s13 + 8u * p2;
+                }
             }
 
+            if constexpr (RTAPS) {
+                // vagg5 / vagg_gd_minus / vagg_gd_plus (pipeline.hpp:136-189)
+                // as running sums: ax = gx, ay = gy, an = M, aq = P
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const uint32_t f = F[q], hh = H[q], d = D[q];
-                const uint32_t f3 = 3u * f;
-                const uint32_t na = f3 - 5u * d;  // i = 0, 4
-                const uint32_t nc = f + 6u * d;   // i = 2
-                // i = 0: open output row r
-                const int s0 = s;
-                ax[s0][q] = f;
-                ay[s0][q] = 0u - hh;
-                an[s0][q] = na;
-                aq[s0][q] = K0[q];
-                // i = 1
-                const int s1 = (s + 4) % 5;
-                ax[s1][q] += 4u * f;
-                ay[s1][q] -= 2u * hh;
-                an[s1][q] += f3;
-                aq[s1][q] += K1[q];
-                // i = 2
-                const int s2 = (s + 3) % 5;
-                ax[s2][q] += 6u * f;
-                an[s2][q] += nc;
-                // i = 3
-                const int s3 = (s + 2) % 5;
-                ax[s3][q] += 4u * f;
-                ay[s3][q] += 2u * hh;
-                an[s3][q] += f3;
-                aq[s3][q] -= K1[q];
-                // i = 4: closes output row r - 4
-                const int s4 = (s + 1) % 5;
-                ax[s4][q] += f;
-                ay[s4][q] += hh;
-                an[s4][q] += na;
-                aq[s4][q] -= K0[q];
+                for (int q = 0; q < 2; ++q) {
+                    const uint32_t f = F[q], hh = H[q], d = D[q];
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) {
+                        const int sl_i = (s - i + 5) % 5;
+                        const uint32_t vx = static_cast<uint32_t>(p.gx_v[i]) * f;
+                        const uint32_t vy = static_cast<uint32_t>(p.gy_v[i]) * hh;
+                        const uint32_t vm = static_cast<uint32_t>(p.gdm_f[i]) * f -
+                                            static_cast<uint32_t>(p.gdm_d[i]) * d;
+                        if (i == 0) {
+                            ax[sl_i][q] = vx;
+                            ay[sl_i][q] = vy;
+                            an[sl_i][q] = vm;
+                            aq[sl_i][q] = K0[q];
+                        } else {
+                            ax[sl_i][q] += vx;
+                            ay[sl_i][q] += vy;
+                            an[sl_i][q] += vm;
+                            if (i == 1) aq[sl_i][q] += K1[q];
+                            if (i == 3) aq[sl_i][q] -= K1[q];
+                            if (i == 4) aq[sl_i][q] -= K0[q];
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const uint32_t f = F[q], hh = H[q], d = D[q];
+                    const uint32_t f3 = 3u * f;
+                    const uint32_t na = f3 - 5u * d;  // i = 0, 4
+                    const uint32_t nc = f + 6u * d;   // i = 2
+                    // i = 0: open output row r
+                    const int s0 = s;
+                    ax[s0][q] = f;
+                    ay[s0][q] = 0u - hh;
+                    an[s0][q] = na;
+                    aq[s0][q] = K0[q];
+                    // i = 1
+                    const int s1 = (s + 4) % 5;
+                    ax[s1][q] += 4u * f;
+                    ay[s1][q] -= 2u * hh;
+                    an[s1][q] += f3;
+                    aq[s1][q] += K1[q];
+                    // i = 2
+                    const int s2 = (s + 3) % 5;
+                    ax[s2][q] += 6u * f;
+                    an[s2][q] += nc;
+                    // i = 3
+                    const int s3 = (s + 2) % 5;
+                    ax[s3][q] += 4u * f;
+                    ay[s3][q] += 2u * hh;
+                    an[s3][q] += f3;
+                    aq[s3][q] -= K1[q];
+                    // i = 4: closes output row r - 4
+                    const int s4 = (s + 1) % 5;
+                    ax[s4][q] += f;
+                    ay[s4][q] += hh;
+                    an[s4][q] += na;
+                    aq[s4][q] -= K0[q];
+                }
             }
 
             if (r >= 4) {
                 const int sl = (s + 1) % 5;
                 int32_t gx[4], gy[4], gd[4], gdt[4];
+                if constexpr (RTAPS) {
+                    // P = aq, M = an extracted per pixel; recover_diag
+                    // (pipeline.hpp:268-282): gd = (P+M)/2, gdt = (P-M)/2
+                    int32_t P[4], M[4];
+                    bool odd_any = false;
+                    int32_t odd_p = 0, odd_m = 0;
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const uint32_t vd = an[sl][q] - aq[sl][q];
-                    const uint32_t vt = 0u - an[sl][q] - aq[sl][q];
-                    // pair q holds pixels (q, q + 2)
-                    gx[q] = lane_lo(ax[sl][q]);
-                    gx[q + 2] = lane_hi(ax[sl][q]);
-                    gy[q] = lane_lo(ay[sl][q]);
-                    gy[q + 2] = lane_hi(ay[sl][q]);
-                    gd[q] = lane_lo(vd);
-                    gd[q + 2] = lane_hi(vd);
-                    gdt[q] = lane_lo(vt);
-                    gdt[q + 2] = lane_hi(vt);
+                    for (int q = 0; q < 2; ++q) {
+                        gx[q] = lane_lo(ax[sl][q]);
+                        gx[q + 2] = lane_hi(ax[sl][q]);
+                        gy[q] = lane_lo(ay[sl][q]);
+                        gy[q + 2] = lane_hi(ay[sl][q]);
+                        P[q] = lane_lo(aq[sl][q]);
+                        P[q + 2] = lane_hi(aq[sl][q]);
+                        M[q] = lane_lo(an[sl][q]);
+                        M[q + 2] = lane_hi(an[sl][q]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int32_t sum = P[j] + M[j];
+                        const bool odd = (sum & 1) != 0 && x0 + j < p.out_w;
+                        if (odd && !odd_any) {
+                            odd_p = P[j];
+                            odd_m = M[j];
+                        }
+                        odd_any |= odd;
+                        gd[j] = sum >> 1;
+                        gdt[j] = (P[j] - M[j]) >> 1;
+                    }
+                    // ParityViolation (pipeline.hpp:269-271), recorded once per warp
+                    const unsigned odd_mask = __ballot_sync(0xffffffffu, odd_any);
+                    if (odd_mask && p.diag && lane == __ffs(odd_mask) - 1) {
+                        if (atomicAdd(&p.diag->violations, 1) == 0) {
+                            p.diag->sum = odd_p;
+                            p.diag->diff = odd_m;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const uint32_t vd = an[sl][q] - aq[sl][q];
+                        const uint32_t vt = 0u - an[sl][q] - aq[sl][q];
+                        // pair q holds pixels (q, q + 2)
+                        gx[q] = lane_lo(ax[sl][q]);
+                        gx[q + 2] = lane_hi(ax[sl][q]);
+                        gy[q] = lane_lo(ay[sl][q]);
+                        gy[q + 2] = lane_hi(ay[sl][q]);
+                        gd[q] = lane_lo(vd);
+                        gd[q + 2] = lane_hi(vd);
+                        gdt[q] = lane_lo(vt);
+                        gdt[q + 2] = lane_hi(vt);
+                    }
                 }
                 const int64_t row_off = out_off;
                 out_off += p.pitch;

@@ -243,3 +243,52 @@ def test_quantize_device_pitched(api, oracle, mode):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(u8[:, :70].cpu().numpy(), oracle.quantize(plane, mode))
     assert (u8[:, 70:].cpu().numpy() == 0x5A).all()
+
+
+# FilterParams whose responses fit int16 take the packed kernel with runtime
+# taps; the others the generic kernel.  Both must equal the oracle.
+PARAMS = [(1, 1, 1, 1), (1, 2, 4, 2), (1, 1, 2, 1), (2, 1, 1, 1), (1, 3, 2, 1), (2, 3, 5, 7),
+          (3, 1, 1, 2)]
+
+
+@pytest.mark.parametrize("params", PARAMS)
+@pytest.mark.parametrize("pad", [False, True])
+def test_params_all_contracts(api, oracle, params, pad):
+    import torch
+    sys_taps = oracle.make_stream_taps(*params)
+    taps = api.Taps.from_dict(sys_taps.as_dict())
+    h, w = 203, 301
+    img = rand_img(h, w, sum(params), 0xFF)
+    ow, oh = (w, h) if pad else (w - 4, h - 4)
+    ref = padded_ref(oracle, img, sys_taps) if pad else oracle.run_stream(img, sys_taps)[1]
+    d, pitch = to_dev(api, img)
+    for planes in (SR, ("u8",), SR + ("u8",)):
+        out, op = api.alloc_planes(ow, oh, planes)
+        for v in out.values():
+            v.fill_(7)
+        api.launch_ex(d, pitch, w, h, taps, 1, pad, out, op)
+        torch.cuda.synchronize()
+        for k in planes:
+            want = oracle.clamp_abs(ref["g"]) if k == "u8" else ref[k]
+            np.testing.assert_array_equal(out[k][:, :ow].cpu().numpy(), want, err_msg=f"{k} {planes}")
+    got = _detect(api, img, pad, api.SaveMode.normalize, planes=("g",), taps=taps)
+    np.testing.assert_array_equal(got["g"], ref["g"])
+    np.testing.assert_array_equal(got["u8"], oracle.quantize(ref["g"], "normalize"))
+
+
+def test_fault_injected_runtime_packed(api, oracle):
+    """Odd perturbations of the default taps still fit the packed kernel and
+    must report recover_diag's ParityViolation with the first pair."""
+    import torch
+    t = oracle.make_stream_taps()
+    t.k0[0] += 1
+    taps = api.Taps.from_dict(t.as_dict())
+    img = rand_img(40, 70, 5)
+    st, _, bad = oracle.run_stream(img, t)
+    assert st == 3
+    d, pitch = to_dev(api, img)
+    out, op = api.alloc_planes(66, 36, SR)
+    diag = torch.zeros(4, dtype=torch.int32, device="cuda")
+    api.launch(d, pitch, 70, 40, taps, 1, out, op, diag)
+    torch.cuda.synchronize()
+    assert diag[0].item() > 0
