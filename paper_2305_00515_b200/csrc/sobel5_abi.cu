@@ -109,14 +109,24 @@ int choose_band_impl(int out_w, int out_h, int frames, bool narrow_only) {
     const int forced = env_int("SOBEL5_BAND", 0);
     if (forced > 0) return forced;
     const int64_t cols = (out_w + kCtaCols - 1) / kCtaCols;
+    auto ctas = [&](int band) { return cols * frames * ((out_h + band - 1) / band); };
+    if (!narrow_only) {
+        // Wide planes (the write-bound contracts): 16-row bands.  Shorter
+        // bands help the bare HBM write pattern (store-only probe: band 4 /
+        // 8 / 16 = 122 / 125 / 134 us at 8K) and the plain default-taps SR
+        // kernel by ~1% at band 8, but cost 3-10% on every issue-bound
+        // variant (generic taps, pad, prefetch off, SR32); taller bands lose
+        // 2-6% (256x1080p, 32768^2: profiles/r1/band_sweep.txt).  Images too
+        // small to fill one wave of CTAs get shorter bands.
+        int band = 16;
+        while (band > 4 && ctas(band) < 148 * 4) band /= 2;
+        return band;
+    }
+    // u8-only / detect passes are issue-bound and prefer taller bands (the
+    // 4 halo rows are 4/band of the row work): 8K u8 57.5 us at 32 vs 59.7
+    // at 16 and 64; keep >= ~16 CTAs per SM for the last partial wave.
     int band = 64;
-    // keep >= ~16 CTAs per SM (4 resident x 4 waves) so the last partial
-    // wave costs little; measured on B200 at 8K SR: band 16 141.9 us, 32
-    // 146.9 us, 64 149.6 us (tools/sweep.py).  Contracts without wide planes
-    // (u8, detect passes) are issue-bound and prefer 32 (halo rows are 4/band
-    // of the row work): 8K u8 57.5 us at 32 vs 59.7 at 16 and 64.
-    const int floor_band = narrow_only ? 32 : 16;
-    while (band > floor_band && cols * frames * ((out_h + band - 1) / band) < 148 * 16) band /= 2;
+    while (band > 32 && ctas(band) < 148 * 16) band /= 2;
     return band;
 }
 

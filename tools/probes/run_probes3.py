@@ -36,3 +36,11 @@ for name in ("reg_planes", "tma_warp", "tma_cta"):
         print(f"{name:11s} band={band:3d}: {us:6.1f} us {byts/us/1e3:5.0f} GB/s", flush=True)
 t = torch.empty(byts // 4, dtype=torch.int32, device="cuda")
 us = timeit(lambda: t.fill_(3)); print(f"torch fill_: {us:.1f} us {byts/us/1e3:.0f} GB/s")
+for warps in (1, 2, 8, 16):
+    f = fn(f"_Z12reg_planes_wILi{warps}EEvPcS0_S0_S0_S0_liii")
+    for band in (4, 8, 16, 32):
+        args = [(p.data_ptr(), np.uint64) for p in pl] + [(g.data_ptr(), np.uint64), (pitch, np.int64),
+                (W, np.int32), (H, np.int32), (band, np.int32)]
+        cols = 128 * warps
+        us = timeit(lambda: launch(f, ((W + cols - 1) // cols, (H + band - 1) // band, 1), (32 * warps, 1, 1), args))
+        print(f"reg warps={warps:2d} band={band:3d}: {us:6.1f} us {byts/us/1e3:5.0f} GB/s", flush=True)

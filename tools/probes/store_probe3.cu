@@ -117,3 +117,28 @@ __global__ void __launch_bounds__(128) tma_cta(char* gx, char* gy, char* gd, cha
     }
     if (t == 0) bulk_wait_read<0>();
 }
+
+// register stores with a configurable CTA width (WARPS warps side by side)
+template <int WARPS>
+__global__ void __launch_bounds__(32 * WARPS) reg_planes_w(char* gx, char* gy, char* gd, char* gdt,
+                                                          char* g, int64_t pitch, int out_w,
+                                                          int out_h, int band) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int x0 = (blockIdx.x * WARPS + warp) * 128 + lane * 4;
+    if (x0 >= out_w) return;
+    const int oy0 = blockIdx.y * band;
+    const int n = min(band, out_h - oy0);
+    for (int v = 0; v < n; ++v) {
+        const int64_t o = static_cast<int64_t>(oy0 + v) * pitch + x0;
+        const uint32_t a = v + x0;
+        stcs4(gx + o * 4, a);
+        stcs4(gy + o * 4, a);
+        stcs4(gd + o * 4, a);
+        stcs4(gdt + o * 4, a);
+        stcs8(g + o * 8, a);
+    }
+}
+template __global__ void reg_planes_w<1>(char*, char*, char*, char*, char*, int64_t, int, int, int);
+template __global__ void reg_planes_w<2>(char*, char*, char*, char*, char*, int64_t, int, int, int);
+template __global__ void reg_planes_w<8>(char*, char*, char*, char*, char*, int64_t, int, int, int);
+template __global__ void reg_planes_w<16>(char*, char*, char*, char*, char*, int64_t, int, int, int);
