@@ -237,8 +237,11 @@ sobel5_status sobel5_ipc_release(const void* d_ptr);
  * Device self-check of the epilogue arithmetic over every integer S in
  * [lo, hi): which = 0 compares the kernels' double sqrt with IEEE
  * __dsqrt_rn((double)S); which = 1 compares the uint8 clamp_abs shortcut with
- * min(255, round(sqrt(S))).  Adds the number of mismatches to *d_count
- * (device pointer, unsigned 64-bit). */
+ * min(255, round(sqrt(S))); which = 2 checks the packed-float u8 epilogue
+ * of the u8-only kernels on every integer S <= 65280 in range, and which = 3
+ * on every float S >= 65281 whose bit pattern is in [lo, hi) (expects 255).
+ * Adds the number of mismatches to *d_count (device pointer, unsigned
+ * 64-bit). */
 sobel5_status sobel5_selftest(int which, uint32_t lo, uint32_t hi, uint64_t* d_count,
                               void* stream);
 

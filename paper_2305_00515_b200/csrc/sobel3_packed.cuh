@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtasPerSm)
     const bool u8_norm = RT ? p.u8_norm != 0 : (OUTS & kOutNorm) != 0;
     const bool w_s = RT ? p.s32 != nullptr : (OUTS & kOutS32) != 0;
     const bool need_g = w_g || w_g32;
+    constexpr bool FU8 = OUTS == kOutU8;  // clamp_abs edge map alone
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int warp_x0 = (blockIdx.x * kCtaWarps + warp) * kWarpCols;
@@ -130,7 +131,26 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtasPerSm)
                 ax[s2][q] += f;       // i = 2 closes output row r - 2
                 ay[s2][q] += hh;
             }
-            if (r >= 2) {
+            if (FU8 && r >= 2) {
+                // u8 clamp_abs only: packed-float epilogue (sobel5_packed.cuh);
+                // S = gx^2 + gy^2 < 2^21 is exact in FP32
+                const int64_t row_off = out_off;
+                out_off += p.pitch;
+                uint32_t u[4];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {  // pair q holds pixels (q, q + 2)
+                    const float2 fx = pair_to_float2(ax[s2][q] + kPairBias);
+                    const float2 fy = pair_to_float2(ay[s2][q] + kPairBias);
+                    u8_from_sf2(__ffma2_rn(fy, fy, __fmul2_rn(fx, fx)), u[q], u[q + 2]);
+                }
+                if (full) {
+                    st_cs_u32(p.u8 + row_off, pack_u8x4(u[0], u[1], u[2], u[3]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (x0 + j < p.out_w) p.u8[row_off + j] = static_cast<uint8_t>(u[j]);
+                }
+            } else if (r >= 2) {
                 int32_t gx[4], gy[4];
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {

@@ -317,11 +317,26 @@ __global__ void selftest_kernel(int which, uint32_t lo, uint32_t hi,
         if (which == 0) {
             const double a = sqrt_u30(S), b = __dsqrt_rn(static_cast<double>(S));
             bad += __double_as_longlong(a) != __double_as_longlong(b);
-        } else {
+        } else if (which == 1) {
             const double g = __dsqrt_rn(static_cast<double>(S));
             const double r = round(g);
             const uint32_t want = r < 255.0 ? static_cast<uint32_t>(r) : 255u;
             bad += u8_from_s(S) != want;
+        } else if (which == 2) {
+            // packed-float u8 epilogue on exact integer sums S <= 65280
+            if (S > 65280u) continue;
+            const double r = round(__dsqrt_rn(static_cast<double>(S)));
+            const uint32_t want = r < 255.0 ? static_cast<uint32_t>(r) : 255u;
+            uint32_t a, b;
+            u8_from_sf2(make_float2(static_cast<float>(S), static_cast<float>(S)), a, b);
+            bad += (a != want) + (b != want);
+        } else {
+            // ... and on every float sum >= 65281 (S = float bit pattern)
+            const float f = __uint_as_float(S);
+            if (!(f >= 65281.0f) || isinf(f)) continue;
+            uint32_t a, b;
+            u8_from_sf2(make_float2(f, f), a, b);
+            bad += (a != 255u) + (b != 255u);
         }
     }
     if (bad) atomicAdd(count, bad);
@@ -459,7 +474,7 @@ sobel5_status sobel5_launch_band(const uint8_t* d_top, const uint8_t* d_in, cons
 
 sobel5_status sobel5_selftest(int which, uint32_t lo, uint32_t hi, uint64_t* d_count,
                               void* stream) {
-    if (!d_count || hi < lo || (which != 0 && which != 1)) return SOBEL5_INVALID_ARG;
+    if (!d_count || hi < lo || which < 0 || which > 3) return SOBEL5_INVALID_ARG;
     if (which == 0 && hi > (1u << 30)) return SOBEL5_INVALID_ARG;
     selftest_kernel<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         which, lo, hi, reinterpret_cast<unsigned long long*>(d_count));

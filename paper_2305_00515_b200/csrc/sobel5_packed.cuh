@@ -78,6 +78,48 @@ __device__ __forceinline__ uint32_t u8_from_s(uint32_t S) {
     return static_cast<uint32_t>(__float2int_rn(y));
 }
 
+// ---- u8-only epilogue in packed FP32 (the issue-bound clamp_abs contract) --
+//
+// A packed register V = lo + hi * 2^16 (|lo|, |hi| < 2^15) biased by
+// 0x80008000 holds lo + 2^15 and hi + 2^15 as its two unsigned halves (no
+// carry crosses).  One byte permute per half splices a half under the
+// exponent of 2^23 (0x4B00xxxx = 2^23 + half), so after one packed FADD2 the
+// pair is {lo, hi} as exact floats: 1.5 instructions per value instead of the
+// integer extraction's 1.5 plus 1 IMAD per square.
+constexpr uint32_t kPairBias = 0x80008000u;
+__device__ __forceinline__ float2 pair_to_float2(uint32_t w_biased) {
+    const float lo = __uint_as_float(__byte_perm(w_biased, 0x4B000000u, 0x7610));
+    const float hi = __uint_as_float(__byte_perm(w_biased, 0x4B000000u, 0x7632));
+    return __fadd2_rn(make_float2(lo, hi), make_float2(-8421376.0f, -8421376.0f));  // 2^23 + 2^15
+}
+// Sum of four squares with packed FMAs.  Exact whenever the true sum is
+// <= 65280 (every partial sum is then an integer below 2^24); when the true
+// sum is >= 65281 the rounded partial sums are non-decreasing and the first
+// one above 65280 rounds to >= 65281 (representable), so the result is
+// >= 65281 -- exactly what clamp_abs needs (saturation at 255).
+__device__ __forceinline__ float2 sumsq4(float2 a, float2 b, float2 c, float2 d) {
+    return __ffma2_rn(d, d, __ffma2_rn(c, c, __ffma2_rn(b, b, __fmul2_rn(a, a))));
+}
+// clamp_abs of sqrt(S) for the float S above: S * rsqrt(S) (MUFU.RSQ) is
+// within 7e-5 of sqrt(S), sqrt(S) is never within 4.9e-4 of k + 0.5 for
+// integer S <= 65280, and cvt.rni.sat.u8 rounds and saturates in one
+// instruction (S >= 65281 -> >= 255.5 -> 255).  S = 0 gives 0 * inf = NaN,
+// which the conversion maps to 0.  Checked for every integer S <= 65280 and
+// every float S >= 65281 by sobel5_selftest(2 / 3).
+__device__ __forceinline__ uint32_t u8_from_sf(float y_times_rsqrt) {
+    uint32_t r;
+    asm("cvt.rni.sat.u8.f32 %0, %1;" : "=r"(r) : "f"(y_times_rsqrt));
+    return r;
+}
+__device__ __forceinline__ void u8_from_sf2(float2 S, uint32_t& a, uint32_t& b) {
+    float ra, rb;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(S.x));
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rb) : "f"(S.y));
+    const float2 y = __fmul2_rn(S, make_float2(ra, rb));
+    a = u8_from_sf(y.x);
+    b = u8_from_sf(y.y);
+}
+
 // ---- TMA bulk stores (cp.async.bulk global <- shared, bulk-group completion)
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
@@ -155,6 +197,8 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtasPerSm)
     const bool u8_norm = RT ? p.u8_norm != 0 : (OUTS & kOutNorm) != 0;
     const bool w_s = RT ? p.s32 != nullptr : (OUTS & kOutS32) != 0;
     const bool need_g = w_g || w_g32;
+    // the clamp_abs edge map alone: packed-float epilogue (u8_from_sf2)
+    constexpr bool FU8 = !RTAPS && OUTS == kOutU8;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int warp_x0 = (blockIdx.x * kCtaWarps + warp) * kWarpCols;
@@ -389,7 +433,28 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtasPerSm)
                 }
             }
 
-            if (r >= 4) {
+            if (FU8 && r >= 4) {
+                // u8 clamp_abs only: packed-float epilogue, no lane extraction
+                const int sl = (s + 1) % 5;
+                const int64_t row_off = out_off;
+                out_off += p.pitch;
+                uint32_t u[4];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {  // pair q holds pixels (q, q + 2)
+                    const float2 fx = pair_to_float2(ax[sl][q] + kPairBias);
+                    const float2 fy = pair_to_float2(ay[sl][q] + kPairBias);
+                    const float2 fd = pair_to_float2(an[sl][q] - aq[sl][q] + kPairBias);
+                    const float2 ft = pair_to_float2(0u - an[sl][q] - aq[sl][q] + kPairBias);
+                    u8_from_sf2(sumsq4(fx, fy, fd, ft), u[q], u[q + 2]);
+                }
+                if (full) {
+                    st_cs_u32(p.u8 + row_off, pack_u8x4(u[0], u[1], u[2], u[3]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (x0 + j < p.out_w) p.u8[row_off + j] = static_cast<uint8_t>(u[j]);
+                }
+            } else if (r >= 4) {
                 const int sl = (s + 1) % 5;
                 int32_t gx[4], gy[4], gd[4], gdt[4];
                 if constexpr (RTAPS) {

@@ -102,28 +102,33 @@ __device__ __forceinline__ uint32_t ld_row_word(const uint8_t* p) {
     return __ldg(reinterpret_cast<const unsigned int*>(p));
 }
 
+// Store qualifier of the output streams (compile-time knob for experiments;
+// default .cs = evict-first streaming, the outputs are not re-read).
+#ifndef SOBEL5_ST_Q
+#define SOBEL5_ST_Q ".cs"
+#endif
 __device__ __forceinline__ void st_cs_v4(int32_t* p, int32_t a, int32_t b, int32_t c, int32_t d) {
-    asm volatile("st.global.cs.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c),
+    asm volatile("st.global" SOBEL5_ST_Q ".v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c),
                  "r"(d)
                  : "memory");
 }
 __device__ __forceinline__ void st_cs_v4f(float* p, float a, float b, float c, float d) {
-    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+    asm volatile("st.global" SOBEL5_ST_Q ".v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
                  "f"(d)
                  : "memory");
 }
 __device__ __forceinline__ void st_cs_v2d(double* p, double a, double b) {
-    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+    asm volatile("st.global" SOBEL5_ST_Q ".v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
 }
 // 256-bit store (STG.E.ENL2.256, sm_100): 4 doubles = 32 B per lane, one
 // instruction; measured ~6% more write bandwidth than two 128-bit stores.
 __device__ __forceinline__ void st_cs_v4d(double* p, double a, double b, double c, double d) {
-    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
+    asm volatile("st.global" SOBEL5_ST_Q ".v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
                  "d"(d)
                  : "memory");
 }
 __device__ __forceinline__ void st_cs_u32(uint8_t* p, uint32_t v) {
-    asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    asm volatile("st.global" SOBEL5_ST_Q ".u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // clamp_abs (image_io.hpp:235-240): min(255, round(|g|)); g >= 0 here and
