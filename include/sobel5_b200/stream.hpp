@@ -13,12 +13,18 @@
 //     per-row/per-call bookkeeping, not the per-pixel path.
 #pragma once
 
+#include <sys/mman.h>
+
 #include <array>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
+#include <exception>
 #include <memory>
 #include <span>
 #include <string>
+#include <thread>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -381,6 +387,117 @@ inline void run(const GrayPlane& img, const StreamTaps& taps, Prefetch prefetch,
     raise(st, "run_stream", &d);
 }
 
+/// Empty storage for n elements with transparent huge pages advised on it
+/// before the first touch: fresh result planes are page-fault bound on the
+/// host (795 MB at 8K: 290 ms as five serial value-initialised
+/// std::vector(n) on the B200 host; profiles/r1/alloc_probe.txt).  Returns
+/// the page range of the storage for pre-faulting.
+template <typename T>
+inline std::pair<std::uintptr_t, std::uintptr_t> huge_reserve(std::vector<T>& v, std::size_t n) {
+    v.reserve(n);
+    constexpr std::uintptr_t kHuge = std::uintptr_t{2} << 20, kPage = 4096;
+    const auto p = reinterpret_cast<std::uintptr_t>(v.data());
+    const std::uintptr_t a = (p + kHuge - 1) & ~(kHuge - 1), e = (p + n * sizeof(T)) & ~(kHuge - 1);
+    if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);  // advisory only
+    return {p & ~(kPage - 1), (p + n * sizeof(T) + kPage - 1) & ~(kPage - 1)};
+}
+
+/// Pre-faults page ranges with MADV_POPULATE_WRITE (Linux >= 5.14; a no-op
+/// elsewhere) on 4 threads: the kernel zeroes the pages without any
+/// user-space access to the not-yet-constructed storage.  Four threads is
+/// the measured optimum on the B200 host (22 ms for 795 MB; 8 or 16 threads
+/// contend and take 56 ms: profiles/r1/populate_probe.txt).
+inline void prefault(const std::vector<std::pair<std::uintptr_t, std::uintptr_t>>& ranges) {
+#ifdef __linux__
+    constexpr int kPopulateWrite = 23;  // MADV_POPULATE_WRITE
+    constexpr std::uintptr_t kPiece = std::uintptr_t{8} << 20;
+    std::vector<std::pair<std::uintptr_t, std::uintptr_t>> pieces;
+    for (const auto& [a, e] : ranges)
+        for (std::uintptr_t o = a; o < e; o += kPiece) pieces.emplace_back(o, std::min(e, o + kPiece));
+    std::atomic<std::size_t> next{0};
+    auto work = [&] {
+        for (std::size_t i; (i = next.fetch_add(1)) < pieces.size();)
+            if (madvise(reinterpret_cast<void*>(pieces[i].first), pieces[i].second - pieces[i].first,
+                        kPopulateWrite) != 0)
+                return;  // unsupported kernel: the first touch faults instead
+    };
+    std::thread th[3];
+    for (auto& t : th) t = std::thread(work);
+    work();
+    for (auto& t : th) t.join();
+#else
+    (void)ranges;
+#endif
+}
+
+/// run() for the five StreamResult planes, built while the device works: the
+/// pipeline is enqueued first (sobel5_run_host_begin, results into pinned
+/// staging); the planes' storage is reserved with huge pages and pre-faulted,
+/// then one host thread per plane appends each row chunk as soon as its
+/// download lands (sobel5_run_host_chunk), so the planes are never
+/// zero-filled in user space and the host copy overlaps the transfers.
+/// The result equals the reference's value-initialised-then-written planes.
+inline void run_alloc(const GrayPlane& img, const StreamTaps& taps, Prefetch prefetch, StreamResult& out) {
+    const sobel5_taps t = to_abi(taps);
+    sobel5_ctx* c = thread_context().get();
+    const int ow = img.width() - 4, oh = img.height() - 4;
+    const std::size_t n = static_cast<std::size_t>(ow) * static_cast<std::size_t>(oh);
+    sobel5_status st = sobel5_run_host_begin(c, img.data().data(), img.width(), img.height(), &t,
+                                             prefetch == Prefetch::on ? 1 : 0, 0x1fu);
+    if (st == SOBEL5_CUDA_ERROR || st == SOBEL5_OUT_OF_MEMORY)
+        raise(st, std::string("run_stream (") + sobel5_ctx_last_error(c) + ")");
+    raise(st, "run_stream");
+    std::vector<std::int32_t> iv[4];
+    std::vector<double> gv;
+    std::exception_ptr errs[5];
+    bool chunk_failed[5] = {};
+    auto fill = [&](int plane, auto& v) {
+        try {
+            using T = typename std::decay_t<decltype(v)>::value_type;
+            const T* src = static_cast<const T*>(sobel5_run_host_staging(c, plane));
+            int y0 = 0, y1 = 0;
+            for (int k = 0; sobel5_run_host_chunk(c, k, &y0, &y1) == SOBEL5_OK; ++k)
+                v.insert(v.end(), src + static_cast<std::size_t>(y0) * ow, src + static_cast<std::size_t>(y1) * ow);
+            chunk_failed[plane] = v.size() != n;
+        } catch (...) {
+            errs[plane] = std::current_exception();
+        }
+    };
+    try {
+        std::vector<std::pair<std::uintptr_t, std::uintptr_t>> ranges;
+        for (auto& v : iv) ranges.push_back(huge_reserve(v, n));
+        ranges.push_back(huge_reserve(gv, n));
+        if (n >= (std::size_t{1} << 22)) prefault(ranges);  // below ~4K the threads cost more
+    } catch (...) {
+        errs[0] = std::current_exception();
+    }
+    if (errs[0]) {
+    } else if (n < (std::size_t{1} << 18)) {
+        for (int i = 0; i < 4; ++i) fill(i, iv[i]);
+        fill(4, gv);
+    } else {
+        std::thread th[4];
+        for (int i = 0; i < 4; ++i) th[i] = std::thread([&, i] { fill(i, iv[i]); });
+        fill(4, gv);
+        for (auto& x : th) x.join();
+    }
+    sobel5_diag d{};
+    st = sobel5_run_host_finish(c, nullptr, &d);  // completes the call: status + diag
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    if (st == SOBEL5_OK)
+        for (bool f : chunk_failed)
+            if (f) st = SOBEL5_CUDA_ERROR;
+    if (st == SOBEL5_CUDA_ERROR || st == SOBEL5_OUT_OF_MEMORY)
+        raise(st, std::string("run_stream (") + sobel5_ctx_last_error(c) + ")");
+    raise(st, "run_stream", &d);
+    out.gx = SignedPlane(ow, oh, std::move(iv[0]));
+    out.gy = SignedPlane(ow, oh, std::move(iv[1]));
+    out.gd = SignedPlane(ow, oh, std::move(iv[2]));
+    out.gdt = SignedPlane(ow, oh, std::move(iv[3]));
+    out.g = RealPlane(ow, oh, std::move(gv));
+}
+
 /// The clamp_abs uint8 edge map (image_io.hpp:235-240 applied to g),
 /// computed in the same fused kernel; (W-4) x (H-4).
 inline GrayPlane edge_map_u8(const GrayPlane& img, const StreamTaps& taps, Prefetch prefetch = Prefetch::on) {
@@ -432,14 +549,7 @@ inline StreamResult run_stream(const GrayPlane& img, const StreamTaps& taps, con
         throw DimMismatch("strip plan covers " + std::to_string(plan.in_width) + " columns at radius " +
                           std::to_string(plan.radius) + ", image has " + std::to_string(img.width()));
     StreamResult out;
-    const int ow = img.width() - 4, oh = img.height() - 4;
-    out.gx = SignedPlane(ow, oh);
-    out.gy = SignedPlane(ow, oh);
-    out.gd = SignedPlane(ow, oh);
-    out.gdt = SignedPlane(ow, oh);
-    out.g = RealPlane(ow, oh);
-    gpu::Outputs o{&out.gx, &out.gy, &out.gd, &out.gdt, &out.g, nullptr};
-    gpu::run(img, taps, prefetch, o);
+    gpu::run_alloc(img, taps, prefetch, out);
     out.counters = stream_counters(img.height(), plan, taps, prefetch);
     return out;
 }

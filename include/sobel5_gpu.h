@@ -261,6 +261,31 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
                               const sobel5_taps* taps, int prefetch, const sobel5_planes* h_out,
                               sobel5_diag* diag_out);
 
+/* Split form of sobel5_run_host for callers that allocate their result
+ * planes while the device works (the C++ run_stream does): _begin enqueues
+ * upload, kernels and downloads into the context's pinned staging and
+ * returns; _finish waits chunk by chunk and copies the planes selected by
+ * plane_mask (bit i = gx, gy, gd, gdt, g, g32, u8) into h_out, whose
+ * non-NULL planes must match the mask exactly (pitch == width-4), or with
+ * h_out = NULL only completes the call.  One
+ * begin/finish pair at a time per context; sobel5_run_host in between
+ * returns SOBEL5_INVALID_ARG.  Pageable destinations anywhere in this API go
+ * through pinned staging plus a small host thread pool; page-locked ones
+ * (cudaMallocHost / cudaHostRegister) are DMA'd directly. */
+sobel5_status sobel5_run_host_begin(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
+                                    const sobel5_taps* taps, int prefetch, unsigned plane_mask);
+sobel5_status sobel5_run_host_finish(sobel5_ctx* ctx, const sobel5_planes* h_out,
+                                     sobel5_diag* diag_out);
+/* Between _begin and _finish the staged planes can also be consumed as
+ * they arrive: _chunk blocks until row chunk `chunk` (0, 1, ... while it
+ * returns SOBEL5_OK) of every plane is in staging and gives its output rows
+ * [*y0, *y1); _staging is the pinned, tightly packed plane i of the mask
+ * (NULL otherwise).  Both may be called from several host threads.  Then
+ * _finish with h_out = NULL completes the call (status, diag) without
+ * copying. */
+sobel5_status sobel5_run_host_chunk(sobel5_ctx* ctx, int chunk, int* y0, int* y1);
+const void* sobel5_run_host_staging(const sobel5_ctx* ctx, int plane);
+
 /* ---- the classic 3x3 two-direction operator ---------
  * run_stream_3x3 (pipeline.hpp:551-573) / sobel3_2d (oracle.hpp:58-70):
  * gx, gy int32 and g double (plus optional g32 / u8 clamp_abs) of a valid

@@ -77,7 +77,8 @@ EXPORTS = (
     "sobel5_ipc_import", "sobel5_ipc_release", "sobel5_launch_ex", "sobel5_detect",
     "sobel5_detect_scratch_bytes", "sobel5_quantize_plane", "sobel5_detect_host",
     "sobel3_launch", "sobel3_detect", "sobel3_plan_counters", "sobel3_run_host",
-    "sobel5_quantize_host",
+    "sobel5_quantize_host", "sobel5_run_host_begin", "sobel5_run_host_finish",
+    "sobel5_run_host_chunk", "sobel5_run_host_staging",
 )
 
 _lib = None
@@ -127,6 +128,14 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.sobel5_run_host.argtypes = [vp, vp, i32, i32, C.POINTER(Taps), i32, C.POINTER(Planes),
                                   C.POINTER(Diag)]
     L.sobel5_run_host.restype = i32
+    L.sobel5_run_host_begin.argtypes = [vp, vp, i32, i32, C.POINTER(Taps), i32, C.c_uint32]
+    L.sobel5_run_host_begin.restype = i32
+    L.sobel5_run_host_finish.argtypes = [vp, C.POINTER(Planes), C.POINTER(Diag)]
+    L.sobel5_run_host_finish.restype = i32
+    L.sobel5_run_host_chunk.argtypes = [vp, i32, C.POINTER(i32), C.POINTER(i32)]
+    L.sobel5_run_host_chunk.restype = i32
+    L.sobel5_run_host_staging.argtypes = [vp, i32]
+    L.sobel5_run_host_staging.restype = vp
     L.sobel5_ipc_export.argtypes = [vp, C.POINTER(IpcHandle)]
     L.sobel5_ipc_export.restype = i32
     L.sobel5_ipc_import.argtypes = [C.POINTER(IpcHandle), C.POINTER(vp)]

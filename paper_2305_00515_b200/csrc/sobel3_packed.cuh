@@ -24,7 +24,7 @@ namespace sobel5_b200 {
 // PF: 0 = load each row when consumed (Prefetch::off), 1 = 6-row register
 // prefetch ring (Prefetch::on).  PAD: pad_replicate(img, 1) fused.
 template <int PF, bool PAD, int OUTS>
-__global__ void __launch_bounds__(kCtaThreads, kMinCtasPerSm)
+__global__ void __launch_bounds__(kCtaThreads, OUTS == kOutU8 ? SOBEL5_U8_MIN_CTAS : kMinCtasPerSm)
     sobel3_packed_kernel(const __grid_constant__ KernelParams p) {
     constexpr bool RT = OUTS == kOutRuntime;
     const bool w_gx = RT ? p.gx != nullptr : (OUTS & kOutGx) != 0;

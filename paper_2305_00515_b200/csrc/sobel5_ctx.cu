@@ -14,12 +14,105 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdint>
 #include <cstring>
+#include <functional>
+#include <memory>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "sobel5_gpu.h"
+
+namespace {
+
+// Host worker pool for the copies between pinned staging and pageable caller
+// memory (one host thread moves ~14 GB/s, four or more ~50 GB/s on the B200
+// host: profiles/r1/alloc_probe.txt).  The calling thread takes part.
+class HostPool {
+public:
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    // fn(i) for i in [0, n), returns when all are done
+    void run(int n, const std::function<void(int)>& fn) {
+        if (n <= 0) return;
+        if (th_.empty()) start();
+        auto b = std::make_shared<Batch>();
+        b->fn = &fn;
+        b->n = n;
+        b->left = n;
+        {
+            std::lock_guard<std::mutex> g(m_);
+            batch_ = b;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work(*b);
+        std::unique_lock<std::mutex> g(b->m);
+        b->done.wait(g, [&] { return b->left == 0; });
+    }
+    int size() const { return static_cast<int>(th_.size()) + 1; }
+
+private:
+    // One run(): a worker that wakes late only sees next >= n and leaves
+    // without touching fn (which may be gone by then).
+    struct Batch {
+        const std::function<void(int)>* fn = nullptr;
+        int n = 0;
+        std::atomic<int> next{0};
+        int left = 0;
+        std::mutex m;
+        std::condition_variable done;
+    };
+    void start() {
+        const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+        const int n = static_cast<int>(std::min(8u, hw) - 1);
+        for (int i = 0; i < n; ++i) th_.emplace_back([this] { loop(); });
+    }
+    static void work(Batch& b) {
+        int done = 0;
+        for (int i; (i = b.next.fetch_add(1)) < b.n;) {
+            (*b.fn)(i);
+            ++done;
+        }
+        if (done) {
+            std::lock_guard<std::mutex> g(b.m);
+            b.left -= done;
+            if (b.left == 0) b.done.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            std::shared_ptr<Batch> b;
+            {
+                std::unique_lock<std::mutex> g(m_);
+                cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                b = batch_;
+            }
+            if (b) work(*b);
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_;
+    std::shared_ptr<Batch> batch_;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+}  // namespace
 
 struct sobel5_ctx {
     int device = 0;
@@ -32,7 +125,20 @@ struct sobel5_ctx {
     sobel5_diag* h_diag = nullptr;  // pinned
     void* d_scratch = nullptr;      // detect / normalize scratch
     size_t d_scratch_bytes = 0;
-    std::vector<cudaEvent_t> ev_in, ev_comp;
+    // pinned staging: the input image and the planes bound for pageable memory
+    void* h_in_stage = nullptr;
+    size_t h_in_stage_bytes = 0;
+    void* h_stage[7] = {};
+    size_t h_stage_bytes[7] = {};
+    std::vector<cudaEvent_t> ev_in, ev_comp, ev_out;
+    HostPool pool;
+    // state between sobel5_run_host_begin and _finish
+    struct Pending {
+        bool active = false;
+        int out_w = 0, out_h = 0, chunk = 0, n_chunks = 0;
+        unsigned mask = 0;
+        sobel5_status status = SOBEL5_OK;
+    } pend;
     std::string last_error;
 };
 
@@ -65,6 +171,16 @@ cudaError_t ensure(void** p, size_t* cap, size_t bytes) {
     return e;
 }
 
+cudaError_t ensure_host(void** p, size_t* cap, size_t bytes) {
+    if (*cap >= bytes) return cudaSuccess;
+    if (*p) cudaFreeHost(*p);
+    *p = nullptr;
+    *cap = 0;
+    cudaError_t e = cudaMallocHost(p, bytes);
+    if (e == cudaSuccess) *cap = bytes;
+    return e;
+}
+
 cudaError_t ensure_events(std::vector<cudaEvent_t>& v, size_t n) {
     while (v.size() < n) {
         cudaEvent_t ev;
@@ -73,6 +189,180 @@ cudaError_t ensure_events(std::vector<cudaEvent_t>& v, size_t n) {
         v.push_back(ev);
     }
     return cudaSuccess;
+}
+
+// Page-locked host memory (cudaMallocHost / cudaHostRegister) is DMA'd
+// directly; anything else goes through the context's pinned staging.
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// Parallel memcpy of n bytes in >= 4 MiB pieces on the context's pool.
+void par_copy(sobel5_ctx* ctx, void* dst, const void* src, size_t n) {
+    constexpr size_t kPiece = size_t{4} << 20;
+    const int pieces = static_cast<int>(std::min<size_t>(
+        static_cast<size_t>(ctx->pool.size()) * 2, std::max<size_t>(1, n / kPiece)));
+    if (pieces <= 1) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    const size_t per = (n + pieces - 1) / pieces;
+    ctx->pool.run(pieces, [&](int i) {
+        const size_t o = static_cast<size_t>(i) * per;
+        if (o < n)
+            std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                        std::min(per, n - o));
+    });
+}
+
+// Enqueues the chunked H2D -> kernel -> D2H pipeline of run_stream on the
+// context's streams.  dst[i] is the host destination of plane i (tightly
+// packed, out_w pitch), or nullptr with bit i of `mask` set to land the
+// plane in the pinned staging buffer h_stage[i].  ev_out[k] marks chunk k's
+// downloads.
+sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
+                             const sobel5_taps* taps, int prefetch, unsigned mask,
+                             void* const dst[7], int* chunk_out, int* n_chunks_out) {
+    const int out_w = width - 4, out_h = height - 4;
+    const int64_t in_pitch = round_up(width, 128);
+    const int64_t dpitch = round_up(out_w, 32);  // elements; 128 B-aligned int rows
+    CK(ensure(reinterpret_cast<void**>(&ctx->d_in), &ctx->d_in_bytes,
+              static_cast<size_t>(in_pitch) * height));
+    // a pageable input is first copied into pinned staging (in parallel) so
+    // the uploads below are true async DMA
+    const uint8_t* src_in = h_in;
+    if (!is_pinned(h_in)) {
+        const size_t n = static_cast<size_t>(width) * height;
+        CK(ensure_host(&ctx->h_in_stage, &ctx->h_in_stage_bytes, n));
+        par_copy(ctx, ctx->h_in_stage, h_in, n);
+        src_in = static_cast<const uint8_t*>(ctx->h_in_stage);
+    }
+    sobel5_planes dp{};
+    dp.pitch = dpitch;
+    void** dslots[7] = {reinterpret_cast<void**>(&dp.gx),  reinterpret_cast<void**>(&dp.gy),
+                        reinterpret_cast<void**>(&dp.gd),  reinterpret_cast<void**>(&dp.gdt),
+                        reinterpret_cast<void**>(&dp.g),   reinterpret_cast<void**>(&dp.g32),
+                        reinterpret_cast<void**>(&dp.u8)};
+    void* hdst[7] = {};
+    for (int i = 0; i < 7; ++i) {
+        if (!((mask >> i) & 1u)) continue;
+        const size_t plane_bytes = static_cast<size_t>(out_w) * out_h * kElem[i];
+        CK(ensure(&ctx->d_plane[i], &ctx->d_plane_bytes[i],
+                  static_cast<size_t>(dpitch) * out_h * kElem[i]));
+        *dslots[i] = ctx->d_plane[i];
+        if (dst[i]) {
+            hdst[i] = dst[i];
+        } else {
+            CK(ensure_host(&ctx->h_stage[i], &ctx->h_stage_bytes[i], plane_bytes));
+            hdst[i] = ctx->h_stage[i];
+        }
+    }
+
+    // Row chunks: enough to overlap copies with compute, few enough that
+    // each kernel still fills the GPU.
+    int chunk = std::max(256, (out_h + 7) / 8);
+    chunk = std::min(chunk, out_h);
+    const int n_chunks = (out_h + chunk - 1) / chunk;
+    CK(ensure_events(ctx->ev_in, static_cast<size_t>(n_chunks)));
+    CK(ensure_events(ctx->ev_comp, static_cast<size_t>(n_chunks)));
+    CK(ensure_events(ctx->ev_out, static_cast<size_t>(n_chunks)));
+    CK(cudaMemsetAsync(ctx->d_diag, 0, sizeof(sobel5_diag), ctx->s_comp));
+
+    int uploaded = 0;  // input rows already enqueued
+    for (int k = 0; k < n_chunks; ++k) {
+        const int y0 = k * chunk, y1 = std::min(out_h, y0 + chunk);
+        const int need = y1 + 4;  // input rows [y0, y1 + 4)
+        CK(cudaMemcpy2DAsync(ctx->d_in + static_cast<int64_t>(uploaded) * in_pitch, in_pitch,
+                             src_in + static_cast<int64_t>(uploaded) * width, width, width,
+                             need - uploaded, cudaMemcpyHostToDevice, ctx->s_h2d));
+        uploaded = need;
+        CK(cudaEventRecord(ctx->ev_in[k], ctx->s_h2d));
+        CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_in[k], 0));
+        sobel5_planes sub = dp;
+        const int64_t off = static_cast<int64_t>(y0) * dpitch;
+        if (sub.gx) sub.gx += off;
+        if (sub.gy) sub.gy += off;
+        if (sub.gd) sub.gd += off;
+        if (sub.gdt) sub.gdt += off;
+        if (sub.g) sub.g += off;
+        if (sub.g32) sub.g32 += off;
+        if (sub.u8) sub.u8 += off;
+        const sobel5_status st =
+            sobel5_launch(ctx->d_in + static_cast<int64_t>(y0) * in_pitch, in_pitch, width,
+                          y1 - y0 + 4, taps, prefetch, &sub, ctx->d_diag, ctx->s_comp);
+        if (st != SOBEL5_OK) {
+            ctx->last_error = cudaGetErrorString(cudaGetLastError());
+            return st;
+        }
+        CK(cudaEventRecord(ctx->ev_comp[k], ctx->s_comp));
+        CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_comp[k], 0));
+        for (int i = 0; i < 7; ++i) {
+            if (!hdst[i]) continue;
+            const size_t es = kElem[i];
+            CK(cudaMemcpy2DAsync(static_cast<char*>(hdst[i]) + static_cast<size_t>(y0) * out_w * es,
+                                 static_cast<size_t>(out_w) * es,
+                                 static_cast<char*>(ctx->d_plane[i]) +
+                                     static_cast<size_t>(y0) * dpitch * es,
+                                 static_cast<size_t>(dpitch) * es, static_cast<size_t>(out_w) * es,
+                                 static_cast<size_t>(y1 - y0), cudaMemcpyDeviceToHost,
+                                 ctx->s_d2h));
+        }
+        CK(cudaEventRecord(ctx->ev_out[k], ctx->s_d2h));
+    }
+    CK(cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(sobel5_diag), cudaMemcpyDeviceToHost,
+                       ctx->s_d2h));
+    *chunk_out = chunk;
+    *n_chunks_out = n_chunks;
+    return SOBEL5_OK;
+}
+
+// Waits for the downloads chunk by chunk and moves the staged planes
+// (stage_dst[i] != nullptr) into the caller's pageable memory while the later
+// chunks are still in flight: every staged plane's rows of the chunk are cut
+// into ~1 MiB pieces copied by the whole pool at once.
+sobel5_status drain_stream(sobel5_ctx* ctx, int out_w, int out_h, int chunk, int n_chunks,
+                           void* const stage_dst[7], sobel5_diag* diag_out) {
+    constexpr size_t kPiece = size_t{1} << 20;
+    struct Piece {
+        char* dst;
+        const char* src;
+        size_t n;
+    };
+    std::vector<Piece> pieces;
+    for (int k = 0; k < n_chunks; ++k) {
+        CK(cudaEventSynchronize(ctx->ev_out[k]));
+        const int y0 = k * chunk, y1 = std::min(out_h, y0 + chunk);
+        pieces.clear();
+        for (int i = 0; i < 7; ++i) {
+            if (!stage_dst[i]) continue;
+            const size_t row = static_cast<size_t>(out_w) * kElem[i];
+            const size_t off = static_cast<size_t>(y0) * row, n = static_cast<size_t>(y1 - y0) * row;
+            for (size_t o = 0; o < n; o += kPiece)
+                pieces.push_back({static_cast<char*>(stage_dst[i]) + off + o,
+                                  static_cast<const char*>(ctx->h_stage[i]) + off + o,
+                                  std::min(kPiece, n - o)});
+        }
+        if (pieces.size() == 1) {
+            std::memcpy(pieces[0].dst, pieces[0].src, pieces[0].n);
+        } else if (!pieces.empty()) {
+            ctx->pool.run(static_cast<int>(pieces.size()), [&](int t) {
+                std::memcpy(pieces[t].dst, pieces[t].src, pieces[t].n);
+            });
+        }
+    }
+    CK(cudaStreamSynchronize(ctx->s_d2h));
+    if (diag_out) *diag_out = *ctx->h_diag;
+    return ctx->h_diag->violations ? SOBEL5_PARITY_VIOLATION : SOBEL5_OK;
+}
+
+void planes_array(const sobel5_planes* p, void* out[7]) {
+    out[0] = p->gx; out[1] = p->gy; out[2] = p->gd; out[3] = p->gdt;
+    out[4] = p->g; out[5] = p->g32; out[6] = p->u8;
 }
 
 }  // namespace
@@ -108,9 +398,13 @@ void sobel5_ctx_destroy(sobel5_ctx* ctx) {
         if (s) cudaStreamSynchronize(s);
     for (auto ev : ctx->ev_in) cudaEventDestroy(ev);
     for (auto ev : ctx->ev_comp) cudaEventDestroy(ev);
+    for (auto ev : ctx->ev_out) cudaEventDestroy(ev);
     if (ctx->d_in) cudaFree(ctx->d_in);
     for (void* p : ctx->d_plane)
         if (p) cudaFree(p);
+    for (void* p : ctx->h_stage)
+        if (p) cudaFreeHost(p);
+    if (ctx->h_in_stage) cudaFreeHost(ctx->h_in_stage);
     if (ctx->d_diag) cudaFree(ctx->d_diag);
     if (ctx->d_scratch) cudaFree(ctx->d_scratch);
     if (ctx->h_diag) cudaFreeHost(ctx->h_diag);
@@ -130,84 +424,91 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     // pipeline.hpp:454-456 first
     if (width < 5 || height < 5) return SOBEL5_IMAGE_TOO_SMALL;
     if (!h_in || !taps || !h_out) return SOBEL5_INVALID_ARG;
+    if (ctx->pend.active) return SOBEL5_INVALID_ARG;  // a begin() awaits its finish()
     const int out_w = width - 4, out_h = height - 4;
     if (h_out->pitch != out_w) return SOBEL5_INVALID_ARG;
     CK(cudaSetDevice(ctx->device));
-
-    const int64_t in_pitch = round_up(width, 128);
-    const int64_t dpitch = round_up(out_w, 32);  // elements; 128 B-aligned int rows
-    void* const hp[7] = {h_out->gx, h_out->gy, h_out->gd, h_out->gdt,
-                         h_out->g,  h_out->g32, h_out->u8};
-    CK(ensure(reinterpret_cast<void**>(&ctx->d_in), &ctx->d_in_bytes,
-              static_cast<size_t>(in_pitch) * height));
-    sobel5_planes dp{};
-    dp.pitch = dpitch;
-    void** dslots[7] = {reinterpret_cast<void**>(&dp.gx),  reinterpret_cast<void**>(&dp.gy),
-                        reinterpret_cast<void**>(&dp.gd),  reinterpret_cast<void**>(&dp.gdt),
-                        reinterpret_cast<void**>(&dp.g),   reinterpret_cast<void**>(&dp.g32),
-                        reinterpret_cast<void**>(&dp.u8)};
+    void* hp[7];
+    planes_array(h_out, hp);
+    unsigned mask = 0;
+    void* direct[7] = {};  // pinned destinations: DMA straight into them
+    void* staged[7] = {};  // pageable ones: through pinned staging
     for (int i = 0; i < 7; ++i) {
         if (!hp[i]) continue;
-        CK(ensure(&ctx->d_plane[i], &ctx->d_plane_bytes[i],
-                  static_cast<size_t>(dpitch) * out_h * kElem[i]));
-        *dslots[i] = ctx->d_plane[i];
+        mask |= 1u << i;
+        (is_pinned(hp[i]) ? direct[i] : staged[i]) = hp[i];
     }
+    int chunk = 0, n_chunks = 0;
+    const sobel5_status st =
+        enqueue_stream(ctx, h_in, width, height, taps, prefetch, mask, direct, &chunk, &n_chunks);
+    if (st != SOBEL5_OK) return st;
+    return drain_stream(ctx, out_w, out_h, chunk, n_chunks, staged, diag_out);
+}
 
-    // Row chunks: enough to overlap copies with compute, few enough that
-    // each kernel still fills the GPU.
-    int chunk = std::max(256, (out_h + 7) / 8);
-    chunk = std::min(chunk, out_h);
-    const int n_chunks = (out_h + chunk - 1) / chunk;
-    CK(ensure_events(ctx->ev_in, static_cast<size_t>(n_chunks)));
-    CK(ensure_events(ctx->ev_comp, static_cast<size_t>(n_chunks)));
-    CK(cudaMemsetAsync(ctx->d_diag, 0, sizeof(sobel5_diag), ctx->s_comp));
-
-    int uploaded = 0;  // input rows already enqueued
-    for (int k = 0; k < n_chunks; ++k) {
-        const int y0 = k * chunk, y1 = std::min(out_h, y0 + chunk);
-        const int need = y1 + 4;  // input rows [y0, y1 + 4)
-        CK(cudaMemcpy2DAsync(ctx->d_in + static_cast<int64_t>(uploaded) * in_pitch, in_pitch,
-                             h_in + static_cast<int64_t>(uploaded) * width, width, width,
-                             need - uploaded, cudaMemcpyHostToDevice, ctx->s_h2d));
-        uploaded = need;
-        CK(cudaEventRecord(ctx->ev_in[k], ctx->s_h2d));
-        CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_in[k], 0));
-        sobel5_planes sub = dp;
-        const int64_t off = static_cast<int64_t>(y0) * dpitch;
-        if (sub.gx) sub.gx += off;
-        if (sub.gy) sub.gy += off;
-        if (sub.gd) sub.gd += off;
-        if (sub.gdt) sub.gdt += off;
-        if (sub.g) sub.g += off;
-        if (sub.g32) sub.g32 += off;
-        if (sub.u8) sub.u8 += off;
-        const sobel5_status st =
-            sobel5_launch(ctx->d_in + static_cast<int64_t>(y0) * in_pitch, in_pitch, width,
-                          y1 - y0 + 4, taps, prefetch, &sub, ctx->d_diag, ctx->s_comp);
-        if (st != SOBEL5_OK) {
-            ctx->last_error = cudaGetErrorString(cudaGetLastError());
-            return st;
-        }
-        CK(cudaEventRecord(ctx->ev_comp[k], ctx->s_comp));
-        CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_comp[k], 0));
-        for (int i = 0; i < 7; ++i) {
-            if (!hp[i]) continue;
-            const size_t es = kElem[i];
-            CK(cudaMemcpy2DAsync(static_cast<char*>(hp[i]) + static_cast<size_t>(y0) * out_w * es,
-                                 static_cast<size_t>(out_w) * es,
-                                 static_cast<char*>(ctx->d_plane[i]) +
-                                     static_cast<size_t>(y0) * dpitch * es,
-                                 static_cast<size_t>(dpitch) * es, static_cast<size_t>(out_w) * es,
-                                 static_cast<size_t>(y1 - y0), cudaMemcpyDeviceToHost,
-                                 ctx->s_d2h));
-        }
+sobel5_status sobel5_run_host_begin(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
+                                    const sobel5_taps* taps, int prefetch, unsigned plane_mask) {
+    if (!ctx) return SOBEL5_INVALID_ARG;
+    if (width < 5 || height < 5) return SOBEL5_IMAGE_TOO_SMALL;
+    if (!h_in || !taps || plane_mask == 0 || plane_mask >= (1u << 7) || ctx->pend.active)
+        return SOBEL5_INVALID_ARG;
+    CK(cudaSetDevice(ctx->device));
+    void* none[7] = {};
+    int chunk = 0, n_chunks = 0;
+    const sobel5_status st = enqueue_stream(ctx, h_in, width, height, taps, prefetch, plane_mask,
+                                            none, &chunk, &n_chunks);
+    if (st != SOBEL5_OK) {
+        // drain whatever was enqueued so the context stays usable
+        cudaStreamSynchronize(ctx->s_h2d);
+        cudaStreamSynchronize(ctx->s_comp);
+        cudaStreamSynchronize(ctx->s_d2h);
+        return st;
     }
-    CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_comp[n_chunks - 1], 0));
-    CK(cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(sobel5_diag), cudaMemcpyDeviceToHost,
-                       ctx->s_d2h));
-    CK(cudaStreamSynchronize(ctx->s_d2h));
-    if (diag_out) *diag_out = *ctx->h_diag;
-    return ctx->h_diag->violations ? SOBEL5_PARITY_VIOLATION : SOBEL5_OK;
+    ctx->pend.active = true;
+    ctx->pend.out_w = width - 4;
+    ctx->pend.out_h = height - 4;
+    ctx->pend.chunk = chunk;
+    ctx->pend.n_chunks = n_chunks;
+    ctx->pend.mask = plane_mask;
+    return SOBEL5_OK;
+}
+
+sobel5_status sobel5_run_host_finish(sobel5_ctx* ctx, const sobel5_planes* h_out,
+                                     sobel5_diag* diag_out) {
+    if (!ctx || !ctx->pend.active) return SOBEL5_INVALID_ARG;
+    CK(cudaSetDevice(ctx->device));
+    const auto pend = ctx->pend;
+    void* hp[7] = {};
+    bool ok = !h_out || h_out->pitch == pend.out_w;
+    if (ok && h_out) {
+        planes_array(h_out, hp);
+        for (int i = 0; i < 7; ++i) ok = ok && ((hp[i] != nullptr) == (((pend.mask >> i) & 1u) != 0));
+    }
+    if (!ok) {  // still complete the pending work, then report the bad argument
+        void* none[7] = {};
+        drain_stream(ctx, pend.out_w, pend.out_h, pend.chunk, pend.n_chunks, none, nullptr);
+        ctx->pend.active = false;
+        return SOBEL5_INVALID_ARG;
+    }
+    const sobel5_status st =
+        drain_stream(ctx, pend.out_w, pend.out_h, pend.chunk, pend.n_chunks, hp, diag_out);
+    ctx->pend.active = false;
+    return st;
+}
+
+sobel5_status sobel5_run_host_chunk(sobel5_ctx* ctx, int chunk, int* y0, int* y1) {
+    if (!ctx || !ctx->pend.active || chunk < 0 || chunk >= ctx->pend.n_chunks || !y0 || !y1)
+        return SOBEL5_INVALID_ARG;
+    const cudaError_t e = cudaEventSynchronize(ctx->ev_out[chunk]);
+    if (e != cudaSuccess) return SOBEL5_CUDA_ERROR;  // (last_error is not thread-safe)
+    *y0 = chunk * ctx->pend.chunk;
+    *y1 = std::min(ctx->pend.out_h, *y0 + ctx->pend.chunk);
+    return SOBEL5_OK;
+}
+
+const void* sobel5_run_host_staging(const sobel5_ctx* ctx, int plane) {
+    if (!ctx || !ctx->pend.active || plane < 0 || plane >= 7 || !((ctx->pend.mask >> plane) & 1u))
+        return nullptr;
+    return ctx->h_stage[plane];
 }
 
 sobel5_status sobel5_detect_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,

@@ -179,8 +179,12 @@ __device__ __forceinline__ uint32_t u8_normalize_s(uint32_t S, const uint32_t* t
 // OUTS = output-set bits; kOutMinMax adds the per-frame min/max of g
 // (normalize pass 1), kOutNorm makes the u8 plane the normalize export
 // (pass 2) instead of clamp_abs.
+#ifndef SOBEL5_U8_MIN_CTAS
+#define SOBEL5_U8_MIN_CTAS kMinCtasPerSm
+#endif
 template <int PF, int GEOM, int OUTS, bool RTAPS = false>
-__global__ void __launch_bounds__(kCtaThreads, kMinCtasPerSm)
+__global__ void __launch_bounds__(kCtaThreads,
+                                  (OUTS == kOutU8 && !RTAPS) ? SOBEL5_U8_MIN_CTAS : kMinCtasPerSm)
     sobel5_packed_default_kernel(const __grid_constant__ KernelParams p) {
     constexpr bool SEG = GEOM == kGeomSeg;
     constexpr bool PAD = GEOM == kGeomPad;

@@ -15,19 +15,26 @@ for i in range(6):
     api.synth_random_device(d, pitch, w, h, 1 + i)
     ins.append(d)
 out, op = api.alloc_planes(w - 4, h - 4, planes_names)
+out3, op3 = api.alloc_planes(w - 2, h - 2, planes_names)
 bands = [int(x) for x in os.environ.get("BANDS", "0").split(",")]
 pfs = [int(x) for x in os.environ.get("OCCS", "0").split(",")]  # CTAs per SM (0 = occupancy)
 res = {}
 for band, pf in itertools.product(bands, pfs):
     os.environ["SOBEL5_BAND"] = str(band)
     os.environ["SOBEL5_CTAS_PER_SM"] = str(pf)
+    k3 = os.environ.get("SOBEL3", "0") == "1"  # the 3x3 operator instead
+    def go(i):
+        if k3:
+            api.launch3(ins[i % 6], pitch, w, h, 1, False, out3, op3)
+        else:
+            api.launch(ins[i % 6], pitch, w, h, taps, 1, out, op)
     for i in range(5):
-        api.launch(ins[i % 6], pitch, w, h, taps, 1, out, op)
+        go(i)
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     torch.cuda.synchronize(); e0.record()
     N = 60
     for i in range(N):
-        api.launch(ins[i % 6], pitch, w, h, taps, 1, out, op)
+        go(i)
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / N
     b = w * h + (w - 4) * (h - 4) * outb
