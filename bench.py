@@ -446,6 +446,27 @@ def main():
                        "overlap on 3 streams"}
         ctx.close()
 
+    # the drop-in C++ API end to end (tools/cpp_e2e.cpp): sobel5::run_stream
+    # returning freshly allocated StreamResult planes, as a reference user calls it
+    e2e_cpp = None
+    exe = os.path.join(ROOT, "build", "cpp_e2e")
+    if rank == 0 and not a.no_e2e and frames == 1 and a.workload != "32k-bands" \
+            and os.path.exists(exe):
+        import subprocess
+        try:
+            r = subprocess.run([exe, str(w), str(h), "10"], capture_output=True, text=True,
+                               timeout=300)
+            d = json.loads(r.stdout.strip().splitlines()[-1])
+            e2e_cpp = {"value": d["run_stream_gpx_s"], "unit": UNIT,
+                       "ms_per_step": d["run_stream_ms"], "h2d_bytes_per_step": w * h,
+                       "d2h_bytes_per_step": d["d2h_bytes"],
+                       "path": "sobel5::run_stream (C++ drop-in, include/sobel5_b200), fresh "
+                               "StreamResult planes per call",
+                       "parts_ms": {k: d[k] for k in ("alloc_planes_ms", "run_host_pageable_ms",
+                                                      "run_host_pinned_ms")}}
+        except Exception as ex:  # informative only
+            e2e_cpp = {"error": str(ex)[:200]}
+
     cpu = None
     if rank == 0 and not a.no_cpu_baseline:
         cpu = cpu_reference(w, h, frames, a.cpu_seconds)
@@ -477,6 +498,7 @@ def main():
             "clocks": clocks.summary(),
             "variants": variants,
             "e2e": e2e,
+            "e2e_cpp_api": e2e_cpp,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
