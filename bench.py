@@ -395,14 +395,16 @@ def main():
         variant("sr_pad", CONTRACT_PLANES["sr"], w, h, OUT_BYTES["sr"],
                 lambda d, vo, vp: api.launch_ex(d, pitch, w, h, taps, 1, True, vo, vp,
                                                 stream=s_ptr))
-        # non-default FilterParams: (1,1,1,1) fits the int16 bound (packed
-        # kernel, runtime taps), (2,3,5,7) does not (generic kernel)
-        for prm in ((1, 1, 1, 1), (2, 3, 5, 7)):
+        # non-default FilterParams: (1,1,1,1) fits the int16 lanes (packed
+        # kernel, runtime taps), (2,3,5,7) the FP32 lanes (f32x2 kernel),
+        # (1,32768,1,1) neither (generic 32-bit kernel)
+        for prm in ((1, 1, 1, 1), (2, 3, 5, 7), (1, 32768, 1, 1)):
             tp = api.make_stream_taps(api.FilterParams(*prm))
-            variant("sr_params_" + "_".join(map(str, prm)), CONTRACT_PLANES["sr"], ow, oh,
-                    OUT_BYTES["sr"],
+            name = "sr_params_" + "_".join(map(str, prm))
+            variant(name, CONTRACT_PLANES["sr"], ow, oh, OUT_BYTES["sr"],
                     lambda d, vo, vp, tp=tp: api.launch(d, pitch, w, h, tp, 1, vo, vp,
                                                         stream=s_ptr))
+            variants[name]["kernel"] = api.kernel_for(tp)
         # 3x3 operator: Stream3Result gx+gy (int32) + g (f64)
         variant("sobel3_sr", ("gx", "gy", "g"), w - 2, h - 2, 16,
                 lambda d, vo, vp: api.launch3(d, pitch, w, h, 1, False, vo, vp, stream=s_ptr))

@@ -233,6 +233,13 @@ sobel5_status sobel5_ipc_export(const void* d_ptr, sobel5_ipc_handle* out);
 sobel5_status sobel5_ipc_import(const sobel5_ipc_handle* h, const void** d_ptr);
 sobel5_status sobel5_ipc_release(const void* d_ptr);
 
+/* Which kernel family serves these taps: 0 packed int16 lanes with the
+ * default (1, 2, 6, 4) algebra compiled in, 1 packed int16 lanes with
+ * runtime taps (every response < 2^15), 2 packed FP32 with runtime taps
+ * (every partial sum < 2^22), 3 generic 32-bit wrapping kernel (any taps);
+ * -1 for NULL.  Host-only, no device needed. */
+int sobel5_kernel_for_taps(const sobel5_taps* taps);
+
 /* ---- diagnostics ----------------------------------------------------------
  * Device self-check of the epilogue arithmetic over every integer S in
  * [lo, hi): which = 0 compares the kernels' double sqrt with IEEE

@@ -78,7 +78,7 @@ EXPORTS = (
     "sobel5_detect_scratch_bytes", "sobel5_quantize_plane", "sobel5_detect_host",
     "sobel3_launch", "sobel3_detect", "sobel3_plan_counters", "sobel3_run_host",
     "sobel5_quantize_host", "sobel5_run_host_begin", "sobel5_run_host_finish",
-    "sobel5_run_host_chunk", "sobel5_run_host_staging",
+    "sobel5_run_host_chunk", "sobel5_run_host_staging", "sobel5_kernel_for_taps",
 )
 
 _lib = None
@@ -132,6 +132,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.sobel5_run_host_begin.restype = i32
     L.sobel5_run_host_finish.argtypes = [vp, C.POINTER(Planes), C.POINTER(Diag)]
     L.sobel5_run_host_finish.restype = i32
+    L.sobel5_kernel_for_taps.argtypes = [C.POINTER(Taps)]
+    L.sobel5_kernel_for_taps.restype = i32
     L.sobel5_run_host_chunk.argtypes = [vp, i32, C.POINTER(i32), C.POINTER(i32)]
     L.sobel5_run_host_chunk.restype = i32
     L.sobel5_run_host_staging.argtypes = [vp, i32]

@@ -133,6 +133,14 @@ def materialize(p: FilterParams, direction: int) -> np.ndarray:
     return np.array([[int(e) for e in row] for row in k], dtype=np.int32)
 
 
+KERNELS = ("packed_default", "packed_runtime_taps", "f32x2_runtime_taps", "generic")
+
+
+def kernel_for(taps: Taps) -> str:
+    """Kernel family the C ABI selects for these taps (sobel5_kernel_for_taps)."""
+    return KERNELS[_abi.load().sobel5_kernel_for_taps(C.byref(taps))]
+
+
 def make_stream_taps(p: FilterParams = FilterParams()) -> Taps:
     """pipeline.hpp:75-107 (validation, then the C ABI builds the taps)."""
     validate_params(p)

@@ -98,6 +98,29 @@ bool taps_fit_packed(const sobel5_taps& t) {
            response_bound(km) <= lim;
 }
 
+// The packed-FP32 kernel (sobel5_f32x2.cuh) is exact for taps whose every
+// partial sum stays an integer below 2^24 and whose final gx, gy, P, M and
+// P +- M fit the 1.5 * 2^23 conversion (< 2^22): bounded by 255 times the
+// absolute tap sums of each stage.  Every tap must itself be exact in FP32.
+bool taps_fit_f32(const sobel5_taps& t) {
+    auto abs_sum = [](const int32_t* v) {
+        int64_t s = 0;
+        for (int i = 0; i < 5; ++i) s += v[i] < 0 ? -int64_t{v[i]} : int64_t{v[i]};
+        return s;
+    };
+    const int32_t* all[8] = {t.f, t.h, t.k0, t.k1, t.gx_v, t.gy_v, t.gdm_f, t.gdm_d};
+    for (const int32_t* v : all)
+        for (int i = 0; i < 5; ++i)
+            if (v[i] >= (1 << 24) || v[i] <= -(1 << 24)) return false;
+    const int64_t sf = abs_sum(t.f), sh = abs_sum(t.h), s0 = abs_sum(t.k0), s1 = abs_sum(t.k1);
+    const int64_t bx = 255 * abs_sum(t.gx_v) * sf;
+    const int64_t by = 255 * abs_sum(t.gy_v) * sh;
+    const int64_t bm = 255 * (abs_sum(t.gdm_f) * sf + abs_sum(t.gdm_d));
+    const int64_t bp = 255 * 2 * (s0 + s1);
+    constexpr int64_t lim = int64_t{1} << 22;
+    return bx < lim && by < lim && bp + bm < lim;
+}
+
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
     return v && *v ? std::atoi(v) : dflt;
@@ -139,6 +162,10 @@ void fill_taps(KernelParams& kp, const sobel5_taps& t) {
     std::memcpy(kp.gy_v, t.gy_v, sizeof kp.gy_v);
     std::memcpy(kp.gdm_f, t.gdm_f, sizeof kp.gdm_f);
     std::memcpy(kp.gdm_d, t.gdm_d, sizeof kp.gdm_d);
+    const int32_t* src[8] = {t.f, t.h, t.k0, t.k1, t.gx_v, t.gy_v, t.gdm_f, t.gdm_d};
+    for (int q = 0; q < 8; ++q)
+        for (int i = 0; i < 5; ++i)
+            kp.tf[q][i] = static_cast<float>(q == 7 ? -static_cast<int64_t>(src[q][i]) : src[q][i]);
 }
 
 bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
@@ -165,6 +192,19 @@ bool taps_fit_packed_p(const KernelParams& kp) {
     return taps_fit_packed(t);
 }
 
+bool taps_fit_f32_p(const KernelParams& kp) {
+    sobel5_taps t{};
+    std::memcpy(t.f, kp.f, sizeof t.f);
+    std::memcpy(t.h, kp.h, sizeof t.h);
+    std::memcpy(t.k0, kp.k0, sizeof t.k0);
+    std::memcpy(t.k1, kp.k1, sizeof t.k1);
+    std::memcpy(t.gx_v, kp.gx_v, sizeof t.gx_v);
+    std::memcpy(t.gy_v, kp.gy_v, sizeof t.gy_v);
+    std::memcpy(t.gdm_f, kp.gdm_f, sizeof t.gdm_f);
+    std::memcpy(t.gdm_d, kp.gdm_d, sizeof t.gdm_d);
+    return taps_fit_f32(t);
+}
+
 cudaError_t dispatch(const KernelParams& kp, dim3 grid, int prefetch, bool dflt, MagMode mag,
                      cudaStream_t s) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -181,6 +221,10 @@ cudaError_t dispatch(const KernelParams& kp, dim3 grid, int prefetch, bool dflt,
         const bool seg = kp.top_rows > 0 || kp.bot != nullptr;
         return seg ? launch_packed_rt_seg(kp, grid, prefetch, s)
                    : launch_packed_rt_plain(kp, grid, prefetch, s);
+    }
+    if (env_int("SOBEL5_GENERIC", 0) == 0 && taps_fit_f32_p(kp)) {
+        // taps beyond the int16 lanes but within 2^22: packed FP32
+        return launch_f32(kp, grid, prefetch, mag, s);
     }
     return launch_generic(kp, grid, prefetch, dflt, mag, s);
 }
@@ -470,6 +514,15 @@ sobel5_status sobel5_launch_band(const uint8_t* d_top, const uint8_t* d_in, cons
                                  const sobel5_planes* d_out, sobel5_diag* d_diag, void* stream) {
     return launch_common(d_top, d_in, d_bot, in_pitch, 0, width, band_rows, 1, taps, prefetch,
                          d_out, 0, d_diag, stream, LaunchExtra{});
+}
+
+int sobel5_kernel_for_taps(const sobel5_taps* t) {
+    if (!t) return -1;
+    if (env_int("SOBEL5_GENERIC", 0) != 0) return 3;
+    if (taps_are_default(*t)) return 0;
+    if (taps_fit_packed(*t)) return 1;
+    if (taps_fit_f32(*t)) return 2;
+    return 3;
 }
 
 sobel5_status sobel5_selftest(int which, uint32_t lo, uint32_t hi, uint64_t* d_count,

@@ -22,6 +22,9 @@ cudaError_t launch_packed_rt_plain(const KernelParams& kp, dim3 grid, int pf, cu
 cudaError_t launch_packed_rt_seg(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
 cudaError_t launch_packed_rt_pad(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
 
+// Packed-FP32 kernel with runtime taps (sobel5_f32x2.cuh), every geometry.
+cudaError_t launch_f32(const KernelParams& kp, dim3 grid, int pf, MagMode mag, cudaStream_t s);
+
 // Generic-taps kernel (sobel5_stream.cuh).
 cudaError_t launch_generic(const KernelParams& kp, dim3 grid, int pf, bool default_taps,
                            MagMode mag, cudaStream_t s);

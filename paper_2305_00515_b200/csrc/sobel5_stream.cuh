@@ -46,6 +46,7 @@ constexpr int kMinCtasPerSm = 16 / kCtaWarps;  // 16 resident warps per SM (<= 1
 enum MagMode : int {
     kMagU32 = 0,  // exact integer sum of squares fits uint32 (host-proven bound)
     kMagF64 = 1,  // general: the reference's ((x*x + y*y) + d*d) + t*t in double
+    kMagU64 = 2,  // exact integer sum of squares < 2^53 in uint64 (then double(S) is exact)
 };
 
 struct KernelParams {
@@ -82,6 +83,9 @@ struct KernelParams {
     uint32_t* s32;               // exact integer g^2 (normalize pass 1 of the detect path)
     // taps (kernel parameter space -> constant-bank operands)
     int32_t f[5], h[5], k0[5], k1[5], gx_v[5], gy_v[5], gdm_f[5], gdm_d[5];
+    // the same taps as floats for the packed-FP32 kernel (sobel5_f32x2.cuh):
+    // f, h, k0, k1, gx_v, gy_v, gdm_f, -gdm_d
+    float tf[8][5];
 };
 
 // Compile-time default taps, (a, b, m, n) = (1, 2, 6, 4) (make_stream_taps,
