@@ -180,3 +180,21 @@ def test_no_silent_cpu_fallback_without_gpu(lib):
     pl = Planes(gx=oaddr, pitch=32)
     st = lib.sobel5_launch(addr, 64, 32, 16, C.byref(t), 1, C.byref(pl), None, None)
     assert st != OK
+
+
+def test_kernel_selection_by_taps_bound():
+    """sobel5_kernel_for_taps (host-only): default taps -> packed default
+    algebra; responses < 2^15 -> packed int16 lanes with runtime taps; partial
+    sums < 2^22 -> packed FP32; anything else -> generic 32-bit kernel."""
+    from paper_2305_00515_b200 import api
+    cases = {(1, 2, 6, 4): "packed_default", (1, 1, 1, 1): "packed_runtime_taps",
+             (2, 3, 5, 1): "packed_runtime_taps", (2, 3, 5, 7): "f32x2_runtime_taps",
+             (2, 5, 11, 13): "f32x2_runtime_taps", (1, 32768, 1, 1): "generic",
+             (4, 16, 64, 64): "generic"}
+    for prm, want in cases.items():
+        assert api.kernel_for(api.make_stream_taps(api.FilterParams(*prm))) == want, prm
+    t = api.make_stream_taps()
+    t.k0[0] += 2  # fault injection keeps the int16 bound
+    assert api.kernel_for(t) == "packed_runtime_taps"
+    t.k1[2] = 1 << 24  # a tap not exact in FP32 is never given to the f32 kernel
+    assert api.kernel_for(t) == "generic"
