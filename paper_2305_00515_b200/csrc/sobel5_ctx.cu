@@ -220,28 +220,61 @@ void par_copy(sobel5_ctx* ctx, void* dst, const void* src, size_t n) {
     });
 }
 
+// A pageable input is first copied into pinned staging (in parallel) so the
+// uploads that follow are true asynchronous DMA; *src is what to upload.
+sobel5_status stage_input(sobel5_ctx* ctx, const uint8_t* h_in, size_t n, const uint8_t** src) {
+    *src = h_in;
+    if (is_pinned(h_in)) return SOBEL5_OK;
+    CK(ensure_host(&ctx->h_in_stage, &ctx->h_in_stage_bytes, n));
+    par_copy(ctx, ctx->h_in_stage, h_in, n);
+    *src = static_cast<const uint8_t*>(ctx->h_in_stage);
+    return SOBEL5_OK;
+}
+
+// Enqueues the download of `rows` rows of plane slot i (device pitch dpitch
+// elements) to tightly packed host memory: straight into a pinned dst, or
+// into the pinned staging h_stage[i], recorded in *staged for
+// finish_staged() once the stream has synchronised.
+sobel5_status download_plane(sobel5_ctx* ctx, int i, void* dst, const void* d_src, int out_w,
+                             int rows, int64_t dpitch, cudaStream_t s, void* staged[7]) {
+    const size_t es = kElem[i], row = static_cast<size_t>(out_w) * es;
+    void* to = dst;
+    if (!is_pinned(dst)) {
+        CK(ensure_host(&ctx->h_stage[i], &ctx->h_stage_bytes[i], row * rows));
+        to = ctx->h_stage[i];
+        staged[i] = dst;
+    }
+    CK(cudaMemcpy2DAsync(to, row, d_src, static_cast<size_t>(dpitch) * es, row,
+                         static_cast<size_t>(rows), cudaMemcpyDeviceToHost, s));
+    return SOBEL5_OK;
+}
+
+void finish_staged(sobel5_ctx* ctx, void* const staged[7], int out_w, int rows) {
+    for (int i = 0; i < 7; ++i)
+        if (staged[i])
+            par_copy(ctx, staged[i], ctx->h_stage[i], static_cast<size_t>(out_w) * kElem[i] * rows);
+}
+
 // Enqueues the chunked H2D -> kernel -> D2H pipeline of run_stream on the
 // context's streams.  dst[i] is the host destination of plane i (tightly
 // packed, out_w pitch), or nullptr with bit i of `mask` set to land the
 // plane in the pinned staging buffer h_stage[i].  ev_out[k] marks chunk k's
 // downloads.
+// (op = 5: the 4-direction 5x5 operator, sobel5_launch; op = 3: the 3x3
+// two-direction one, sobel3_launch, taps unused.)
 sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
                              const sobel5_taps* taps, int prefetch, unsigned mask,
-                             void* const dst[7], int* chunk_out, int* n_chunks_out) {
-    const int out_w = width - 4, out_h = height - 4;
+                             void* const dst[7], int* chunk_out, int* n_chunks_out, int op = 5) {
+    const int R = op == 3 ? 1 : 2;  // operator radius
+    const int out_w = width - 2 * R, out_h = height - 2 * R;
     const int64_t in_pitch = round_up(width, 128);
     const int64_t dpitch = round_up(out_w, 32);  // elements; 128 B-aligned int rows
     CK(ensure(reinterpret_cast<void**>(&ctx->d_in), &ctx->d_in_bytes,
               static_cast<size_t>(in_pitch) * height));
-    // a pageable input is first copied into pinned staging (in parallel) so
-    // the uploads below are true async DMA
-    const uint8_t* src_in = h_in;
-    if (!is_pinned(h_in)) {
-        const size_t n = static_cast<size_t>(width) * height;
-        CK(ensure_host(&ctx->h_in_stage, &ctx->h_in_stage_bytes, n));
-        par_copy(ctx, ctx->h_in_stage, h_in, n);
-        src_in = static_cast<const uint8_t*>(ctx->h_in_stage);
-    }
+    const uint8_t* src_in = nullptr;
+    if (const sobel5_status st = stage_input(ctx, h_in, static_cast<size_t>(width) * height, &src_in);
+        st != SOBEL5_OK)
+        return st;
     sobel5_planes dp{};
     dp.pitch = dpitch;
     void** dslots[7] = {reinterpret_cast<void**>(&dp.gx),  reinterpret_cast<void**>(&dp.gy),
@@ -276,7 +309,7 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
     int uploaded = 0;  // input rows already enqueued
     for (int k = 0; k < n_chunks; ++k) {
         const int y0 = k * chunk, y1 = std::min(out_h, y0 + chunk);
-        const int need = y1 + 4;  // input rows [y0, y1 + 4)
+        const int need = y1 + 2 * R;  // input rows [y0, y1 + 2R)
         CK(cudaMemcpy2DAsync(ctx->d_in + static_cast<int64_t>(uploaded) * in_pitch, in_pitch,
                              src_in + static_cast<int64_t>(uploaded) * width, width, width,
                              need - uploaded, cudaMemcpyHostToDevice, ctx->s_h2d));
@@ -292,9 +325,12 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
         if (sub.g) sub.g += off;
         if (sub.g32) sub.g32 += off;
         if (sub.u8) sub.u8 += off;
+        const uint8_t* d_rows = ctx->d_in + static_cast<int64_t>(y0) * in_pitch;
         const sobel5_status st =
-            sobel5_launch(ctx->d_in + static_cast<int64_t>(y0) * in_pitch, in_pitch, width,
-                          y1 - y0 + 4, taps, prefetch, &sub, ctx->d_diag, ctx->s_comp);
+            op == 3 ? sobel3_launch(d_rows, in_pitch, 0, width, y1 - y0 + 2, 1, prefetch, 0, &sub, 0,
+                                    ctx->s_comp)
+                    : sobel5_launch(d_rows, in_pitch, width, y1 - y0 + 4, taps, prefetch, &sub,
+                                    ctx->d_diag, ctx->s_comp);
         if (st != SOBEL5_OK) {
             ctx->last_error = cudaGetErrorString(cudaGetLastError());
             return st;
@@ -550,7 +586,11 @@ sobel5_status sobel5_detect_host(sobel5_ctx* ctx, const uint8_t* h_in, int width
     CK(ensure(&ctx->d_scratch, &ctx->d_scratch_bytes,
               sobel5_detect_scratch_bytes(out_h, dpitch, 0, 1)));
     CK(cudaMemsetAsync(ctx->d_diag, 0, sizeof(sobel5_diag), ctx->s_comp));
-    CK(cudaMemcpy2DAsync(ctx->d_in, in_pitch, h_in, width, width, height, cudaMemcpyHostToDevice,
+    const uint8_t* src_in = nullptr;
+    if (const sobel5_status st = stage_input(ctx, h_in, static_cast<size_t>(width) * height, &src_in);
+        st != SOBEL5_OK)
+        return st;
+    CK(cudaMemcpy2DAsync(ctx->d_in, in_pitch, src_in, width, width, height, cudaMemcpyHostToDevice,
                          ctx->s_comp));
     const sobel5_status st = sobel5_detect(ctx->d_in, in_pitch, 0, width, height, 1, taps,
                                            prefetch, pad, save_mode, &dp, 0, ctx->d_scratch,
@@ -559,16 +599,18 @@ sobel5_status sobel5_detect_host(sobel5_ctx* ctx, const uint8_t* h_in, int width
         ctx->last_error = cudaGetErrorString(cudaGetLastError());
         return st;
     }
+    void* staged[7] = {};
     for (int i = 0; i < 7; ++i) {
         if (!hp[i]) continue;
-        const size_t es = kElem[i];
-        CK(cudaMemcpy2DAsync(hp[i], static_cast<size_t>(out_w) * es, ctx->d_plane[i],
-                             static_cast<size_t>(dpitch) * es, static_cast<size_t>(out_w) * es,
-                             static_cast<size_t>(out_h), cudaMemcpyDeviceToHost, ctx->s_comp));
+        if (const sobel5_status ds = download_plane(ctx, i, hp[i], ctx->d_plane[i], out_w, out_h,
+                                                    dpitch, ctx->s_comp, staged);
+            ds != SOBEL5_OK)
+            return ds;
     }
     CK(cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(sobel5_diag), cudaMemcpyDeviceToHost,
                        ctx->s_comp));
     CK(cudaStreamSynchronize(ctx->s_comp));
+    finish_staged(ctx, staged, out_w, out_h);
     if (diag_out) *diag_out = *ctx->h_diag;
     return ctx->h_diag->violations ? SOBEL5_PARITY_VIOLATION : SOBEL5_OK;
 }
@@ -578,72 +620,27 @@ sobel5_status sobel3_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     if (!ctx) return SOBEL5_INVALID_ARG;
     if (width < 3 || height < 3) return SOBEL5_IMAGE_TOO_SMALL;  // pipeline.hpp:553-556
     if (!h_in || !h_out || h_out->gd || h_out->gdt) return SOBEL5_INVALID_ARG;
+    if (ctx->pend.active) return SOBEL5_INVALID_ARG;
     const int out_w = width - 2, out_h = height - 2;
     if (h_out->pitch != out_w) return SOBEL5_INVALID_ARG;
     CK(cudaSetDevice(ctx->device));
-    const int64_t in_pitch = round_up(width, 128);
-    const int64_t dpitch = round_up(out_w, 32);
-    CK(ensure(reinterpret_cast<void**>(&ctx->d_in), &ctx->d_in_bytes,
-              static_cast<size_t>(in_pitch) * height));
-    sobel5_planes dp{};
-    dp.pitch = dpitch;
-    void* const hp[7] = {h_out->gx, h_out->gy, nullptr, nullptr, h_out->g, h_out->g32, h_out->u8};
-    void** dslots[7] = {reinterpret_cast<void**>(&dp.gx),  reinterpret_cast<void**>(&dp.gy),
-                        reinterpret_cast<void**>(&dp.gd),  reinterpret_cast<void**>(&dp.gdt),
-                        reinterpret_cast<void**>(&dp.g),   reinterpret_cast<void**>(&dp.g32),
-                        reinterpret_cast<void**>(&dp.u8)};
+    // the same chunked upload / kernel / download pipeline as sobel5_run_host
+    void* hp[7];
+    planes_array(h_out, hp);
+    unsigned mask = 0;
+    void* direct[7] = {};
+    void* staged[7] = {};
     for (int i = 0; i < 7; ++i) {
         if (!hp[i]) continue;
-        CK(ensure(&ctx->d_plane[i], &ctx->d_plane_bytes[i],
-                  static_cast<size_t>(dpitch) * out_h * kElem[i]));
-        *dslots[i] = ctx->d_plane[i];
+        mask |= 1u << i;
+        (is_pinned(hp[i]) ? direct[i] : staged[i]) = hp[i];
     }
-    // row chunks: upload / kernel / download overlap as in sobel5_run_host
-    int chunk = std::max(256, (out_h + 7) / 8);
-    chunk = std::min(chunk, out_h);
-    const int n_chunks = (out_h + chunk - 1) / chunk;
-    CK(ensure_events(ctx->ev_in, static_cast<size_t>(n_chunks)));
-    CK(ensure_events(ctx->ev_comp, static_cast<size_t>(n_chunks)));
-    int uploaded = 0;
-    for (int k = 0; k < n_chunks; ++k) {
-        const int y0 = k * chunk, y1 = std::min(out_h, y0 + chunk);
-        const int need = y1 + 2;
-        CK(cudaMemcpy2DAsync(ctx->d_in + static_cast<int64_t>(uploaded) * in_pitch, in_pitch,
-                             h_in + static_cast<int64_t>(uploaded) * width, width, width,
-                             need - uploaded, cudaMemcpyHostToDevice, ctx->s_h2d));
-        uploaded = need;
-        CK(cudaEventRecord(ctx->ev_in[k], ctx->s_h2d));
-        CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_in[k], 0));
-        sobel5_planes sub = dp;
-        const int64_t off = static_cast<int64_t>(y0) * dpitch;
-        if (sub.gx) sub.gx += off;
-        if (sub.gy) sub.gy += off;
-        if (sub.g) sub.g += off;
-        if (sub.g32) sub.g32 += off;
-        if (sub.u8) sub.u8 += off;
-        const sobel5_status st =
-            sobel3_launch(ctx->d_in + static_cast<int64_t>(y0) * in_pitch, in_pitch, 0, width,
-                          y1 - y0 + 2, 1, prefetch, 0, &sub, 0, ctx->s_comp);
-        if (st != SOBEL5_OK) {
-            ctx->last_error = cudaGetErrorString(cudaGetLastError());
-            return st;
-        }
-        CK(cudaEventRecord(ctx->ev_comp[k], ctx->s_comp));
-        CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_comp[k], 0));
-        for (int i = 0; i < 7; ++i) {
-            if (!hp[i]) continue;
-            const size_t es = kElem[i];
-            CK(cudaMemcpy2DAsync(static_cast<char*>(hp[i]) + static_cast<size_t>(y0) * out_w * es,
-                                 static_cast<size_t>(out_w) * es,
-                                 static_cast<char*>(ctx->d_plane[i]) +
-                                     static_cast<size_t>(y0) * dpitch * es,
-                                 static_cast<size_t>(dpitch) * es, static_cast<size_t>(out_w) * es,
-                                 static_cast<size_t>(y1 - y0), cudaMemcpyDeviceToHost,
-                                 ctx->s_d2h));
-        }
-    }
-    CK(cudaStreamSynchronize(ctx->s_d2h));
-    return SOBEL5_OK;
+    if (!mask) return SOBEL5_OK;
+    int chunk = 0, n_chunks = 0;
+    const sobel5_status st = enqueue_stream(ctx, h_in, width, height, nullptr, prefetch, mask,
+                                            direct, &chunk, &n_chunks, 3);
+    if (st != SOBEL5_OK) return st;
+    return drain_stream(ctx, out_w, out_h, chunk, n_chunks, staged, nullptr);
 }
 
 sobel5_status sobel5_quantize_host(sobel5_ctx* ctx, const void* h_plane, int kind, int width,
@@ -658,14 +655,23 @@ sobel5_status sobel5_quantize_host(sobel5_ctx* ctx, const void* h_plane, int kin
     CK(ensure(&ctx->d_plane[4], &ctx->d_plane_bytes[4], n * 8));
     CK(ensure(&ctx->d_plane[6], &ctx->d_plane_bytes[6], n));
     CK(ensure(&ctx->d_scratch, &ctx->d_scratch_bytes, sobel5_detect_scratch_bytes(0, 0, 0, 1)));
-    CK(cudaMemcpyAsync(ctx->d_plane[4], h_plane, n * es, cudaMemcpyHostToDevice, ctx->s_comp));
+    const uint8_t* src = nullptr;
+    if (const sobel5_status ss = stage_input(ctx, static_cast<const uint8_t*>(h_plane), n * es, &src);
+        ss != SOBEL5_OK)
+        return ss;
+    CK(cudaMemcpyAsync(ctx->d_plane[4], src, n * es, cudaMemcpyHostToDevice, ctx->s_comp));
     const sobel5_status st =
         sobel5_quantize_plane(ctx->d_plane[4], kind, width, width, height, save_mode,
                               static_cast<uint8_t*>(ctx->d_plane[6]), width, ctx->d_scratch,
                               ctx->s_comp);
     if (st != SOBEL5_OK) return st;
-    CK(cudaMemcpyAsync(h_u8, ctx->d_plane[6], n, cudaMemcpyDeviceToHost, ctx->s_comp));
+    void* staged[7] = {};
+    if (const sobel5_status ds = download_plane(ctx, 6, h_u8, ctx->d_plane[6], width, height, width,
+                                                ctx->s_comp, staged);
+        ds != SOBEL5_OK)
+        return ds;
     CK(cudaStreamSynchronize(ctx->s_comp));
+    finish_staged(ctx, staged, width, height);
     return SOBEL5_OK;
 }
 
