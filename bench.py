@@ -61,6 +61,9 @@ def parse():
                     help="32k-bands halo transport")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="testing only: every rank uses cuda:0 and gloo (exercises the N>1 "
+                         "code path on a one-GPU box; numbers are not scaling numbers)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="budget of CPU work for the cpu_baseline sample")
     return ap.parse_args()
@@ -243,9 +246,14 @@ def main():
     from paper_2305_00515_b200 import _abi, api
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    if a.share_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if a.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     _abi.load()
 
@@ -327,7 +335,7 @@ def main():
     launches = api.launch_count() - launches0
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms], device="cpu" if a.share_gpu else dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
@@ -497,6 +505,7 @@ def main():
                          else "sobel5_stream_kernel",
                          "kernel_us": ms_step * 1e3},
             "gpu_launches": launches,
+            **({"share_gpu": "testing mode: all ranks on cuda:0 over gloo"} if a.share_gpu else {}),
             "clocks": clocks.summary(),
             "variants": variants,
             "e2e": e2e,

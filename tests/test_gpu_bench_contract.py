@@ -1,0 +1,41 @@
+"""GPU: bench.py's JSON contract, single rank and the multi-rank path
+(torchrun, 2 ranks; --share-gpu puts both on cuda:0 over gloo so the N>1
+code -- frame split, max over ranks, rank-0 line -- runs on a one-GPU box)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+        "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "gpu_launches", "clocks")
+
+
+def run(args, timeout=600):
+    r = subprocess.run(args, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_single_rank_line(cuda):
+    d = run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3", "--no-cpu-baseline",
+             "--no-e2e"])
+    for k in KEYS:
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] == 5
+    assert 0 < d["roofline"]["frac"] < 1.2 and d["roofline"]["bound"] == "hbm"
+
+
+@pytest.mark.parametrize("workload", ["8k", "32k-bands"])
+def test_two_ranks_share_gpu(cuda, workload):
+    d = run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+             "--master-addr", "127.0.0.1", "--master-port", "29537", "bench.py", "--gpus", "2",
+             "--steps", "4", "--warmup", "3", "--workload", workload, "--share-gpu",
+             "--no-cpu-baseline", "--no-e2e"])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["scaling"] == ("strong" if workload == "32k-bands" else "weak")
