@@ -473,7 +473,8 @@ def main():
                        "path": "sobel5::run_stream (C++ drop-in, include/sobel5_b200), fresh "
                                "StreamResult planes per call",
                        "parts_ms": {k: d[k] for k in ("alloc_planes_ms", "run_host_pageable_ms",
-                                                      "run_host_pinned_ms")}}
+                                                      "run_host_pinned_ms", "run_stream_3x3_ms")
+                                    if k in d}}
         except Exception as ex:  # informative only
             e2e_cpp = {"error": str(ex)[:200]}
 

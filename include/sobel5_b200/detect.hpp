@@ -61,21 +61,24 @@ inline Stream3Result run_stream_3x3(const GrayPlane& img, const StripPlan& plan,
     if (plan.in_width != img.width() || plan.radius != 1)
         throw DimMismatch("strip plan covers " + std::to_string(plan.in_width) + " columns at radius " +
                           std::to_string(plan.radius) + ", image has " + std::to_string(img.width()));
+    // device work first, planes built while it runs (gpu::collect_pending)
     Stream3Result out;
     const int ow = img.width() - 2, oh = img.height() - 2;
-    out.gx = SignedPlane(ow, oh);
-    out.gy = SignedPlane(ow, oh);
-    out.g = RealPlane(ow, oh);
-    sobel5_planes pl{};
-    pl.pitch = ow;
-    pl.gx = out.gx.data().data();
-    pl.gy = out.gy.data().data();
-    pl.g = out.g.data().data();
-    gpu::Context& ctx = gpu::thread_context();
-    const sobel5_status st = sobel3_run_host(ctx.get(), img.data().data(), img.width(), img.height(),
-                                             prefetch == Prefetch::on ? 1 : 0, &pl);
+    sobel5_ctx* c = gpu::thread_context().get();
+    sobel5_status st = sobel3_run_host_begin(c, img.data().data(), img.width(), img.height(),
+                                             prefetch == Prefetch::on ? 1 : 0, 0x13u /* gx gy g */);
+    if (st == SOBEL5_OK) {
+        std::vector<std::int32_t> gx, gy;
+        std::vector<double> g;
+        st = gpu::collect_pending(c, ow, oh, {{0, &gx}, {1, &gy}, {4, nullptr, &g}}, nullptr);
+        if (st == SOBEL5_OK) {
+            out.gx = SignedPlane(ow, oh, std::move(gx));
+            out.gy = SignedPlane(ow, oh, std::move(gy));
+            out.g = RealPlane(ow, oh, std::move(g));
+        }
+    }
     if (st != SOBEL5_OK)
-        gpu::raise(st, std::string("run_stream_3x3 (") + sobel5_ctx_last_error(ctx.get()) + ")");
+        gpu::raise(st, std::string("run_stream_3x3 (") + sobel5_ctx_last_error(c) + ")");
     out.counters = stream3_counters(img.height(), plan, prefetch);
     return out;
 }

@@ -430,18 +430,78 @@ inline void prefault(const std::vector<std::pair<std::uintptr_t, std::uintptr_t>
 #endif
 }
 
-/// run() for the five StreamResult planes, built while the device works: the
-/// pipeline is enqueued first (sobel5_run_host_begin, results into pinned
-/// staging); the planes' storage is reserved with huge pages and pre-faulted,
-/// then one host thread per plane appends each row chunk as soon as its
-/// download lands (sobel5_run_host_chunk), so the planes are never
-/// zero-filled in user space and the host copy overlaps the transfers.
-/// The result equals the reference's value-initialised-then-written planes.
+/// One result plane of a pending sobel5_run_host_begin / sobel3_run_host_begin:
+/// the ABI plane slot (0 gx, 1 gy, 2 gd, 3 gdt, 4 g) and its storage.
+struct PendingPlane {
+    int slot;
+    std::vector<std::int32_t>* i32 = nullptr;
+    std::vector<double>* f64 = nullptr;
+};
+
+/// Builds the planes of a pending host call while the device works: the
+/// storage is reserved with huge pages and pre-faulted, then one host thread
+/// per plane appends each row chunk as soon as its download lands
+/// (sobel5_run_host_chunk), so the planes are never zero-filled in user
+/// space and the host copy overlaps the transfers.  Always completes the
+/// pending call (sobel5_run_host_finish); returns its status, rethrows
+/// allocation failures.
+inline sobel5_status collect_pending(sobel5_ctx* c, int ow, int oh, const std::vector<PendingPlane>& planes,
+                                     sobel5_diag* d) {
+    const std::size_t n = static_cast<std::size_t>(ow) * static_cast<std::size_t>(oh);
+    std::vector<std::exception_ptr> errs(planes.size());
+    std::vector<char> short_plane(planes.size(), 0);
+    auto fill = [&](std::size_t k, auto& v) {
+        try {
+            using T = typename std::decay_t<decltype(v)>::value_type;
+            const T* src = static_cast<const T*>(sobel5_run_host_staging(c, planes[k].slot));
+            int y0 = 0, y1 = 0;
+            for (int ch = 0; sobel5_run_host_chunk(c, ch, &y0, &y1) == SOBEL5_OK; ++ch)
+                v.insert(v.end(), src + static_cast<std::size_t>(y0) * ow, src + static_cast<std::size_t>(y1) * ow);
+            short_plane[k] = v.size() != n;
+        } catch (...) {
+            errs[k] = std::current_exception();
+        }
+    };
+    auto run_one = [&](std::size_t k) {
+        if (planes[k].i32) fill(k, *planes[k].i32);
+        else fill(k, *planes[k].f64);
+    };
+    bool reserved = true;
+    try {
+        std::vector<std::pair<std::uintptr_t, std::uintptr_t>> ranges;
+        for (const auto& pp : planes)
+            ranges.push_back(pp.i32 ? huge_reserve(*pp.i32, n) : huge_reserve(*pp.f64, n));
+        if (n >= (std::size_t{1} << 22)) prefault(ranges);  // below ~4K the threads cost more
+    } catch (...) {
+        errs[0] = std::current_exception();
+        reserved = false;
+    }
+    if (reserved) {
+        if (n < (std::size_t{1} << 18)) {
+            for (std::size_t k = 0; k < planes.size(); ++k) run_one(k);
+        } else {
+            std::vector<std::thread> th;
+            for (std::size_t k = 1; k < planes.size(); ++k) th.emplace_back([&, k] { run_one(k); });
+            run_one(0);
+            for (auto& x : th) x.join();
+        }
+    }
+    sobel5_status st = sobel5_run_host_finish(c, nullptr, d);  // completes the call: status + diag
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+    if (st == SOBEL5_OK)
+        for (char f : short_plane)
+            if (f) st = SOBEL5_CUDA_ERROR;
+    return st;
+}
+
+/// run() for the five StreamResult planes, built while the device works
+/// (sobel5_run_host_begin, then collect_pending).  The result equals the
+/// reference's value-initialised-then-written planes.
 inline void run_alloc(const GrayPlane& img, const StreamTaps& taps, Prefetch prefetch, StreamResult& out) {
     const sobel5_taps t = to_abi(taps);
     sobel5_ctx* c = thread_context().get();
     const int ow = img.width() - 4, oh = img.height() - 4;
-    const std::size_t n = static_cast<std::size_t>(ow) * static_cast<std::size_t>(oh);
     sobel5_status st = sobel5_run_host_begin(c, img.data().data(), img.width(), img.height(), &t,
                                              prefetch == Prefetch::on ? 1 : 0, 0x1fu);
     if (st == SOBEL5_CUDA_ERROR || st == SOBEL5_OUT_OF_MEMORY)
@@ -449,45 +509,9 @@ inline void run_alloc(const GrayPlane& img, const StreamTaps& taps, Prefetch pre
     raise(st, "run_stream");
     std::vector<std::int32_t> iv[4];
     std::vector<double> gv;
-    std::exception_ptr errs[5];
-    bool chunk_failed[5] = {};
-    auto fill = [&](int plane, auto& v) {
-        try {
-            using T = typename std::decay_t<decltype(v)>::value_type;
-            const T* src = static_cast<const T*>(sobel5_run_host_staging(c, plane));
-            int y0 = 0, y1 = 0;
-            for (int k = 0; sobel5_run_host_chunk(c, k, &y0, &y1) == SOBEL5_OK; ++k)
-                v.insert(v.end(), src + static_cast<std::size_t>(y0) * ow, src + static_cast<std::size_t>(y1) * ow);
-            chunk_failed[plane] = v.size() != n;
-        } catch (...) {
-            errs[plane] = std::current_exception();
-        }
-    };
-    try {
-        std::vector<std::pair<std::uintptr_t, std::uintptr_t>> ranges;
-        for (auto& v : iv) ranges.push_back(huge_reserve(v, n));
-        ranges.push_back(huge_reserve(gv, n));
-        if (n >= (std::size_t{1} << 22)) prefault(ranges);  // below ~4K the threads cost more
-    } catch (...) {
-        errs[0] = std::current_exception();
-    }
-    if (errs[0]) {
-    } else if (n < (std::size_t{1} << 18)) {
-        for (int i = 0; i < 4; ++i) fill(i, iv[i]);
-        fill(4, gv);
-    } else {
-        std::thread th[4];
-        for (int i = 0; i < 4; ++i) th[i] = std::thread([&, i] { fill(i, iv[i]); });
-        fill(4, gv);
-        for (auto& x : th) x.join();
-    }
     sobel5_diag d{};
-    st = sobel5_run_host_finish(c, nullptr, &d);  // completes the call: status + diag
-    for (auto& e : errs)
-        if (e) std::rethrow_exception(e);
-    if (st == SOBEL5_OK)
-        for (bool f : chunk_failed)
-            if (f) st = SOBEL5_CUDA_ERROR;
+    st = collect_pending(c, ow, oh,
+                         {{0, &iv[0]}, {1, &iv[1]}, {2, &iv[2]}, {3, &iv[3]}, {4, nullptr, &gv}}, &d);
     if (st == SOBEL5_CUDA_ERROR || st == SOBEL5_OUT_OF_MEMORY)
         raise(st, std::string("run_stream (") + sobel5_ctx_last_error(c) + ")");
     raise(st, "run_stream", &d);

@@ -291,6 +291,11 @@ sobel5_status sobel5_run_host_finish(sobel5_ctx* ctx, const sobel5_planes* h_out
  * _finish with h_out = NULL completes the call (status, diag) without
  * copying. */
 sobel5_status sobel5_run_host_chunk(sobel5_ctx* ctx, int chunk, int* y0, int* y1);
+/* The same split form for the 3x3 operator (run_stream_3x3): planes gx, gy,
+ * g, g32, u8 (mask bits 0, 1, 4, 5, 6; gd / gdt bits are rejected), then
+ * _chunk / _staging / _finish as above with pitch == width-2. */
+sobel5_status sobel3_run_host_begin(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
+                                    int prefetch, unsigned plane_mask);
 const void* sobel5_run_host_staging(const sobel5_ctx* ctx, int plane);
 
 /* ---- the classic 3x3 two-direction operator ---------

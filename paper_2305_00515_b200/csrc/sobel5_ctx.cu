@@ -481,17 +481,17 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     return drain_stream(ctx, out_w, out_h, chunk, n_chunks, staged, diag_out);
 }
 
-sobel5_status sobel5_run_host_begin(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
-                                    const sobel5_taps* taps, int prefetch, unsigned plane_mask) {
-    if (!ctx) return SOBEL5_INVALID_ARG;
-    if (width < 5 || height < 5) return SOBEL5_IMAGE_TOO_SMALL;
-    if (!h_in || !taps || plane_mask == 0 || plane_mask >= (1u << 7) || ctx->pend.active)
-        return SOBEL5_INVALID_ARG;
+}  // extern "C"
+
+namespace {
+sobel5_status begin_common(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
+                           const sobel5_taps* taps, int prefetch, unsigned plane_mask, int op) {
+    const int R = op == 3 ? 1 : 2;
     CK(cudaSetDevice(ctx->device));
     void* none[7] = {};
     int chunk = 0, n_chunks = 0;
     const sobel5_status st = enqueue_stream(ctx, h_in, width, height, taps, prefetch, plane_mask,
-                                            none, &chunk, &n_chunks);
+                                            none, &chunk, &n_chunks, op);
     if (st != SOBEL5_OK) {
         // drain whatever was enqueued so the context stays usable
         cudaStreamSynchronize(ctx->s_h2d);
@@ -500,12 +500,35 @@ sobel5_status sobel5_run_host_begin(sobel5_ctx* ctx, const uint8_t* h_in, int wi
         return st;
     }
     ctx->pend.active = true;
-    ctx->pend.out_w = width - 4;
-    ctx->pend.out_h = height - 4;
+    ctx->pend.out_w = width - 2 * R;
+    ctx->pend.out_h = height - 2 * R;
     ctx->pend.chunk = chunk;
     ctx->pend.n_chunks = n_chunks;
     ctx->pend.mask = plane_mask;
     return SOBEL5_OK;
+}
+}  // namespace
+
+extern "C" {
+
+sobel5_status sobel5_run_host_begin(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
+                                    const sobel5_taps* taps, int prefetch, unsigned plane_mask) {
+    if (!ctx) return SOBEL5_INVALID_ARG;
+    if (width < 5 || height < 5) return SOBEL5_IMAGE_TOO_SMALL;
+    if (!h_in || !taps || plane_mask == 0 || plane_mask >= (1u << 7) || ctx->pend.active)
+        return SOBEL5_INVALID_ARG;
+    return begin_common(ctx, h_in, width, height, taps, prefetch, plane_mask, 5);
+}
+
+sobel5_status sobel3_run_host_begin(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
+                                    int prefetch, unsigned plane_mask) {
+    if (!ctx) return SOBEL5_INVALID_ARG;
+    if (width < 3 || height < 3) return SOBEL5_IMAGE_TOO_SMALL;  // pipeline.hpp:553-556
+    // gd / gdt do not exist for the 3x3 operator
+    if (!h_in || plane_mask == 0 || plane_mask >= (1u << 7) || (plane_mask & 0xcu) ||
+        ctx->pend.active)
+        return SOBEL5_INVALID_ARG;
+    return begin_common(ctx, h_in, width, height, nullptr, prefetch, plane_mask, 3);
 }
 
 sobel5_status sobel5_run_host_finish(sobel5_ctx* ctx, const sobel5_planes* h_out,

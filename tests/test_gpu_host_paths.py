@@ -159,3 +159,27 @@ def test_chunk_staging_consumer(ctx, oracle):
     d = _abi.Diag()
     assert L.sobel5_run_host_finish(ctx.handle, None, C.byref(d)) == 0
     assert L.sobel5_run_host_chunk(ctx.handle, 0, C.byref(y0), C.byref(y1)) == _abi.INVALID_ARG
+
+
+def test_sobel3_begin_finish(ctx, oracle):
+    """The 3x3 split form: sobel3_run_host_begin -> finish, pageable planes."""
+    from paper_2305_00515_b200 import _abi
+    L = _abi.load()
+    h, w = 1200, 301
+    img = np.random.default_rng(31).integers(0, 256, (h, w), dtype=np.uint8)
+    st, ref = oracle.sobel3_2d(img)
+    assert st == 0
+    ow, oh = w - 2, h - 2
+    assert L.sobel3_run_host_begin(ctx.handle, img.ctypes.data, w, h, 1,
+                                   BIT["gx"] | BIT["gd"]) == _abi.INVALID_ARG  # no gd for 3x3
+    assert L.sobel3_run_host_begin(ctx.handle, img.ctypes.data, 2, h, 1,
+                                   BIT["gx"]) == _abi.IMAGE_TOO_SMALL
+    want = ("gx", "gy", "g", "u8")
+    assert L.sobel3_run_host_begin(ctx.handle, img.ctypes.data, w, h, 1,
+                                   sum(BIT[k] for k in want)) == 0
+    res = {k: np.zeros((oh, ow), DT[k]) for k in want}
+    d = _abi.Diag()
+    assert L.sobel5_run_host_finish(ctx.handle, C.byref(planes_struct(res, ow)), C.byref(d)) == 0
+    for k in ("gx", "gy", "g"):
+        np.testing.assert_array_equal(res[k], ref[k], err_msg=k)
+    np.testing.assert_array_equal(res["u8"], oracle.quantize(ref["g"], "clamp_abs"))

@@ -6,6 +6,7 @@
 //                   Plane(w, h) zero-fills too, plane.hpp:21)
 //   run_host_pageable  sobel5_run_host into already-allocated std::vector planes
 //   run_host_pinned    sobel5_run_host into cudaMallocHost planes
+//   run_stream_3x3     sobel5::run_stream_3x3 (gx, gy, g: 16 B/px) as a user calls it
 // Prints one JSON line.  Build: tools/build_cpp.sh; run on the GPU box.
 #include <cuda_runtime.h>
 
@@ -41,6 +42,8 @@ int main(int argc, char** argv) {
 
     StreamResult keep;
     const double t_run = time_ms(iters, [&] { keep = run_stream(img, taps, plan, Prefetch::on); });
+    Stream3Result keep3;
+    const double t_run3 = time_ms(iters, [&] { keep3 = run_stream_3x3(img, Prefetch::on); });
     const double t_alloc = time_ms(iters, [&] {
         StreamResult r;
         r.gx = SignedPlane(ow, oh);
@@ -86,9 +89,10 @@ int main(int argc, char** argv) {
     std::printf(
         "{\"w\": %d, \"h\": %d, \"iters\": %d, \"run_stream_ms\": %.3f, \"run_stream_gpx_s\": %.4f, "
         "\"alloc_planes_ms\": %.3f, \"run_host_pageable_ms\": %.3f, \"run_host_pinned_ms\": %.3f, "
-        "\"pinned_gpx_s\": %.4f, \"d2h_bytes\": %zu, \"pinned_equals_pageable\": %s}\n",
+        "\"pinned_gpx_s\": %.4f, \"d2h_bytes\": %zu, \"pinned_equals_pageable\": %s, "
+        "\"run_stream_3x3_ms\": %.3f}\n",
         w, h, iters, t_run, px / t_run / 1e6, t_alloc, t_page, t_pin, px / t_pin / 1e6, n * 24,
-        same ? "true" : "false");
+        same ? "true" : "false", t_run3);
     sobel5_ctx_destroy(ctx);
     return same ? 0 : 4;
 }
