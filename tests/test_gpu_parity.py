@@ -264,3 +264,34 @@ def test_epilogue_arithmetic_exhaustive(S, which, hi):
     S.api.check(_abi.load().sobel5_selftest(which, 0, hi, cnt.data_ptr(), None), "selftest")
     torch.cuda.synchronize()
     assert cnt.item() == 0
+
+
+@pytest.mark.parametrize("extra", [0, 4, 12])
+def test_plane_pitch_variants(S, oracle, extra):
+    """Output pitch = round_up(out_w, 4) + extra elements: the lane-pair
+    256-bit stores need 8-column (32-B) aligned rows and fall back to 128-bit
+    stores otherwise; both must write exactly the valid columns."""
+    import torch
+    from paper_2305_00515_b200 import api
+    rng = np.random.default_rng(extra + 1)
+    for w, h in ((301, 37), (1029, 21), (517, 9)):
+        img = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        d_in, pitch = api.alloc_input(w, h)
+        d_in[:, :w].copy_(torch.from_numpy(img))
+        ow, oh = w - 4, h - 4
+        op = (ow + 3) // 4 * 4 + extra
+        dt = {"gx": torch.int32, "gy": torch.int32, "gd": torch.int32, "gdt": torch.int32,
+              "g": torch.float64}
+        out = {}
+        for k in PLANES:  # 32-B aligned bases, poisoned
+            t = torch.full((oh * op + 8,), 7, dtype=dt[k], device="cuda")
+            off = (-(t.data_ptr() // t.element_size())) % (32 // t.element_size())
+            out[k] = t[off:off + oh * op].view(oh, op)
+        api.launch(d_in, pitch, w, h, S.make_stream_taps(), 1, out, op)
+        torch.cuda.synchronize()
+        st, ref, _ = oracle.run_stream(img)
+        for k in PLANES:
+            got = out[k].cpu().numpy()
+            np.testing.assert_array_equal(got[:, :ow], ref[k], err_msg=f"{k} pitch {op}")
+            if op > ow:
+                assert (got[:, ow:] == 7).all(), f"{k}: wrote past the row (pitch {op})"
