@@ -6,13 +6,14 @@
 // Reference flow (sobel5_cli.cpp:127-189): img = pad_replicate(img, r)
 // (:133) -> run_stream (:160-167) -> save_plane(g, normalize) (:177).
 // Here: normalize needs the frame's min/max of g before any pixel can be
-// mapped, so it is two passes over the input (the second recomputes the
-// stencil instead of round-tripping g through HBM):
+// mapped, so it takes two passes:
 //   init   : minmax keys <- (+inf, -inf)
 //   pass 1 : stencil, optional planes, per-frame min/max of g (warp reduce +
-//            one atomic per warp)
+//            one atomic per warp) and, for integer magnitudes, the exact
+//            S = g^2 plane (u32, L2-resident where it fits)
 //   table  : per frame, the exact threshold table of S -> u8 (256 threads)
-//   pass 2 : stencil, u8 = normalize(g) through the table
+//   pass 2 : memory-bound map of the S plane through the table (integer
+//            magnitudes), or the stencil again with the double formula
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -98,30 +99,82 @@ __global__ void norm_table_kernel(const sobel5_minmax* mm, sobel5_norm_table* ta
 }
 
 // Normalize pass 2 of the detect path (integer magnitudes): u8 from the S
-// plane written by pass 1, 4 pixels per thread (16-byte load, 4-byte store).
+// plane written by pass 1, 4 pixels per thread per row (16-byte load, 4-byte
+// store), kRows rows in flight per thread.  u(S) = max{k : thr[k] <= S};
+// a float estimate of (sqrt(S) - lo) * 255 / span picks k, one 8-byte
+// shared load of (thr[k], thr[k+1]) confirms it -- the check is exact, so
+// any estimate is safe -- and a binary search decides the rare misses
+// (tiny spans, estimates off by more than one step).
+__device__ __forceinline__ bool norm_check(uint32_t S, uint32_t e, const uint2* pr) {
+    const uint2 t = pr[e];
+    return t.x <= S && S < t.y;
+}
+__device__ __noinline__ uint32_t norm_search(uint32_t S, const uint32_t* thr) {
+    uint32_t k = 0;
+#pragma unroll
+    for (uint32_t step = 128; step >= 1; step >>= 1)
+        if (thr[k + step] <= S) k += step;
+    return k;
+}
+// est -> clamp(rint(est), ., 255) via the 1.5 * 2^23 mantissa trick; a
+// negative or huge estimate just lands on an entry whose check fails
+__device__ __forceinline__ uint32_t est_index(float m) {
+    return min(__float_as_uint(m) - 0x4B400000u, 255u);
+}
+
 __global__ void norm_map_kernel(const uint32_t* __restrict__ s32, int64_t pitch,
                                 int64_t frame_stride, int out_w, int out_h,
                                 const sobel5_norm_table* __restrict__ tab, uint8_t* __restrict__ u8) {
     __shared__ uint32_t s_thr[257];
+    __shared__ uint2 s_pair[256];
     const sobel5_norm_table* t = tab + blockIdx.z;
     for (int i = threadIdx.x; i < 257; i += blockDim.x) s_thr[i] = t->thr[i];
-    const float lo_f = t->lo_f, scale_f = t->scale_f;
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_pair[i] = make_uint2(s_thr[i], s_thr[i + 1]);
+    const float2 scale2 = make_float2(t->scale_f, t->scale_f);
+    const float nlo = -t->lo_f * t->scale_f;
+    const float2 off2 = make_float2(nlo, nlo);
+    const float2 magic2 = make_float2(12582912.0f, 12582912.0f);
     __syncthreads();
     const int x = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
     if (x >= out_w) return;
     const int64_t base = static_cast<int64_t>(blockIdx.z) * frame_stride + x;
-    for (int y = blockIdx.y; y < out_h; y += gridDim.y) {
-        const int64_t o = base + static_cast<int64_t>(y) * pitch;
-        const uint4 S = __ldcs(reinterpret_cast<const uint4*>(s32 + o));
-        const uint32_t u0 = u8_normalize_s(S.x, s_thr, lo_f, scale_f);
-        const uint32_t u1 = u8_normalize_s(S.y, s_thr, lo_f, scale_f);
-        const uint32_t u2 = u8_normalize_s(S.z, s_thr, lo_f, scale_f);
-        const uint32_t u3 = u8_normalize_s(S.w, s_thr, lo_f, scale_f);
-        if (x + 3 < out_w) {
-            st_cs_u32(u8 + o, pack_u8x4(u0, u1, u2, u3));
-        } else {
-            const uint32_t u[4] = {u0, u1, u2, u3};
-            for (int j = 0; j < 4 && x + j < out_w; ++j) u8[o + j] = static_cast<uint8_t>(u[j]);
+    // kRows rows per iteration: their loads are in flight together (one
+    // 16-B load per thread per row would leave HBM latency exposed)
+    constexpr int kRows = 4;
+    for (int y0 = blockIdx.y * kRows; y0 < out_h; y0 += gridDim.y * kRows) {
+        uint4 S[kRows];
+#pragma unroll
+        for (int k = 0; k < kRows; ++k)
+            if (y0 + k < out_h)
+                S[k] = __ldcs(reinterpret_cast<const uint4*>(s32 + base + static_cast<int64_t>(y0 + k) * pitch));
+#pragma unroll
+        for (int k = 0; k < kRows; ++k) {
+            if (y0 + k >= out_h) break;
+            const int64_t o = base + static_cast<int64_t>(y0 + k) * pitch;
+            const uint4 v = S[k];
+            const float2 fa = make_float2(__uint2float_rn(v.x), __uint2float_rn(v.y));
+            const float2 fb = make_float2(__uint2float_rn(v.z), __uint2float_rn(v.w));
+            const float2 ra = make_float2(rsqrt_approx(fmaxf(fa.x, 1.0f)), rsqrt_approx(fmaxf(fa.y, 1.0f)));
+            const float2 rb = make_float2(rsqrt_approx(fmaxf(fb.x, 1.0f)), rsqrt_approx(fmaxf(fb.y, 1.0f)));
+            const float2 ma = __fadd2_rn(__ffma2_rn(__fmul2_rn(fa, ra), scale2, off2), magic2);
+            const float2 mb = __fadd2_rn(__ffma2_rn(__fmul2_rn(fb, rb), scale2, off2), magic2);
+            uint32_t u0 = est_index(ma.x), u1 = est_index(ma.y);
+            uint32_t u2 = est_index(mb.x), u3 = est_index(mb.y);
+            const bool k0 = norm_check(v.x, u0, s_pair), k1 = norm_check(v.y, u1, s_pair);
+            const bool k2 = norm_check(v.z, u2, s_pair), k3 = norm_check(v.w, u3, s_pair);
+            if (!(k0 && k1 && k2 && k3)) {  // rare: one branch per 4 pixels
+                if (!k0) u0 = norm_search(v.x, s_thr);
+                if (!k1) u1 = norm_search(v.y, s_thr);
+                if (!k2) u2 = norm_search(v.z, s_thr);
+                if (!k3) u3 = norm_search(v.w, s_thr);
+            }
+            if (x + 3 < out_w) {
+                st_cs_u32(u8 + o, pack_u8x4(u0, u1, u2, u3));
+            } else {
+                const uint32_t u[4] = {u0, u1, u2, u3};
+                for (int j = 0; j < 4 && x + j < out_w; ++j) u8[o + j] = static_cast<uint8_t>(u[j]);
+            }
         }
     }
 }
@@ -215,9 +268,13 @@ sobel5_status detect_normalize(void* scratch, int frames, bool exact, const sobe
     count_launch();
     if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return map_cuda(e);
     if (exact) {
-        const dim3 grid(static_cast<unsigned>((out_w + 4 * 128 - 1) / (4 * 128)),
-                        static_cast<unsigned>(std::min(out_h, 65535)),
-                        static_cast<unsigned>(frames));
+        // a few thousand CTAs that loop over rows: every CTA first stages the
+        // 257-entry threshold table in shared memory, so one CTA per row
+        // (the first version) spent more loads on tables than on pixels
+        const unsigned gx = static_cast<unsigned>((out_w + 4 * 128 - 1) / (4 * 128));
+        const unsigned gy = static_cast<unsigned>(std::max(
+            1, std::min((out_h + 3) / 4, static_cast<int>(148u * 16u / (gx * frames)) + 1)));
+        const dim3 grid(gx, gy, static_cast<unsigned>(frames));
         norm_map_kernel<<<grid, 128, 0, s>>>(e1.s32, d_out->pitch, out_frame_stride, out_w, out_h,
                                              tab, d_out->u8);
         count_launch();
