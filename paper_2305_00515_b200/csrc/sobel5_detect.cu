@@ -190,15 +190,27 @@ template <class T>
 __global__ void plane_minmax_kernel(const T* plane, int64_t pitch, int width, int height,
                                     sobel5_minmax* mm) {
     unsigned long long lo = ~0ull, hi = 0ull;
-    const int64_t n = static_cast<int64_t>(width) * height;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t y = i / width, x = i - y * width;
-        const double v = as_double(plane[y * pitch + x]);
-        if (v != v) continue;  // NaN never occurs for Sobel planes
-        const unsigned long long k = dkey(v);
-        lo = min(lo, k);
-        hi = max(hi, k);
+    // 2-D grid-stride (rows over blockIdx.y, columns over x): no per-element
+    // 64-bit division
+    constexpr int kU = 4;  // loads in flight per thread
+    for (int y = blockIdx.y; y < height; y += gridDim.y) {
+        const T* row = plane + static_cast<int64_t>(y) * pitch;
+        const int stride = gridDim.x * blockDim.x;
+        for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < width; x += kU * stride) {
+            T vals[kU];
+#pragma unroll
+            for (int k = 0; k < kU; ++k)
+                if (x + k * stride < width) vals[k] = __ldcs(row + x + k * stride);
+#pragma unroll
+            for (int k = 0; k < kU; ++k) {
+                if (x + k * stride >= width) break;
+                const double v = as_double(vals[k]);
+                if (v != v) continue;  // NaN never occurs for Sobel planes
+                const unsigned long long key = dkey(v);
+                lo = min(lo, key);
+                hi = max(hi, key);
+            }
+        }
     }
     for (int o = 16; o > 0; o >>= 1) {
         lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
@@ -215,19 +227,30 @@ template <class T>
 __global__ void plane_map_kernel(const T* plane, int64_t pitch, int width, int height, int mode,
                                  const sobel5_norm_table* tab, uint8_t* out, int64_t out_pitch) {
     const double lo = mode ? tab->lo : 0.0, span = mode ? tab->span : 0.0;
-    const int64_t n = static_cast<int64_t>(width) * height;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t y = i / width, x = i - y * width;
-        const double v = as_double(plane[y * pitch + x]);
-        uint32_t u;
-        if (mode) {
-            u = normalize_u8(v, lo, span);
-        } else {
-            const double r = round(fabs(v));
-            u = r < 255.0 ? static_cast<uint32_t>(r) : 255u;
+    constexpr int kU = 4;  // loads in flight per thread
+    for (int y = blockIdx.y; y < height; y += gridDim.y) {
+        const T* row = plane + static_cast<int64_t>(y) * pitch;
+        uint8_t* orow = out + static_cast<int64_t>(y) * out_pitch;
+        const int stride = gridDim.x * blockDim.x;
+        for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < width; x += kU * stride) {
+            T vals[kU];
+#pragma unroll
+            for (int k = 0; k < kU; ++k)
+                if (x + k * stride < width) vals[k] = __ldcs(row + x + k * stride);
+#pragma unroll
+            for (int k = 0; k < kU; ++k) {
+                if (x + k * stride >= width) break;
+                const double v = as_double(vals[k]);
+                uint32_t u;
+                if (mode) {
+                    u = normalize_u8(v, lo, span);
+                } else {
+                    const double r = round(fabs(v));
+                    u = r < 255.0 ? static_cast<uint32_t>(r) : 255u;
+                }
+                orow[x + k * stride] = static_cast<uint8_t>(u);
+            }
         }
-        out[y * out_pitch + x] = static_cast<uint8_t>(u);
     }
 }
 
@@ -360,7 +383,8 @@ sobel5_status sobel5_quantize_plane(const void* d_plane, int kind, int64_t pitch
         pitch < width || u8_pitch < width)
         return SOBEL5_INVALID_ARG;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int blocks = 148 * 8;
+    const unsigned bx = static_cast<unsigned>(std::min((width + 1023) / 1024, 148 * 8));
+    const dim3 blocks(bx, static_cast<unsigned>(std::max(1, std::min(height, static_cast<int>(148u * 8u / bx)))));
     sobel5_norm_table* tab = nullptr;
     if (save_mode == 1) {
         if (!d_scratch || reinterpret_cast<uintptr_t>(d_scratch) % 16 != 0)
