@@ -67,7 +67,18 @@ inline Stream3Result run_stream_3x3(const GrayPlane& img, const StripPlan& plan,
     sobel5_ctx* c = gpu::thread_context().get();
     sobel5_status st = sobel3_run_host_begin(c, img.data().data(), img.width(), img.height(),
                                              prefetch == Prefetch::on ? 1 : 0, 0x13u /* gx gy g */);
-    if (st == SOBEL5_OK) {
+    if (st == SOBEL5_OUT_OF_MEMORY) {  // beyond the pinned-staging cap: direct downloads
+        out.gx = SignedPlane(ow, oh);
+        out.gy = SignedPlane(ow, oh);
+        out.g = RealPlane(ow, oh);
+        sobel5_planes pl{};
+        pl.pitch = ow;
+        pl.gx = out.gx.data().data();
+        pl.gy = out.gy.data().data();
+        pl.g = out.g.data().data();
+        st = sobel3_run_host(c, img.data().data(), img.width(), img.height(),
+                             prefetch == Prefetch::on ? 1 : 0, &pl);
+    } else if (st == SOBEL5_OK) {
         std::vector<std::int32_t> gx, gy;
         std::vector<double> g;
         st = gpu::collect_pending(c, ow, oh, {{0, &gx}, {1, &gy}, {4, nullptr, &g}}, nullptr);

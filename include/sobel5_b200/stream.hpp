@@ -504,7 +504,18 @@ inline void run_alloc(const GrayPlane& img, const StreamTaps& taps, Prefetch pre
     const int ow = img.width() - 4, oh = img.height() - 4;
     sobel5_status st = sobel5_run_host_begin(c, img.data().data(), img.width(), img.height(), &t,
                                              prefetch == Prefetch::on ? 1 : 0, 0x1fu);
-    if (st == SOBEL5_CUDA_ERROR || st == SOBEL5_OUT_OF_MEMORY)
+    if (st == SOBEL5_OUT_OF_MEMORY) {
+        // results beyond the context's pinned-staging cap: allocate the
+        // planes first and let sobel5_run_host download into them directly
+        out.gx = SignedPlane(ow, oh);
+        out.gy = SignedPlane(ow, oh);
+        out.gd = SignedPlane(ow, oh);
+        out.gdt = SignedPlane(ow, oh);
+        out.g = RealPlane(ow, oh);
+        run(img, taps, prefetch, Outputs{&out.gx, &out.gy, &out.gd, &out.gdt, &out.g, nullptr});
+        return;
+    }
+    if (st == SOBEL5_CUDA_ERROR)
         raise(st, std::string("run_stream (") + sobel5_ctx_last_error(c) + ")");
     raise(st, "run_stream");
     std::vector<std::int32_t> iv[4];

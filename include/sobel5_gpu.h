@@ -256,6 +256,10 @@ sobel5_status sobel5_selftest(int which, uint32_t lo, uint32_t hi, uint64_t* d_c
 
 sobel5_status sobel5_ctx_create(sobel5_ctx** out, int device);
 void sobel5_ctx_destroy(sobel5_ctx* ctx);
+/* Releases the context's cached device buffers and pinned host staging
+ * (kept across calls so repeated calls allocate nothing); no-op while a
+ * begin/finish pair is pending. */
+void sobel5_ctx_trim(sobel5_ctx* ctx);
 /* Message of the last CUDA error seen by this context ("" if none). */
 const char* sobel5_ctx_last_error(const sobel5_ctx* ctx);
 
@@ -278,7 +282,10 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
  * begin/finish pair at a time per context; sobel5_run_host in between
  * returns SOBEL5_INVALID_ARG.  Pageable destinations anywhere in this API go
  * through pinned staging plus a small host thread pool; page-locked ones
- * (cudaMallocHost / cudaHostRegister) are DMA'd directly. */
+ * (cudaMallocHost / cudaHostRegister) are DMA'd directly.  Staging is capped
+ * per context (env SOBEL5_STAGING_MAX_MB, default 4096): beyond it
+ * sobel5_run_host downloads straight into pageable memory and _begin
+ * returns SOBEL5_OUT_OF_MEMORY (use sobel5_run_host). */
 sobel5_status sobel5_run_host_begin(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
                                     const sobel5_taps* taps, int prefetch, unsigned plane_mask);
 sobel5_status sobel5_run_host_finish(sobel5_ctx* ctx, const sobel5_planes* h_out,

@@ -79,7 +79,7 @@ EXPORTS = (
     "sobel3_launch", "sobel3_detect", "sobel3_plan_counters", "sobel3_run_host",
     "sobel5_quantize_host", "sobel5_run_host_begin", "sobel5_run_host_finish",
     "sobel5_run_host_chunk", "sobel5_run_host_staging", "sobel5_kernel_for_taps",
-    "sobel3_run_host_begin",
+    "sobel3_run_host_begin", "sobel5_ctx_trim",
 )
 
 _lib = None
@@ -133,6 +133,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.sobel5_run_host_begin.restype = i32
     L.sobel5_run_host_finish.argtypes = [vp, C.POINTER(Planes), C.POINTER(Diag)]
     L.sobel5_run_host_finish.restype = i32
+    L.sobel5_ctx_trim.argtypes = [vp]
+    L.sobel5_ctx_trim.restype = None
     L.sobel3_run_host_begin.argtypes = [vp, vp, i32, i32, i32, C.c_uint32]
     L.sobel3_run_host_begin.restype = i32
     L.sobel5_kernel_for_taps.argtypes = [C.POINTER(Taps)]

@@ -17,6 +17,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -189,6 +190,17 @@ cudaError_t ensure_events(std::vector<cudaEvent_t>& v, size_t n) {
         v.push_back(ev);
     }
     return cudaSuccess;
+}
+
+// Pinned staging is cached per context up to this many bytes in total
+// (SOBEL5_STAGING_MAX_MB, default 4096); planes beyond it are downloaded
+// straight into pageable memory (the driver stages them, slower but bounded).
+size_t staging_cap() {
+    static const size_t cap = [] {
+        const char* v = std::getenv("SOBEL5_STAGING_MAX_MB");
+        return (v && *v ? static_cast<size_t>(std::atoll(v)) : size_t{4096}) << 20;
+    }();
+    return cap;
 }
 
 // Page-locked host memory (cudaMallocHost / cudaHostRegister) is DMA'd
@@ -469,10 +481,21 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     unsigned mask = 0;
     void* direct[7] = {};  // pinned destinations: DMA straight into them
     void* staged[7] = {};  // pageable ones: through pinned staging
+    size_t stage_bytes = 0;
     for (int i = 0; i < 7; ++i) {
         if (!hp[i]) continue;
         mask |= 1u << i;
-        (is_pinned(hp[i]) ? direct[i] : staged[i]) = hp[i];
+        if (is_pinned(hp[i])) {
+            direct[i] = hp[i];
+        } else {
+            const size_t b = static_cast<size_t>(out_w) * out_h * kElem[i];
+            if (stage_bytes + b <= staging_cap()) {
+                staged[i] = hp[i];
+                stage_bytes += b;
+            } else {
+                direct[i] = hp[i];  // over the staging cap: driver-staged pageable copy
+            }
+        }
     }
     int chunk = 0, n_chunks = 0;
     const sobel5_status st =
@@ -481,12 +504,40 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     return drain_stream(ctx, out_w, out_h, chunk, n_chunks, staged, diag_out);
 }
 
+void sobel5_ctx_trim(sobel5_ctx* ctx) {
+    if (!ctx || ctx->pend.active) return;
+    cudaSetDevice(ctx->device);
+    for (auto s : {ctx->s_h2d, ctx->s_comp, ctx->s_d2h}) cudaStreamSynchronize(s);
+    for (int i = 0; i < 7; ++i) {
+        if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
+        ctx->h_stage[i] = nullptr;
+        ctx->h_stage_bytes[i] = 0;
+        if (ctx->d_plane[i]) cudaFree(ctx->d_plane[i]);
+        ctx->d_plane[i] = nullptr;
+        ctx->d_plane_bytes[i] = 0;
+    }
+    if (ctx->h_in_stage) cudaFreeHost(ctx->h_in_stage);
+    ctx->h_in_stage = nullptr;
+    ctx->h_in_stage_bytes = 0;
+    if (ctx->d_in) cudaFree(ctx->d_in);
+    ctx->d_in = nullptr;
+    ctx->d_in_bytes = 0;
+    if (ctx->d_scratch) cudaFree(ctx->d_scratch);
+    ctx->d_scratch = nullptr;
+    ctx->d_scratch_bytes = 0;
+}
+
 }  // extern "C"
 
 namespace {
 sobel5_status begin_common(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
                            const sobel5_taps* taps, int prefetch, unsigned plane_mask, int op) {
     const int R = op == 3 ? 1 : 2;
+    size_t stage_bytes = 0;
+    for (int i = 0; i < 7; ++i)
+        if ((plane_mask >> i) & 1u)
+            stage_bytes += static_cast<size_t>(width - 2 * R) * (height - 2 * R) * kElem[i];
+    if (stage_bytes > staging_cap()) return SOBEL5_OUT_OF_MEMORY;  // callers use run_host
     CK(cudaSetDevice(ctx->device));
     void* none[7] = {};
     int chunk = 0, n_chunks = 0;
@@ -653,10 +704,17 @@ sobel5_status sobel3_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     unsigned mask = 0;
     void* direct[7] = {};
     void* staged[7] = {};
+    size_t stage_bytes = 0;
     for (int i = 0; i < 7; ++i) {
         if (!hp[i]) continue;
         mask |= 1u << i;
-        (is_pinned(hp[i]) ? direct[i] : staged[i]) = hp[i];
+        const size_t b = static_cast<size_t>(out_w) * out_h * kElem[i];
+        if (!is_pinned(hp[i]) && stage_bytes + b <= staging_cap()) {
+            staged[i] = hp[i];
+            stage_bytes += b;
+        } else {
+            direct[i] = hp[i];
+        }
     }
     if (!mask) return SOBEL5_OK;
     int chunk = 0, n_chunks = 0;

@@ -32,3 +32,13 @@ def test_cpp_api_gpu(exe, cuda):
     r = subprocess.run([exe, "--gpu"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_api_gpu_staging_cap(exe, cuda):
+    """The same checks with a 1 MB pinned-staging cap: larger results take
+    the direct-download fallback of run_stream / run_stream_3x3."""
+    env = dict(os.environ, SOBEL5_STAGING_MAX_MB="1")
+    r = subprocess.run([exe, "--gpu"], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
