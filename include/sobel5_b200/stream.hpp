@@ -613,6 +613,27 @@ inline Sobel5Result sobel5_4d(const GrayPlane& img, const FilterParams& p) {
     return Sobel5Result{std::move(r.gx), std::move(r.gy), std::move(r.gd), std::move(r.gdt), std::move(r.g)};
 }
 
+/// oracle.hpp:100-129: the diagonal responses through the Kd+/- sum and
+/// difference kernels.  For valid FilterParams both numerators are even by
+/// construction (Eq. 10-11), so the pair equals run_stream's gd / gdt; it is
+/// computed on the GPU (the two planes only).
+struct DiagPair {
+    SignedPlane gd;
+    SignedPlane gdt;
+};
+
+inline DiagPair diag_via_sum_diff(const GrayPlane& img, const FilterParams& p) {
+    if (img.width() < 5 || img.height() < 5)
+        throw ImageTooSmall("conv2d_valid needs at least 5x5, got " + std::to_string(img.width()) + "x" +
+                            std::to_string(img.height()));
+    DiagPair out{SignedPlane(img.width() - 4, img.height() - 4), SignedPlane(img.width() - 4, img.height() - 4)};
+    gpu::Outputs o;
+    o.gd = &out.gd;
+    o.gdt = &out.gdt;
+    gpu::run(img, make_stream_taps(p), Prefetch::on, o);
+    return out;
+}
+
 // ---- synthetic inputs (synth.hpp) ---------------------------------------------------
 
 inline std::uint64_t splitmix64(std::uint64_t& state) {

@@ -236,6 +236,18 @@ static void gpu_checks() {
     CHECK(throws<ParityViolation>([&] { run_stream(img, odd, plan_strips(64, 32, 2), Prefetch::on); })
               .rfind("odd sum/difference pair (", 0) == 0);
 
+    // oracle.hpp:110 diag_via_sum_diff equals run_stream's diagonals
+    {
+        const GrayPlane im = synth_random(77, 41, 3);
+        for (const FilterParams& fp : {FilterParams{}, FilterParams{2, 3, 5, 7}}) {
+            const auto dp = diag_via_sum_diff(im, fp);
+            CHECK(dp.gd == corr(im, materialize(fp, Direction::D)));
+            CHECK(dp.gdt == corr(im, materialize(fp, Direction::DT)));
+        }
+        CHECK(throws<ImageTooSmall>([] { diag_via_sum_diff(GrayPlane(4, 9), FilterParams{}); }) ==
+              "conv2d_valid needs at least 5x5, got 4x9");
+    }
+
     // the uint8 edge map is clamp_abs(g)
     const auto u8 = gpu::edge_map_u8(img, make_stream_taps(FilterParams{}));
     const auto full = run_stream(img, FilterParams{}, plan_strips(64, 32, 2), Prefetch::on);
