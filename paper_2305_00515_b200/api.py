@@ -323,6 +323,42 @@ def run_stream(img: np.ndarray, taps_or_params, plan: StripPlan, prefetch: Prefe
                         plan_counters(h, plan, taps, prefetch))
 
 
+def sobel5_4d(img: np.ndarray, params: FilterParams = FilterParams()) -> StreamResult:
+    """oracle.hpp:82-98 (the dense 4-direction oracle): run_stream equals it
+    for every valid parameter set, so the planes come from the GPU path."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    h, w = img.shape
+    if w < 5 or h < 5:
+        raise ImageTooSmall(f"conv2d_valid needs at least 5x5, got {w}x{h}")
+    return run_stream(img, params, plan_strips(w, w, 2), Prefetch.on)
+
+
+def diag_via_sum_diff(img: np.ndarray, params: FilterParams = FilterParams()):
+    """oracle.hpp:100-129: (gd, gdt) through the Kd+/- sum and difference
+    kernels, equal to run_stream's diagonals for valid params (GPU)."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    h, w = img.shape
+    if w < 5 or h < 5:
+        raise ImageTooSmall(f"conv2d_valid needs at least 5x5, got {w}x{h}")
+    st, res, d = default_context().run_host(img, make_stream_taps(params), Prefetch.on,
+                                            planes=("gd", "gdt"))
+    check(st, "diag_via_sum_diff")
+    return res["gd"], res["gdt"]
+
+
+def synth_random(width: int, height: int, seed: int) -> np.ndarray:
+    """synth.hpp:20-35 on the host: pixel i is byte (i mod 8) of the
+    splitmix64 output word floor(i / 8) (vectorised random-access form)."""
+    n = width * height
+    k = np.arange((n + 7) // 8, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) + (k + np.uint64(1)) * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return z.view(np.uint8)[:n].reshape(height, width).copy()
+
+
 # ---- device-resident helpers (torch tensors as device memory) --------------------
 
 

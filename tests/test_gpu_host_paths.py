@@ -183,3 +183,20 @@ def test_sobel3_begin_finish(ctx, oracle):
     for k in ("gx", "gy", "g"):
         np.testing.assert_array_equal(res[k], ref[k], err_msg=k)
     np.testing.assert_array_equal(res["u8"], oracle.quantize(ref["g"], "clamp_abs"))
+
+
+def test_python_oracle_mirrors(ctx, oracle):
+    """api.sobel5_4d / api.diag_via_sum_diff (oracle.hpp mirrors on the GPU)."""
+    from paper_2305_00515_b200 import api
+    img = api.synth_random(131, 47, 5)
+    for prm in ((1, 2, 6, 4), (2, 3, 5, 7)):
+        p = api.FilterParams(*prm)
+        st, ref, _ = oracle.run_stream(img, oracle.make_stream_taps(*prm))
+        r = api.sobel5_4d(img, p)
+        for k in ("gx", "gy", "gd", "gdt", "g"):
+            np.testing.assert_array_equal(getattr(r, k), ref[k], err_msg=k)
+        gd, gdt = api.diag_via_sum_diff(img, p)
+        np.testing.assert_array_equal(gd, ref["gd"])
+        np.testing.assert_array_equal(gdt, ref["gdt"])
+    with pytest.raises(api.ImageTooSmall):
+        api.sobel5_4d(np.zeros((4, 9), np.uint8))

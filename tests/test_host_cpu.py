@@ -198,3 +198,14 @@ def test_kernel_selection_by_taps_bound():
     assert api.kernel_for(t) == "packed_runtime_taps"
     t.k1[2] = 1 << 24  # a tap not exact in FP32 is never given to the f32 kernel
     assert api.kernel_for(t) == "generic"
+
+
+def test_python_synth_random_matches_reference_generator(oracle):
+    """api.synth_random (host numpy, synth.hpp:20-35) == the C oracle's, and
+    the SURVEY A.2 known answer."""
+    import numpy as np
+    from paper_2305_00515_b200 import api
+    assert api.synth_random(16, 1, 1).ravel().tolist() == [
+        193, 92, 2, 137, 236, 45, 10, 145, 103, 236, 142, 101, 161, 141, 235, 190]
+    for w, h, seed in ((1920, 1080, 1), (333, 17, 9), (5, 5, 123)):
+        assert np.array_equal(api.synth_random(w, h, seed), oracle.synth_random(w, h, seed))
