@@ -208,6 +208,12 @@ bool taps_fit_f32_p(const KernelParams& kp) {
 cudaError_t dispatch(const KernelParams& kp, dim3 grid, int prefetch, bool dflt, MagMode mag,
                      cudaStream_t s) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (dflt && env_int("SOBEL5_DENSE", 0) != 0 && !kp.pad && kp.top_rows == 0 && !kp.bot &&
+        grid.z == 1 && (packed_out_set(kp) == kOutSR || packed_out_set(kp) == kOutU8)) {
+        // ablation only: four dense 5x5 correlations, no operator
+        // transformation (sobel5_k_dense.cu)
+        return launch_dense_ablation(kp, grid, s);
+    }
     if (dflt && env_int("SOBEL5_GENERIC", 0) == 0) {
         // default taps: packed two-pixels-per-register kernel (sobel5_packed.cuh)
         if (kp.pad) return launch_packed_pad(kp, grid, prefetch, s);

@@ -25,6 +25,9 @@ cudaError_t launch_packed_rt_pad(const KernelParams& kp, dim3 grid, int pf, cuda
 // Packed-FP32 kernel with runtime taps (sobel5_f32x2.cuh), every geometry.
 cudaError_t launch_f32(const KernelParams& kp, dim3 grid, int pf, MagMode mag, cudaStream_t s);
 
+// Ablation only: default taps as four dense 5x5 correlations (sobel5_k_dense.cu).
+cudaError_t launch_dense_ablation(const KernelParams& kp, dim3 grid, cudaStream_t s);
+
 // Generic-taps kernel (sobel5_stream.cuh).
 cudaError_t launch_generic(const KernelParams& kp, dim3 grid, int pf, bool default_taps,
                            MagMode mag, cudaStream_t s);

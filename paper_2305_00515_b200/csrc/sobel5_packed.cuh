@@ -254,10 +254,37 @@ __global__ void __launch_bounds__(kCtaThreads,
     const bool load_a = x0 < p.width;
     // the one extra word: lane 31's right neighbour; in pad mode lane 0's left
     const int xoff = (PAD && lane == 0) ? -4 : 4;
-    const bool load_b = (lane == 31 && x0 + 4 < p.width) || (PAD && lane == 0 && x0 > 0);
+    // Column sharing (the paper's idea 1).  Ablation builds only
+    // (-DSOBEL5_COLSHARE, plain geometry): 0 = warp shuffle (default),
+    // 1 = every lane loads its right neighbour word itself (redundant global
+    // loads, L1 hits), 2 = each warp stages its row words in shared memory.
+#ifndef SOBEL5_COLSHARE
+#define SOBEL5_COLSHARE 0
+#endif
+    constexpr int CS = PAD ? 0 : SOBEL5_COLSHARE;
+    const bool load_b = CS == 1 ? (x0 + 4 < p.width)
+                                : (lane == 31 && x0 + 4 < p.width) || (PAD && lane == 0 && x0 > 0);
     const bool full = x0 + 3 < p.out_w;
     const bool warp_full = warp_x0 + kWarpCols <= p.out_w;  // warp-uniform
     const PadEdge pe = PAD ? pad_edge_setup(p.width, warp_x0) : PadEdge{0, 0, 0, 0u};
+    __shared__ uint32_t s_cols[CS == 2 ? kCtaWarps * 2 * 33 : 1];
+    int cs_buf = 0;
+    auto window = [&](uint32_t own, uint32_t xtra, uint32_t& wa, uint32_t& wb) {
+        if constexpr (CS == 0) {
+            row_window<PAD>(own, xtra, lane, x0, p.width, pe, wa, wb);
+        } else if constexpr (CS == 1) {
+            wa = own;
+            wb = xtra;
+        } else {  // double-buffered per warp; the next call's syncwarp orders reuse
+            uint32_t* row = s_cols + (warp * 2 + cs_buf) * 33;
+            row[lane] = own;
+            if (lane == 31) row[32] = xtra;
+            __syncwarp();
+            wa = own;
+            wb = row[lane + 1];
+            cs_buf ^= 1;
+        }
+    };
 
     // Plain images: rows are loaded strictly in order, so one running
     // pointer advanced by the pitch replaces the 64-bit address arithmetic
@@ -302,7 +329,7 @@ __global__ void __launch_bounds__(kCtaThreads,
             if (k < n_in) load_row(k, qa[k], qb[k]);
             else qa[k] = qb[k] = 0u;
         }
-        row_window<PAD>(qa[0], qb[0], lane, x0, p.width, pe, cur_a, cur_b);
+        window(qa[0], qb[0], cur_a, cur_b);
     }
 
     for (int base = 0; base < n_in; base += 5) {
@@ -317,7 +344,7 @@ __global__ void __launch_bounds__(kCtaThreads,
             } else {
                 uint32_t o, x;
                 load_row(r, o, x);
-                row_window<PAD>(o, x, lane, x0, p.width, pe, wa, wb);
+                window(o, x, wa, wb);
             }
 
             // E_k = byte k | byte k+2 << 16
@@ -335,7 +362,7 @@ __global__ void __launch_bounds__(kCtaThreads,
                 if (r + 5 < n_in) load_row(r + 5, qa[s], qb[s]);
                 // warp-shuffle column sharing for row r+1
                 const int sn = (s + 1) % 5;
-                row_window<PAD>(qa[sn], qb[sn], lane, x0, p.width, pe, cur_a, cur_b);
+                window(qa[sn], qb[sn], cur_a, cur_b);
             }
 
             uint32_t F[2], H[2], D[2], K0[2], K1[2];
