@@ -295,3 +295,18 @@ def test_plane_pitch_variants(S, oracle, extra):
             np.testing.assert_array_equal(got[:, :ow], ref[k], err_msg=f"{k} pitch {op}")
             if op > ow:
                 assert (got[:, ow:] == 7).all(), f"{k}: wrote past the row (pitch {op})"
+
+
+def test_ablation_kernels_bit_exact(S, oracle, monkeypatch):
+    """The dense-correlation ablation kernel (SOBEL5_DENSE=1, no operator
+    transformation) gives the same planes and u8 map as the oracle."""
+    monkeypatch.setenv("SOBEL5_DENSE", "1")
+    rng = np.random.default_rng(17)
+    for w, h, mask in ((517, 61, 0xFF), (130, 33, 0x07), (5, 5, 0xFF)):
+        img = (rng.integers(0, 256, (h, w), dtype=np.uint8) & mask).astype(np.uint8)
+        st, ref, _ = oracle.run_stream(img)
+        got, _ = run_device(S, img, S.make_stream_taps(), 1, PLANES)
+        for k in PLANES:
+            np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
+        got, _ = run_device(S, img, S.make_stream_taps(), 1, ("u8",))
+        np.testing.assert_array_equal(got["u8"], oracle.clamp_abs(ref["g"]))
