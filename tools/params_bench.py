@@ -14,7 +14,7 @@ for i in range(6):
 names = ("gx", "gy", "gd", "gdt", "g")
 out, op = api.alloc_planes(w - 4, h - 4, names)
 ref = {}
-for prm in [(2, 3, 5, 7), (1, 1, 1, 1), (3, 2, 7, 5), (1, 4, 9, 9), (2, 5, 11, 13)]:
+for prm in [tuple(int(v) for v in x.split(',')) for x in os.environ.get('PARAMS', '2,3,5,7;1,1,1,1;3,2,7,5;1,4,9,9;2,5,11,13').split(';')]:
     taps = api.make_stream_taps(api.FilterParams(*prm))
     for gen in ("0", "1"):
         os.environ["SOBEL5_GENERIC"] = gen
