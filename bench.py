@@ -61,6 +61,8 @@ def parse():
                     help="32k-bands halo transport")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time the K steps as a Python launch loop instead of one CUDA graph")
     ap.add_argument("--share-gpu", action="store_true",
                     help="testing only: every rank uses cuda:0 and gloo (exercises the N>1 "
                          "code path on a one-GPU box; numbers are not scaling numbers)")
@@ -287,8 +289,8 @@ def main():
         px_job = w * h
         rank_in_px, rank_out_px = w * plan.body_rows, ow * plan.out_rows
 
-        def step(i):
-            part.run(taps, out, op, a.prefetch, stream=s_ptr)
+        def step(i, sp=s_ptr):
+            part.run(taps, out, op, a.prefetch, stream=sp)
     else:
         # Inputs: rotate over enough frames that the input set exceeds L2
         # (126 MB); the outputs alone (24 B/px) are 6x L2 at 8K.
@@ -307,13 +309,13 @@ def main():
         px_job = w * h * frames * world
         rank_in_px, rank_out_px = w * h * frames, ow * oh * frames
 
-        def step(i):
+        def step(i, sp=s_ptr):
             d = ins[i % n_in]
             if frames > 1:
                 api.launch_batch(d, pitch, h * pitch, w, h, frames, taps, a.prefetch, out, op,
-                                 oh * op, stream=s_ptr)
+                                 oh * op, stream=sp)
             else:
-                api.launch(d, pitch, w, h, taps, a.prefetch, out, op, stream=s_ptr)
+                api.launch(d, pitch, w, h, taps, a.prefetch, out, op, stream=sp)
     torch.cuda.synchronize()
 
     for i in range(a.warmup):
@@ -322,17 +324,42 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # The K timed steps run as ONE CUDA graph (captured after the warm-up):
+    # the device time of the steps without Python's per-launch host cost
+    # between them, as a production loop over frames would issue them.
+    # Host-synchronising transports (nccl / gloo halos) run as a plain loop.
+    use_graph = not a.no_graph and not (a.workload == "32k-bands" and a.transport != "peer"
+                                        and world > 1)
+    run_stream_obj = stream  # CUDAGraph.replay() launches on the current stream
+    if use_graph:
+        gs = torch.cuda.Stream(dev)
+        gs.wait_stream(stream)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        n0 = api.launch_count()
+        with torch.cuda.graph(graph, stream=gs):
+            for i in range(a.steps):
+                step(i, gs.cuda_stream)
+        launches_per_replay = api.launch_count() - n0
+        graph.replay()  # one untimed replay (graph upload); replays run on `stream`
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     clocks = ClockSampler(local)
     launches0 = api.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks.start()
-    e0.record(stream)
-    for i in range(a.steps):
-        step(i)
-    e1.record(stream)
+    e0.record(run_stream_obj)
+    if use_graph:
+        graph.replay()
+    else:
+        for i in range(a.steps):
+            step(i)
+    e1.record(run_stream_obj)
     torch.cuda.synchronize()
     clocks.stop()
-    launches = api.launch_count() - launches0
+    launches = launches_per_replay if use_graph else api.launch_count() - launches0
     ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms], device="cpu" if a.share_gpu else dev, dtype=torch.float64)
@@ -365,18 +392,27 @@ def main():
         scratch = api.alloc_scratch(1, dev, out_h=h, pitch=api.round_up(w, 32))
 
         def variant(name, planes_names_v, out_w_v, out_h_v, out_bytes_px, call, passes=1):
+            # timed like the headline: 50 calls captured in one CUDA graph
             vo, vp = api.alloc_planes(out_w_v, out_h_v, planes_names_v, dev)
             for i in range(5):
-                call(ins[i % n_in], vo, vp)
+                call(ins[i % n_in], vo, vp, s_ptr)
+            torch.cuda.synchronize()
+            n = 50
+            vs = torch.cuda.Stream(dev)
+            vs.wait_stream(stream)
+            vg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(vg, stream=vs):
+                for i in range(n):
+                    call(ins[i % n_in], vo, vp, vs.cuda_stream)
+            vg.replay()
             torch.cuda.synchronize()
             v0, v1 = torch.cuda.Event(True), torch.cuda.Event(True)
-            v0.record(stream)
-            n = 50
-            for i in range(n):
-                call(ins[i % n_in], vo, vp)
+            v0.record(stream)  # replay() launches on the current stream
+            vg.replay()
             v1.record(stream)
             torch.cuda.synchronize()
             vms = v0.elapsed_time(v1) / n
+            del vg
             vb = w * h + out_w_v * out_h_v * out_bytes_px
             variants[name] = {"gpx_s": w * h / vms / 1e6, "us": vms * 1e3,
                               "hbm_gbs": vb / vms / 1e6, "frac": vb / vms / 1e6 / hbm_peak,
@@ -388,21 +424,21 @@ def main():
             if contract == a.contract and pf == a.prefetch:
                 continue
             variant(name, CONTRACT_PLANES[contract], ow, oh, OUT_BYTES[contract],
-                    lambda d, vo, vp, pf=pf: api.launch(d, pitch, w, h, taps, pf, vo, vp,
-                                                        stream=s_ptr))
+                    lambda d, vo, vp, sp, pf=pf: api.launch(d, pitch, w, h, taps, pf, vo, vp,
+                                                        stream=sp))
         # detect path: replicate padding fused, same-size
         # u8 edge map; normalize = 2 stencil passes + threshold table
         variant("detect_pad_clamp_abs", ("u8",), w, h, 1,
-                lambda d, vo, vp: api.detect_device(d, pitch, w, h, taps, 1, True,
+                lambda d, vo, vp, sp: api.detect_device(d, pitch, w, h, taps, 1, True,
                                                     api.SaveMode.clamp_abs, vo, vp, scratch,
-                                                    stream=s_ptr))
+                                                    stream=sp))
         variant("detect_pad_normalize", ("u8",), w, h, 1,
-                lambda d, vo, vp: api.detect_device(d, pitch, w, h, taps, 1, True,
+                lambda d, vo, vp, sp: api.detect_device(d, pitch, w, h, taps, 1, True,
                                                     api.SaveMode.normalize, vo, vp, scratch,
-                                                    stream=s_ptr), passes=2)
+                                                    stream=sp), passes=2)
         variant("sr_pad", CONTRACT_PLANES["sr"], w, h, OUT_BYTES["sr"],
-                lambda d, vo, vp: api.launch_ex(d, pitch, w, h, taps, 1, True, vo, vp,
-                                                stream=s_ptr))
+                lambda d, vo, vp, sp: api.launch_ex(d, pitch, w, h, taps, 1, True, vo, vp,
+                                                stream=sp))
         # non-default FilterParams: (1,1,1,1) fits the int16 lanes (packed
         # kernel, runtime taps), (2,3,5,7) the FP32 lanes (f32x2 kernel),
         # (1,32768,1,1) neither (generic 32-bit kernel)
@@ -410,14 +446,14 @@ def main():
             tp = api.make_stream_taps(api.FilterParams(*prm))
             name = "sr_params_" + "_".join(map(str, prm))
             variant(name, CONTRACT_PLANES["sr"], ow, oh, OUT_BYTES["sr"],
-                    lambda d, vo, vp, tp=tp: api.launch(d, pitch, w, h, tp, 1, vo, vp,
-                                                        stream=s_ptr))
+                    lambda d, vo, vp, sp, tp=tp: api.launch(d, pitch, w, h, tp, 1, vo, vp,
+                                                        stream=sp))
             variants[name]["kernel"] = api.kernel_for(tp)
         # 3x3 operator: Stream3Result gx+gy (int32) + g (f64)
         variant("sobel3_sr", ("gx", "gy", "g"), w - 2, h - 2, 16,
-                lambda d, vo, vp: api.launch3(d, pitch, w, h, 1, False, vo, vp, stream=s_ptr))
+                lambda d, vo, vp, sp: api.launch3(d, pitch, w, h, 1, False, vo, vp, stream=sp))
         variant("sobel3_u8", ("u8",), w - 2, h - 2, 1,
-                lambda d, vo, vp: api.launch3(d, pitch, w, h, 1, False, vo, vp, stream=s_ptr))
+                lambda d, vo, vp, sp: api.launch3(d, pitch, w, h, 1, False, vo, vp, stream=sp))
         torch.cuda.empty_cache()
 
     # ---- e2e through the C ABI host entry with pinned buffers ----
@@ -491,6 +527,8 @@ def main():
             "config": {"workload": wl["name"], "frames_per_rank": frames,
                        "contract": a.contract + " (" + "+".join(planes_names) + ")",
                        "prefetch": bool(a.prefetch),
+                       "timed_as": ("one CUDA graph of the K steps (captured after warm-up)"
+                                    if use_graph else "Python launch loop"),
                        "parallelism": (f"row-bands x{world} ({a.transport} halos)"
                                        if a.workload == "32k-bands" else f"batch-split x{world}"),
                        "l2": f"inputs rotated over {n_in} buffers ({n_in * in_bytes / 1e6:.0f} MB)"
