@@ -299,8 +299,25 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     kp.width = width;
     kp.out_w = out_w;
     kp.out_h = out_h;
-    kp.band = choose_band(out_w, out_h, frames,
-                          !(out->gx || out->gy || out->gd || out->gdt || out->g || out->g32));
+    const bool wide = out->gx || out->gy || out->gd || out->gdt || out->g || out->g32;
+    kp.band = choose_band(out_w, out_h, frames, !wide);
+    // Write-bound contracts of the default-taps kernel on plain images: the
+    // CTA's band rows come in by TMA bulk copies (kGeomPlainTma), with 8-row
+    // bands (8K SR: 142.2 us register ring, band 16 -> 137.1 us TMA, band 8;
+    // the u8-only contract is 8% slower with TMA and keeps the ring;
+    // profiles/r1/tma_load.txt).  SOBEL5_TMA_LOAD=0 disables it.
+    kp.tma_load = (prefetch && !ex.pad && !top && !bot && wide && taps_are_default(*taps) &&
+                   env_int("SOBEL5_TMA_LOAD", 1) != 0 && env_int("SOBEL5_GENERIC", 0) == 0 &&
+                   env_int("SOBEL5_DENSE", 0) == 0 && !(ex.u8_norm || ex.norm))
+                      ? 1
+                      : 0;
+    if (kp.tma_load && env_int("SOBEL5_BAND", 0) <= 0) {
+        const int64_t cols = (out_w + kCtaCols - 1) / kCtaCols;
+        int band = 8;
+        while (band > 4 && cols * frames * ((out_h + band - 1) / band) < 148 * 4) band /= 2;
+        kp.band = band;
+    }
+    if (kp.band > 32) kp.tma_load = 0;  // the shared-memory band holds 36 rows
     kp.gx = out->gx;
     kp.gy = out->gy;
     kp.gd = out->gd;
@@ -325,6 +342,7 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     if (grid.y > 65535u) {
         // very tall images: grow the band until the grid fits
         kp.band = (out_h + 65534) / 65535;
+        if (kp.band > 32) kp.tma_load = 0;  // the shared-memory band holds 36 rows
     }
     const dim3 grid2(grid.x, static_cast<unsigned>((out_h + kp.band - 1) / kp.band), grid.z);
     const cudaError_t e = dispatch(kp, grid2, prefetch, taps_are_default(*taps), choose_mag(*taps),

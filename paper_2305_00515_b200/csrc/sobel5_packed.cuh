@@ -120,6 +120,34 @@ __device__ __forceinline__ void u8_from_sf2(float2 S, uint32_t& a, uint32_t& b) 
     b = u8_from_sf(y.y);
 }
 
+// ---- TMA bulk loads (cp.async.bulk shared <- global, mbarrier completion) --
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra W;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(sdst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
 // ---- TMA bulk stores (cp.async.bulk global <- shared, bulk-group completion)
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
@@ -188,6 +216,13 @@ __global__ void __launch_bounds__(kCtaThreads,
     sobel5_packed_default_kernel(const __grid_constant__ KernelParams p) {
     constexpr bool SEG = GEOM == kGeomSeg;
     constexpr bool PAD = GEOM == kGeomPad;
+    // TMAL: the CTA's band (n_in rows x its 512 + 16 columns) is bulk-copied
+    // into shared memory at the start, rows 0..4 and 5..n_in-1 on two
+    // mbarriers, and the prefetch ring reads rows from there (band <= 32)
+    constexpr bool TMAL = GEOM == kGeomPlainTma;
+    constexpr int kTmaRowBytes = kCtaCols + 16, kTmaRows = 36;
+    __shared__ __align__(128) uint8_t s_band[TMAL ? kTmaRows * kTmaRowBytes : 16];
+    __shared__ __align__(8) uint64_t s_bar[2];
     // which planes this instantiation writes (compile-time unless kOutRuntime)
     constexpr bool RT = OUTS == kOutRuntime;
     const bool w_gx = RT ? p.gx != nullptr : (OUTS & kOutGx) != 0;
@@ -245,6 +280,34 @@ __global__ void __launch_bounds__(kCtaThreads,
             __syncthreads();
         }
     }
+    if constexpr (TMAL) {
+        if (threadIdx.x == 0) {
+            mbar_init(&s_bar[0], 1);
+            mbar_init(&s_bar[1], 1);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        __syncthreads();  // barrier init visible before anyone waits
+        if (threadIdx.x < 32) {  // warp 0: one lane per row issues its bulk copy
+            const int b_oy0 = blockIdx.y * p.band;
+            const int b_in = min(p.band, p.out_h - b_oy0) + 4;
+            const int n0 = min(5, b_in);
+            const int cta_x0 = blockIdx.x * kCtaCols;
+            // 16-B multiple inside the row (pitch is a multiple of 16 >= width)
+            const uint32_t rb = static_cast<uint32_t>(
+                min(kTmaRowBytes, ((p.width + 15) & ~15) - cta_x0));
+            if (threadIdx.x == 0) {
+                mbar_expect_tx(&s_bar[0], rb * n0);
+                mbar_expect_tx(&s_bar[1], rb * (b_in - n0));
+            }
+            __syncwarp();
+            const int r = threadIdx.x;
+            if (r < b_in)
+                bulk_load(s_band + r * kTmaRowBytes,
+                          p.mid + static_cast<int64_t>(blockIdx.z) * p.in_frame_stride +
+                              static_cast<int64_t>(b_oy0 + r) * p.in_pitch + cta_x0,
+                          rb, &s_bar[r < n0 ? 0 : 1]);
+        }
+    }
     if (warp_x0 >= p.out_w) return;  // whole warp right of the image
     const int oy0 = blockIdx.y * p.band;
     const int n_out = min(p.band, p.out_h - oy0);
@@ -297,6 +360,14 @@ __global__ void __launch_bounds__(kCtaThreads,
         return p.mid + in_frame + static_cast<int64_t>(y) * p.in_pitch + x0;
     };
     auto load_row = [&](int r, uint32_t& a, uint32_t& b) {
+        if constexpr (TMAL) {
+            if (r == 0) mbar_wait(&s_bar[0], 0);
+            if (r == 5) mbar_wait(&s_bar[1], 0);
+            const uint8_t* sr = s_band + r * kTmaRowBytes + (x0 - static_cast<int>(blockIdx.x) * kCtaCols);
+            a = load_a ? *reinterpret_cast<const uint32_t*>(sr) : 0u;
+            b = load_b ? *reinterpret_cast<const uint32_t*>(sr + 4) : 0u;
+            return;
+        }
         const uint8_t* rp;
         if (!SEG && !PAD) {
             rp = plain;

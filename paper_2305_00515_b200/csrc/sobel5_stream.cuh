@@ -83,6 +83,7 @@ struct KernelParams {
     uint32_t* s32;               // exact integer g^2 (normalize pass 1 of the detect path)
     // taps (kernel parameter space -> constant-bank operands)
     int32_t f[5], h[5], k0[5], k1[5], gx_v[5], gy_v[5], gdm_f[5], gdm_d[5];
+    int tma_load;  // packed plain kernel: band rows bulk-copied into shared memory
     // the same taps as floats for the packed-FP32 kernel (sobel5_f32x2.cuh):
     // f, h, k0, k1, gx_v, gy_v, gdm_f, -gdm_d
     float tf[8][5];
@@ -186,6 +187,7 @@ enum Geom : int {
     kGeomPlain = 0,  // valid mode over one (or a batch of) plain image(s)
     kGeomSeg = 1,    // valid mode over a stacked [top halo; band; bottom halo]
     kGeomPad = 2,    // pad_replicate(img, 2) fused: same-size output (image_io.hpp:279-291)
+    kGeomPlainTma = 3,  // plain, the CTA's band rows bulk-copied (TMA) into shared memory
 };
 
 // The 8-byte window (wa = input columns c..c+3, wb = c+4..c+7) a lane needs
