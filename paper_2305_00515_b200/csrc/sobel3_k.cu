@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "sobel3_packed.cuh"
@@ -18,7 +19,10 @@ constexpr int kOut3 = kOutGx | kOutGy | kOutG;  // Stream3Result
 
 template <int PF, bool PAD, int OUTS>
 cudaError_t go(const KernelParams& kp, dim3 grid, cudaStream_t s) {
-    sobel3_packed_kernel<PF, PAD, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
+    if (PF > 0 && !PAD && kp.tma_load)  // band rows by TMA (sobel3_common decides)
+        sobel3_packed_kernel<PF, PAD, OUTS, true><<<grid, kCtaThreads, 0, s>>>(kp);
+    else
+        sobel3_packed_kernel<PF, PAD, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
     return cudaGetLastError();
 }
 
@@ -78,11 +82,24 @@ sobel5_status sobel3_common(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
     kp.norm = ex.norm;
     kp.u8_norm = ex.u8_norm;
     kp.s32 = ex.s32;
+    // the write-bound Stream3Result contract reads its band rows by TMA with
+    // 8-row bands, as the 5x5 kernel does (SOBEL5_TMA_LOAD=0 disables it)
+    const bool wide = out->gx || out->gy || out->g || out->g32;
+    const char* tv = std::getenv("SOBEL5_TMA_LOAD");
+    const char* bv = std::getenv("SOBEL5_BAND");
+    kp.tma_load = (prefetch && !ex.pad && wide && !ex.norm && !(tv && *tv && std::atoi(tv) == 0)) ? 1 : 0;
+    if (kp.tma_load && !(bv && *bv && std::atoi(bv) > 0)) {
+        const int64_t cols = (out_w + kCtaCols - 1) / kCtaCols;
+        int band = 8;
+        while (band > 4 && cols * frames * ((out_h + band - 1) / band) < 148 * 4) band /= 2;
+        kp.band = band;
+    }
     unsigned gy = static_cast<unsigned>((out_h + kp.band - 1) / kp.band);
     if (gy > 65535u) {
         kp.band = (out_h + 65534) / 65535;
         gy = static_cast<unsigned>((out_h + kp.band - 1) / kp.band);
     }
+    if (kp.band > 32) kp.tma_load = 0;  // the shared-memory band holds 34 rows
     const dim3 grid(static_cast<unsigned>((out_w + kCtaCols - 1) / kCtaCols), gy,
                     static_cast<unsigned>(frames));
     count_launch();

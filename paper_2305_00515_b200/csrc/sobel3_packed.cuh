@@ -23,9 +23,41 @@ namespace sobel5_b200 {
 
 // PF: 0 = load each row when consumed (Prefetch::off), 1 = 6-row register
 // prefetch ring (Prefetch::on).  PAD: pad_replicate(img, 1) fused.
-template <int PF, bool PAD, int OUTS>
+// TMAL: the CTA's band rows bulk-copied into shared memory at the start (as
+// kGeomPlainTma of the 5x5 kernel; valid mode, prefetch on, band <= 32).
+template <int PF, bool PAD, int OUTS, bool TMAL = false>
 __global__ void __launch_bounds__(kCtaThreads, OUTS == kOutU8 ? SOBEL5_U8_MIN_CTAS : kMinCtasPerSm)
     sobel3_packed_kernel(const __grid_constant__ KernelParams p) {
+    constexpr int kTmaRowBytes = kCtaCols + 16, kTmaRows = 34;
+    __shared__ __align__(128) uint8_t s_band[TMAL ? kTmaRows * kTmaRowBytes : 16];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    if constexpr (TMAL) {
+        if (threadIdx.x == 0) {
+            mbar_init(&s_bar[0], 1);
+            mbar_init(&s_bar[1], 1);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // warp 0: one lane per row issues its bulk copy
+            const int b_oy0 = blockIdx.y * p.band;
+            const int b_in = min(p.band, p.out_h - b_oy0) + 2;
+            const int n0 = min(6, b_in);
+            const int cta_x0 = blockIdx.x * kCtaCols;
+            const uint32_t rb = static_cast<uint32_t>(
+                min(kTmaRowBytes, ((p.width + 15) & ~15) - cta_x0));
+            if (threadIdx.x == 0) {
+                mbar_expect_tx(&s_bar[0], rb * n0);
+                mbar_expect_tx(&s_bar[1], rb * (b_in - n0));
+            }
+            __syncwarp();
+            const int r = threadIdx.x;
+            if (r < b_in)
+                bulk_load(s_band + r * kTmaRowBytes,
+                          p.mid + static_cast<int64_t>(blockIdx.z) * p.in_frame_stride +
+                              static_cast<int64_t>(b_oy0 + r) * p.in_pitch + cta_x0,
+                          rb, &s_bar[r < n0 ? 0 : 1]);
+        }
+    }
     constexpr bool RT = OUTS == kOutRuntime;
     const bool w_gx = RT ? p.gx != nullptr : (OUTS & kOutGx) != 0;
     const bool w_gy = RT ? p.gy != nullptr : (OUTS & kOutGy) != 0;
@@ -69,6 +101,14 @@ __global__ void __launch_bounds__(kCtaThreads, OUTS == kOutU8 ? SOBEL5_U8_MIN_CT
     // of pad_replicate(img, 1) (image_io.hpp:285)
     const uint8_t* plain = p.mid + in_frame + static_cast<int64_t>(oy0) * p.in_pitch + x0;
     auto load_row = [&](int r, uint32_t& a, uint32_t& b) {
+        if constexpr (TMAL) {
+            if (r == 0) mbar_wait(&s_bar[0], 0);
+            if (r == 6) mbar_wait(&s_bar[1], 0);
+            const uint8_t* sr = s_band + r * kTmaRowBytes + (x0 - static_cast<int>(blockIdx.x) * kCtaCols);
+            a = load_a ? *reinterpret_cast<const uint32_t*>(sr) : 0u;
+            b = load_b ? *reinterpret_cast<const uint32_t*>(sr + 4) : 0u;
+            return;
+        }
         const uint8_t* rp;
         if (PAD) {
             const int y = min(max(oy0 + r - 1, 0), p.mid_rows - 1);
