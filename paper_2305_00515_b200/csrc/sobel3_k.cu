@@ -89,10 +89,9 @@ sobel5_status sobel3_common(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
     const char* bv = std::getenv("SOBEL5_BAND");
     kp.tma_load = (prefetch && !ex.pad && wide && !ex.norm && !(tv && *tv && std::atoi(tv) == 0)) ? 1 : 0;
     if (kp.tma_load && !(bv && *bv && std::atoi(bv) > 0)) {
-        const int64_t cols = (out_w + kCtaCols - 1) / kCtaCols;
-        int band = 8;
-        while (band > 4 && cols * frames * ((out_h + band - 1) / band) < 148 * 4) band /= 2;
-        kp.band = band;
+        const int64_t cols = (out_w + kCtaCols - 1) / kCtaCols;  // many waves only
+        if (cols * frames * ((out_h + 7) / 8) >= 148 * 4 * 8) kp.band = 8;
+        else kp.tma_load = 0;
     }
     unsigned gy = static_cast<unsigned>((out_h + kp.band - 1) / kp.band);
     if (gy > 65535u) {

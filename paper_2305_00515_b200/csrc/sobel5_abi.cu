@@ -313,10 +313,12 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
                       ? 1
                       : 0;
     if (kp.tma_load && env_int("SOBEL5_BAND", 0) <= 0) {
+        // worth it with many waves of 8-row CTAs (8K: 8100 CTAs); a 4K image
+        // (2160) is faster on the register ring with 16-row bands
+        // (39.3 vs 41.3 us, profiles/r1/tma_load.txt)
         const int64_t cols = (out_w + kCtaCols - 1) / kCtaCols;
-        int band = 8;
-        while (band > 4 && cols * frames * ((out_h + band - 1) / band) < 148 * 4) band /= 2;
-        kp.band = band;
+        if (cols * frames * ((out_h + 7) / 8) >= 148 * 4 * 8) kp.band = 8;
+        else kp.tma_load = 0;
     }
     if (kp.band > 32) kp.tma_load = 0;  // the shared-memory band holds 36 rows
     kp.gx = out->gx;
