@@ -50,8 +50,7 @@ __global__ void __launch_bounds__(kCtaThreads, OUTS == kOutU8 ? SOBEL5_U8_MIN_CT
                 mbar_expect_tx(&s_bar[1], rb * (b_in - n0));
             }
             __syncwarp();
-            const int r = threadIdx.x;
-            if (r < b_in)
+            for (int r = threadIdx.x; r < b_in; r += 32)  // bands up to kTmaRows - 2
                 bulk_load(s_band + r * kTmaRowBytes,
                           p.mid + static_cast<int64_t>(blockIdx.z) * p.in_frame_stride +
                               static_cast<int64_t>(b_oy0 + r) * p.in_pitch + cta_x0,

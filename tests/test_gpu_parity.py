@@ -310,3 +310,30 @@ def test_ablation_kernels_bit_exact(S, oracle, monkeypatch):
             np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
         got, _ = run_device(S, img, S.make_stream_taps(), 1, ("u8",))
         np.testing.assert_array_equal(got["u8"], oracle.clamp_abs(ref["g"]))
+
+
+@pytest.mark.parametrize("band", ["8", "16", "32"])
+def test_tma_band_loads_any_band(S, oracle, monkeypatch, band):
+    """TMA band loads (kGeomPlainTma) with forced bands up to the 36-row
+    shared-memory limit: more band rows than warp-0 lanes must all be issued
+    (bulk copies loop over the rows), ragged last band, batch frames."""
+    import torch
+    from paper_2305_00515_b200 import api
+    monkeypatch.setenv("SOBEL5_BAND", band)
+    rng = np.random.default_rng(int(band))
+    for w, h, n in ((1541, 77, 1), (600, 45, 3)):
+        imgs = rng.integers(0, 256, (n, h, w), dtype=np.uint8)
+        d_in, pitch = api.alloc_input(w, h, frames=n)
+        d_in.view(n, h, pitch)[:, :, :w].copy_(torch.from_numpy(imgs))
+        out, op = api.alloc_planes(w - 4, h - 4, PLANES, frames=n)
+        if n > 1:
+            api.launch_batch(d_in, pitch, h * pitch, w, h, n, S.make_stream_taps(), 1, out, op,
+                             (h - 4) * op)
+        else:
+            api.launch(d_in, pitch, w, h, S.make_stream_taps(), 1, out, op)
+        torch.cuda.synchronize()
+        for f in range(n):
+            st, ref, _ = oracle.run_stream(imgs[f])
+            for k in PLANES:
+                got = out[k].view(n, h - 4, op)[f, :, : w - 4].cpu().numpy()
+                np.testing.assert_array_equal(got, ref[k], err_msg=f"band {band} {k} frame {f}")
