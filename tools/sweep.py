@@ -7,8 +7,8 @@ from paper_2305_00515_b200 import api
 w, h = int(os.environ.get("W", 7680)), int(os.environ.get("H", 4320))
 contract = os.environ.get("CONTRACT", "sr")
 planes_names = {"sr": ("gx", "gy", "gd", "gdt", "g"), "u8": ("u8",), "int": ("gx", "gy", "gd", "gdt"),
-                "sr3": ("gx", "gy", "g")}[contract]
-outb = {"sr": 24, "u8": 1, "int": 16, "sr3": 16}[contract]
+                "sr3": ("gx", "gy", "g"), "sr32": ("gx", "gy", "gd", "gdt", "g32")}[contract]
+outb = {"sr": 24, "u8": 1, "int": 16, "sr3": 16, "sr32": 20}[contract]
 taps = api.make_stream_taps()
 ins = []
 for i in range(6):
