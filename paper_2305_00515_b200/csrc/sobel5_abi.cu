@@ -308,7 +308,8 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     // contract 8% slower: both keep the ring, and so
     // does the runtime-taps packed kernel (171 vs 150 us at 8-row bands);
     // profiles/r1/tma_load.txt).  SOBEL5_TMA_LOAD=0 disables it.
-    kp.tma_load = (prefetch && !ex.pad && !top && !bot && out->g && taps_are_default(*taps) &&
+    kp.tma_load = (prefetch && (!ex.pad || env_int("SOBEL5_TMA_PAD", 1) != 0) && !top && !bot &&
+                   out->g && taps_are_default(*taps) &&
                    env_int("SOBEL5_TMA_LOAD", 1) != 0 && env_int("SOBEL5_GENERIC", 0) == 0 &&
                    env_int("SOBEL5_DENSE", 0) == 0 && !(ex.u8_norm || ex.norm))
                       ? 1

@@ -215,12 +215,15 @@ __global__ void __launch_bounds__(kCtaThreads,
                                   (OUTS == kOutU8 && !RTAPS) ? SOBEL5_U8_MIN_CTAS : kMinCtasPerSm)
     sobel5_packed_default_kernel(const __grid_constant__ KernelParams p) {
     constexpr bool SEG = GEOM == kGeomSeg;
-    constexpr bool PAD = GEOM == kGeomPad;
+    constexpr bool PAD = GEOM == kGeomPad || GEOM == kGeomPadTma;
     // TMAL: the CTA's band (n_in rows x its 512 + 16 columns) is bulk-copied
     // into shared memory at the start, rows 0..4 and 5..n_in-1 on two
     // mbarriers, and the prefetch ring reads rows from there (band <= 32)
-    constexpr bool TMAL = GEOM == kGeomPlainTma;
-    constexpr int kTmaRowBytes = kCtaCols + 16, kTmaRows = 36;
+    constexpr bool TMAL = GEOM == kGeomPlainTma || GEOM == kGeomPadTma;
+    // row layout: PAD keeps 16 bytes left of the CTA's first column (lane 0's
+    // left word) at offset 0, so a row holds columns [x0 - 16, x0 + 528)
+    constexpr int kTmaLead = PAD ? 16 : 0;
+    constexpr int kTmaRowBytes = kCtaCols + 16 + kTmaLead, kTmaRows = 36;
     __shared__ __align__(128) uint8_t s_band[TMAL ? kTmaRows * kTmaRowBytes : 16];
     __shared__ __align__(8) uint64_t s_bar[2];
     // which planes this instantiation writes (compile-time unless kOutRuntime)
@@ -292,19 +295,26 @@ __global__ void __launch_bounds__(kCtaThreads,
             const int b_in = min(p.band, p.out_h - b_oy0) + 4;
             const int n0 = min(5, b_in);
             const int cta_x0 = blockIdx.x * kCtaCols;
-            // 16-B multiple inside the row (pitch is a multiple of 16 >= width)
+            // source columns [src_x, ...): 16-B aligned, inside the row (pitch
+            // is a multiple of 16 >= width); PAD starts 16 columns early
+            // except at the left image edge
+            const int src_x = max(cta_x0 - kTmaLead, 0);
+            const int dst_off = src_x - (cta_x0 - kTmaLead);
             const uint32_t rb = static_cast<uint32_t>(
-                min(kTmaRowBytes, ((p.width + 15) & ~15) - cta_x0));
+                min(kTmaRowBytes - dst_off, ((p.width + 15) & ~15) - src_x));
             if (threadIdx.x == 0) {
                 mbar_expect_tx(&s_bar[0], rb * n0);
                 mbar_expect_tx(&s_bar[1], rb * (b_in - n0));
             }
             __syncwarp();
-            for (int r = threadIdx.x; r < b_in; r += 32)  // bands up to kTmaRows - 4
-                bulk_load(s_band + r * kTmaRowBytes,
+            for (int r = threadIdx.x; r < b_in; r += 32) {  // bands up to kTmaRows - 4
+                // PAD: padded row b_oy0 + r is image row clamp(b_oy0 + r - 2)
+                const int y = PAD ? min(max(b_oy0 + r - 2, 0), p.mid_rows - 1) : b_oy0 + r;
+                bulk_load(s_band + r * kTmaRowBytes + dst_off,
                           p.mid + static_cast<int64_t>(blockIdx.z) * p.in_frame_stride +
-                              static_cast<int64_t>(b_oy0 + r) * p.in_pitch + cta_x0,
+                              static_cast<int64_t>(y) * p.in_pitch + src_x,
                           rb, &s_bar[r < n0 ? 0 : 1]);
+            }
         }
     }
     if (warp_x0 >= p.out_w) return;  // whole warp right of the image
@@ -362,9 +372,10 @@ __global__ void __launch_bounds__(kCtaThreads,
         if constexpr (TMAL) {
             if (r == 0) mbar_wait(&s_bar[0], 0);
             if (r == 5) mbar_wait(&s_bar[1], 0);
-            const uint8_t* sr = s_band + r * kTmaRowBytes + (x0 - static_cast<int>(blockIdx.x) * kCtaCols);
+            const uint8_t* sr =
+                s_band + r * kTmaRowBytes + kTmaLead + (x0 - static_cast<int>(blockIdx.x) * kCtaCols);
             a = load_a ? *reinterpret_cast<const uint32_t*>(sr) : 0u;
-            b = load_b ? *reinterpret_cast<const uint32_t*>(sr + 4) : 0u;
+            b = load_b ? *reinterpret_cast<const uint32_t*>(sr + xoff) : 0u;
             return;
         }
         const uint8_t* rp;

@@ -292,3 +292,20 @@ def test_fault_injected_runtime_packed(api, oracle):
     api.launch(d, pitch, 70, 40, taps, 1, out, op, diag)
     torch.cuda.synchronize()
     assert diag[0].item() > 0
+
+
+@pytest.mark.parametrize("band", ["8", "32"])
+@pytest.mark.parametrize("h,w", [(77, 1541), (9, 129), (40, 515), (3, 600)])
+def test_pad_tma_band_loads(api, oracle, monkeypatch, h, w, band):
+    """Replicate padding with the TMA band loads (kGeomPadTma, forced by
+    SOBEL5_BAND): clamped rows, the left 16-byte lead, right-edge patching."""
+    import torch
+    monkeypatch.setenv("SOBEL5_BAND", band)
+    img = rand_img(h, w, 3 * w + h)
+    d, pitch = to_dev(api, img)
+    out, op = api.alloc_planes(w, h, SR)
+    api.launch_ex(d, pitch, w, h, api.make_stream_taps(), 1, True, out, op)
+    torch.cuda.synchronize()
+    ref = padded_ref(oracle, img)
+    for k in SR:
+        np.testing.assert_array_equal(out[k][:, :w].cpu().numpy(), ref[k], err_msg=f"{k} band {band}")
