@@ -5,7 +5,9 @@
                     [--workload 8k|1080p-batch|32k-bands] [--contract sr|u8|sr32]
 
 One "step" = one pass of the hot path over one synthetic image (or batch):
-the fused sm_100a kernel over an input already resident in HBM.  Default
+the fused sm_100a kernel over an input already resident in HBM; the K timed
+steps are captured after the warm-up as one CUDA graph and replayed once
+(--no-graph: a Python launch loop).  Default
 workload is BASELINE config C3, 7680x4320 uint8 (the north-star roofline
 case); at N>1 every rank processes its own frame (weak scaling, no
 communication: the batch-split sharding of SURVEY.md section 8e).
@@ -540,8 +542,10 @@ def main():
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
                          if peak_kind == "measured" else "fallback (B200_PROFILING.md)",
                          "alg_bytes_per_launch": alg_bytes,
-                         "kernel": "sobel5_packed_default_kernel" if taps_default
-                         else "sobel5_stream_kernel",
+                         "kernel": ("sobel5_packed_default_kernel" if taps_default
+                                    else "sobel5_stream_kernel")
+                         + (" (TMA band rows, 8-row bands)" if a.contract == "sr" and a.prefetch
+                            and a.workload != "4k" else ""),
                          "kernel_us": ms_step * 1e3},
             "gpu_launches": launches,
             **({"share_gpu": "testing mode: all ranks on cuda:0 over gloo"} if a.share_gpu else {}),
