@@ -545,7 +545,8 @@ def main():
                          "kernel": ("sobel5_packed_default_kernel" if taps_default
                                     else "sobel5_stream_kernel")
                          + (" (TMA band rows, 8-row bands)" if a.contract == "sr" and a.prefetch
-                            and a.workload != "4k" else ""),
+                            and a.workload != "4k" and not (a.workload == "32k-bands" and world > 1)
+                            else ""),
                          "kernel_us": ms_step * 1e3},
             "gpu_launches": launches,
             **({"share_gpu": "testing mode: all ranks on cuda:0 over gloo"} if a.share_gpu else {}),
