@@ -150,6 +150,13 @@ int choose_band_impl(int out_w, int out_h, int frames, bool narrow_only) {
     // at 16 and 64; keep >= ~16 CTAs per SM for the last partial wave.
     int band = 64;
     while (band > 32 && ctas(band) < 148 * 16) band /= 2;
+    // images too small for one wave of CTAs (~5 u8 CTAs per SM): shorter
+    // bands until it is filled (1080p u8: band 32 -> 6, 9.7 -> 6.1 us; 4K:
+    // 32 -> 24, 17.5 -> 16.1 us; profiles/r1/u8_band_sweep.txt)
+    if (ctas(band) < 148 * 5) {
+        const int64_t per_col = (148 * 5 + cols * frames - 1) / (cols * frames);  // bands wanted
+        band = static_cast<int>(std::max<int64_t>(4, (out_h + per_col - 1) / per_col));
+    }
     return band;
 }
 

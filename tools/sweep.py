@@ -32,11 +32,21 @@ for band, pf in itertools.product(bands, pfs):
     for i in range(5):
         go(i)
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-    torch.cuda.synchronize(); e0.record()
     N = 60
-    for i in range(N):
-        go(i)
-    e1.record(); torch.cuda.synchronize()
+    if os.environ.get("GRAPH", "0") == "1":  # device time without Python launch gaps
+        torch.cuda.synchronize()
+        gs = torch.cuda.Stream(); gs.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=gs):
+            for i in range(N):
+                go(i)
+        g.replay(); torch.cuda.synchronize()
+        e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
+    else:
+        torch.cuda.synchronize(); e0.record()
+        for i in range(N):
+            go(i)
+        e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / N
     b = w * h + (w - 4) * (h - 4) * outb
     res[f"{band},{pf}"] = ms * 1e3
