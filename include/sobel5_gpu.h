@@ -233,7 +233,9 @@ sobel5_status sobel5_ipc_export(const void* d_ptr, sobel5_ipc_handle* out);
 sobel5_status sobel5_ipc_import(const sobel5_ipc_handle* h, const void** d_ptr);
 sobel5_status sobel5_ipc_release(const void* d_ptr);
 
-/* Which kernel family serves these taps: 0 packed int16 lanes with the
+/* Mirrors the reference's own path choice for wide taps (make_stream_taps'
+ * wide_vagg flag, pipeline.hpp:94-105, selecting the int64 vagg path).
+ * Which kernel family serves these taps: 0 packed int16 lanes with the
  * default (1, 2, 6, 4) algebra compiled in, 1 packed int16 lanes with
  * runtime taps (every response < 2^15), 2 packed FP32 with runtime taps
  * (every partial sum < 2^22), 3 generic 32-bit wrapping kernel (any taps);
@@ -256,14 +258,18 @@ sobel5_status sobel5_selftest(int which, uint32_t lo, uint32_t hi, uint64_t* d_c
 
 sobel5_status sobel5_ctx_create(sobel5_ctx** out, int device);
 void sobel5_ctx_destroy(sobel5_ctx* ctx);
-/* Releases the context's cached device buffers and pinned host staging
+/* (No reference counterpart: the reference allocates per call,
+ * pipeline.hpp:462-467.)  Releases the context's cached device buffers and
+ * pinned host staging
  * (kept across calls so repeated calls allocate nothing); no-op while a
  * begin/finish pair is pending. */
 void sobel5_ctx_trim(sobel5_ctx* ctx);
 /* Message of the last CUDA error seen by this context ("" if none). */
 const char* sobel5_ctx_last_error(const sobel5_ctx* ctx);
 
-/* Synchronous end-to-end call: host image in (tightly packed W x H), host
+/* Replaces sobel5::run_stream (pipeline.hpp:452-477: validation :454-460,
+ * plane allocation :462-467, strip dispatch :416-445) for host buffers.
+ * Synchronous end-to-end call: host image in (tightly packed W x H), host
  * planes out (tightly packed, pitch == width-4; NULL planes skipped).
  * Copies are chunked by row bands over pinned staging and overlapped with
  * the kernels on the context's streams.  On SOBEL5_PARITY_VIOLATION the
@@ -272,7 +278,8 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
                               const sobel5_taps* taps, int prefetch, const sobel5_planes* h_out,
                               sobel5_diag* diag_out);
 
-/* Split form of sobel5_run_host for callers that allocate their result
+/* Split form of sobel5_run_host (same reference interface, pipeline.hpp:452)
+ * for callers that allocate their result
  * planes while the device works (the C++ run_stream does): _begin enqueues
  * upload, kernels and downloads into the context's pinned staging and
  * returns; _finish waits chunk by chunk and copies the planes selected by
