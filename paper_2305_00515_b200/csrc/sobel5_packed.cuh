@@ -7,7 +7,7 @@
 // homomorphism.  The lanes are recovered exactly at the end,
 //     lo = sext16(V),   hi = (V + 0x8000) >> 16 (arithmetic),
 // provided every EXTRACTED quantity lies in [-2^15, 2^15).  The host proves
-// that bound from the taps before selecting this kernel (choose_kernel in
+// that bound from the taps before selecting this kernel (taps_fit_packed in
 // sobel5_abi.cu); for the default (1, 2, 6, 4) taps the extracted maxima are
 // |gx|, |gy|, |gd|, |gdt| <= 12240 and |P|/2 <= 8925.
 //

@@ -18,11 +18,10 @@ for i in range(6):
 out, op = api.alloc_planes(w - 4, h - 4, planes_names)
 out3, op3 = api.alloc_planes(w - 2, h - 2, planes_names)
 bands = [int(x) for x in os.environ.get("BANDS", "0").split(",")]
-pfs = [int(x) for x in os.environ.get("OCCS", "0").split(",")]  # CTAs per SM (0 = occupancy)
+pfs = [0]  # (the CTAs-per-SM knob of an earlier build no longer exists)
 res = {}
 for band, pf in itertools.product(bands, pfs):
     os.environ["SOBEL5_BAND"] = str(band)
-    os.environ["SOBEL5_CTAS_PER_SM"] = str(pf)
     k3 = os.environ.get("SOBEL3", "0") == "1"  # the 3x3 operator instead
     def go(i):
         if k3:
