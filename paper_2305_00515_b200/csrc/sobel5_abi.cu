@@ -311,12 +311,13 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     // Write-bound contracts of the default-taps kernel on plain images: the
     // CTA's band rows come in by TMA bulk copies (kGeomPlainTma), with 8-row
     // bands (8K SR: 142.2 us register ring, band 16 -> 137.1 us TMA, band 8;
-    // SR32 (float g) is 4% slower with TMA (126.5 vs 121.0 us), the u8-only
-    // contract 8% slower: both keep the ring, and so
+    // with the rows read from shared memory when consumed SR32 gains too
+    // (117.3 vs 119.1 us); the u8-only contract stays 4-8% faster on the
+    // register ring, and so
     // does the runtime-taps packed kernel (171 vs 150 us at 8-row bands);
     // profiles/r1/tma_load.txt).  SOBEL5_TMA_LOAD=0 disables it.
     kp.tma_load = (prefetch && (!ex.pad || env_int("SOBEL5_TMA_PAD", 1) != 0) && !top && !bot &&
-                   out->g && taps_are_default(*taps) &&
+                   (out->g || out->g32) && taps_are_default(*taps) &&
                    env_int("SOBEL5_TMA_LOAD", 1) != 0 && env_int("SOBEL5_GENERIC", 0) == 0 &&
                    env_int("SOBEL5_DENSE", 0) == 0 && !(ex.u8_norm || ex.norm))
                       ? 1
