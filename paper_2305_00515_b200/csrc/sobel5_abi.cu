@@ -330,6 +330,15 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
         if (cols * frames * ((out_h + 7) / 8) >= 148 * 4 * 8) kp.band = 8;
         else kp.tma_load = 0;
     }
+    // The detect path's padded narrow passes (clamp_abs u8 map; normalize
+    // pass 1 = min/max + S plane) read their clamped rows by TMA too, at
+    // their own band: 8K pad clamp_abs 68.4 -> 59.6 us, pad normalize
+    // 113.3 -> 103.1 us (the plain u8 map stays on the register ring:
+    // 53.4 vs 51.1 us; profiles/r1/tma_load.txt).
+    if (!kp.tma_load && ex.pad && prefetch && !wide && env_int("SOBEL5_TMA_LOAD", 1) != 0 &&
+        env_int("SOBEL5_TMA_PAD", 1) != 0 &&
+        ((out->u8 && !(ex.u8_norm || ex.norm)) || (ex.minmax && ex.s32)) && taps_are_default(*taps))
+        kp.tma_load = 1;
     if (kp.band > 32) kp.tma_load = 0;  // the shared-memory band holds 36 rows
     kp.gx = out->gx;
     kp.gy = out->gy;
