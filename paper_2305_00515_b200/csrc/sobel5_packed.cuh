@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(kCtaThreads,
     constexpr bool PAD = GEOM == kGeomPad || GEOM == kGeomPadTma;
     // TMAL: the CTA's band (n_in rows x its 512 + 16 columns) is bulk-copied
     // into shared memory at the start, rows 0..4 and 5..n_in-1 on two
-    // mbarriers, and the prefetch ring reads rows from there (band <= 32)
+    // mbarriers; the launchers instantiate it with PF = 0, so each row is read
+    // from shared memory when it is consumed (band <= 32)
     constexpr bool TMAL = GEOM == kGeomPlainTma || GEOM == kGeomPadTma;
     // row layout: PAD keeps 16 bytes left of the CTA's first column (lane 0's
     // left word) at offset 0, so a row holds columns [x0 - 16, x0 + 528)
