@@ -19,7 +19,7 @@ constexpr int kOut3 = kOutGx | kOutGy | kOutG;  // Stream3Result
 
 template <int PF, bool PAD, int OUTS>
 cudaError_t go(const KernelParams& kp, dim3 grid, cudaStream_t s) {
-    if (PF > 0 && !PAD && kp.tma_load)  // band rows by TMA (sobel3_common decides)
+    if (PF > 0 && kp.tma_load)  // band rows by TMA (sobel3_common decides)
         sobel3_packed_kernel<0, PAD, OUTS, true><<<grid, kCtaThreads, 0, s>>>(kp);
     else
         sobel3_packed_kernel<PF, PAD, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
@@ -87,7 +87,9 @@ sobel5_status sobel3_common(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
     const bool wide = out->gx || out->gy || out->g || out->g32;
     const char* tv = std::getenv("SOBEL5_TMA_LOAD");
     const char* bv = std::getenv("SOBEL5_BAND");
-    kp.tma_load = (prefetch && !ex.pad && wide && !ex.norm && !(tv && *tv && std::atoi(tv) == 0)) ? 1 : 0;
+    const char* tp = std::getenv("SOBEL5_TMA_PAD");
+    const bool tma_on = !(tv && *tv && std::atoi(tv) == 0);
+    kp.tma_load = (prefetch && !ex.pad && wide && !ex.norm && tma_on) ? 1 : 0;
     if (kp.tma_load && !(bv && *bv && std::atoi(bv) > 0)) {
         const int64_t cols = (out_w + kCtaCols - 1) / kCtaCols;  // many waves only
         if (cols * frames * ((out_h + 7) / 8) >= 148 * 4 * 8) kp.band = 8;
@@ -98,6 +100,11 @@ sobel5_status sobel3_common(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
         kp.band = (out_h + 65534) / 65535;
         gy = static_cast<unsigned>((out_h + kp.band - 1) / kp.band);
     }
+    // replicate padding (detect --op sobel3_2d): clamped rows by TMA for the
+    // wide planes and the narrow passes, as in the 5x5 kernel
+    if (prefetch && ex.pad && tma_on && !(tp && *tp && std::atoi(tp) == 0) && !ex.norm &&
+        (wide || (out->u8 && !ex.u8_norm) || (ex.minmax && ex.s32)))
+        kp.tma_load = 1;
     if (kp.band > 32) kp.tma_load = 0;  // the shared-memory band holds 34 rows
     const dim3 grid(static_cast<unsigned>((out_w + kCtaCols - 1) / kCtaCols), gy,
                     static_cast<unsigned>(frames));

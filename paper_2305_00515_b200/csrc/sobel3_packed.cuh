@@ -28,7 +28,8 @@ namespace sobel5_b200 {
 template <int PF, bool PAD, int OUTS, bool TMAL = false>
 __global__ void __launch_bounds__(kCtaThreads, OUTS == kOutU8 ? SOBEL5_U8_MIN_CTAS : kMinCtasPerSm)
     sobel3_packed_kernel(const __grid_constant__ KernelParams p) {
-    constexpr int kTmaRowBytes = kCtaCols + 16, kTmaRows = 34;
+    constexpr int kTmaLead = PAD ? 16 : 0;  // PAD: lane 0's left word precedes the CTA's columns
+    constexpr int kTmaRowBytes = kCtaCols + 16 + kTmaLead, kTmaRows = 34;
     __shared__ __align__(128) uint8_t s_band[TMAL ? kTmaRows * kTmaRowBytes : 16];
     __shared__ __align__(8) uint64_t s_bar[2];
     if constexpr (TMAL) {
@@ -43,18 +44,23 @@ __global__ void __launch_bounds__(kCtaThreads, OUTS == kOutU8 ? SOBEL5_U8_MIN_CT
             const int b_in = min(p.band, p.out_h - b_oy0) + 2;
             const int n0 = min(6, b_in);
             const int cta_x0 = blockIdx.x * kCtaCols;
+            const int src_x = max(cta_x0 - kTmaLead, 0);
+            const int dst_off = src_x - (cta_x0 - kTmaLead);
             const uint32_t rb = static_cast<uint32_t>(
-                min(kTmaRowBytes, ((p.width + 15) & ~15) - cta_x0));
+                min(kTmaRowBytes - dst_off, ((p.width + 15) & ~15) - src_x));
             if (threadIdx.x == 0) {
                 mbar_expect_tx(&s_bar[0], rb * n0);
                 mbar_expect_tx(&s_bar[1], rb * (b_in - n0));
             }
             __syncwarp();
-            for (int r = threadIdx.x; r < b_in; r += 32)  // bands up to kTmaRows - 2
-                bulk_load(s_band + r * kTmaRowBytes,
+            for (int r = threadIdx.x; r < b_in; r += 32) {  // bands up to kTmaRows - 2
+                // PAD: padded row b_oy0 + r is image row clamp(b_oy0 + r - 1)
+                const int y = PAD ? min(max(b_oy0 + r - 1, 0), p.mid_rows - 1) : b_oy0 + r;
+                bulk_load(s_band + r * kTmaRowBytes + dst_off,
                           p.mid + static_cast<int64_t>(blockIdx.z) * p.in_frame_stride +
-                              static_cast<int64_t>(b_oy0 + r) * p.in_pitch + cta_x0,
+                              static_cast<int64_t>(y) * p.in_pitch + src_x,
                           rb, &s_bar[r < n0 ? 0 : 1]);
+            }
         }
     }
     constexpr bool RT = OUTS == kOutRuntime;
@@ -103,9 +109,10 @@ __global__ void __launch_bounds__(kCtaThreads, OUTS == kOutU8 ? SOBEL5_U8_MIN_CT
         if constexpr (TMAL) {
             if (r == 0) mbar_wait(&s_bar[0], 0);
             if (r == 6) mbar_wait(&s_bar[1], 0);
-            const uint8_t* sr = s_band + r * kTmaRowBytes + (x0 - static_cast<int>(blockIdx.x) * kCtaCols);
+            const uint8_t* sr =
+                s_band + r * kTmaRowBytes + kTmaLead + (x0 - static_cast<int>(blockIdx.x) * kCtaCols);
             a = load_a ? *reinterpret_cast<const uint32_t*>(sr) : 0u;
-            b = load_b ? *reinterpret_cast<const uint32_t*>(sr + 4) : 0u;
+            b = load_b ? *reinterpret_cast<const uint32_t*>(sr + xoff) : 0u;
             return;
         }
         const uint8_t* rp;
