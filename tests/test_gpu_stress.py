@@ -1,0 +1,66 @@
+"""GPU: randomized cross-product of the launch space against the oracle --
+image sizes around the lane/warp/CTA tiles, valid and replicate-padded
+geometry, every output contract (SR, SR32, u8 alone, mixed subsets), all
+four kernel families (default, int16 runtime taps, packed FP32, generic),
+prefetch on/off and forced bands (which also force the TMA band loads where
+they apply).  Bit-exact, float magnitude within 1 ulp."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+PLANE_SETS = [("gx", "gy", "gd", "gdt", "g"), ("gx", "gy", "gd", "gdt", "g32"), ("u8",),
+              ("gd", "g"), ("gx", "u8"), ("gy", "gdt", "g", "u8")]
+PARAMS = [(1, 2, 6, 4), (1, 1, 1, 1), (2, 3, 5, 7), (1, 32768, 1, 1)]
+BANDS = ["", "4", "8", "16", "32"]
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SOBEL5_STRESS_SEEDS", "6"))))
+def test_random_launch_space(cuda, oracle, monkeypatch, seed):
+    import torch
+    from paper_2305_00515_b200 import api
+    rng = np.random.default_rng(1000 + seed)
+    for case in range(10):
+        w = int(rng.choice([5, 9, 127, 128, 131, 509, 512, 517, 1029, 1543]))
+        h = int(rng.integers(5, 90))
+        pad = bool(rng.integers(0, 2))
+        planes = PLANE_SETS[int(rng.integers(0, len(PLANE_SETS)))]
+        prm = PARAMS[int(rng.integers(0, len(PARAMS)))]
+        pf = int(rng.integers(0, 2))
+        band = BANDS[int(rng.integers(0, len(BANDS)))]
+        mask = int(rng.choice([0xFF, 0x0F, 0x03]))
+        if band:
+            monkeypatch.setenv("SOBEL5_BAND", band)
+        else:
+            monkeypatch.delenv("SOBEL5_BAND", raising=False)
+        img = (rng.integers(0, 256, (h, w), dtype=np.uint8) & mask).astype(np.uint8)
+        st_t = oracle.make_stream_taps(*prm)
+        taps = api.Taps.from_dict(st_t.as_dict())
+        src = img
+        if pad:
+            st, src = oracle.pad_replicate(img, 2)
+            assert st == 0
+        st, ref, _ = oracle.run_stream(src, st_t)
+        assert st == 0
+        ow, oh = (w, h) if pad else (w - 4, h - 4)
+        d, pitch = api.alloc_input(w, h)
+        d.fill_(0xA5)
+        d[:, :w].copy_(torch.from_numpy(img))
+        out, op = api.alloc_planes(ow, oh, planes)
+        for v in out.values():
+            v.fill_(0x5A if v.dtype == torch.uint8 else 7)
+        api.launch_ex(d, pitch, w, h, taps, pf, pad, out, op)
+        torch.cuda.synchronize()
+        what = f"{w}x{h} pad={pad} {planes} {prm} pf={pf} band={band or 'auto'}"
+        for k in planes:
+            got = out[k][:, :ow].cpu().numpy()
+            if k == "u8":
+                np.testing.assert_array_equal(got, oracle.clamp_abs(ref["g"]), err_msg=what)
+            elif k == "g32":
+                exact = ref["g"].astype(np.float32)
+                ulps = np.abs(got.view(np.int32).astype(np.int64) - exact.view(np.int32))
+                assert ulps.max() <= 1, what
+            else:
+                np.testing.assert_array_equal(got, ref[k], err_msg=f"{k} {what}")
