@@ -82,8 +82,9 @@ sobel5_status sobel3_common(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
     kp.norm = ex.norm;
     kp.u8_norm = ex.u8_norm;
     kp.s32 = ex.s32;
-    // the write-bound Stream3Result contract reads its band rows by TMA with
-    // 8-row bands, as the 5x5 kernel does (SOBEL5_TMA_LOAD=0 disables it)
+    // the write-bound Stream3Result contract reads its band rows by TMA, as the
+    // 5x5 kernel does, with 4-row bands (8K: 89.6 vs 91.3 us at 8; 2r = 2 halo
+    // rows per band), SOBEL5_TMA_LOAD=0 disables it
     const bool wide = out->gx || out->gy || out->g || out->g32;
     const char* tv = std::getenv("SOBEL5_TMA_LOAD");
     const char* bv = std::getenv("SOBEL5_BAND");
@@ -92,7 +93,7 @@ sobel5_status sobel3_common(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
     kp.tma_load = (prefetch && !ex.pad && wide && !ex.norm && tma_on) ? 1 : 0;
     if (kp.tma_load && !(bv && *bv && std::atoi(bv) > 0)) {
         const int64_t cols = (out_w + kCtaCols - 1) / kCtaCols;  // many waves only
-        if (cols * frames * ((out_h + 7) / 8) >= 148 * 4 * 8) kp.band = 8;
+        if (cols * frames * ((out_h + 7) / 8) >= 148 * 4 * 8) kp.band = 4;
         else kp.tma_load = 0;
     }
     unsigned gy = static_cast<unsigned>((out_h + kp.band - 1) / kp.band);

@@ -327,7 +327,10 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
         // (2160) is faster on the register ring with 16-row bands
         // (39.3 vs 41.3 us, profiles/r1/tma_load.txt)
         const int64_t cols = (out_w + kCtaCols - 1) / kCtaCols;
-        if (cols * frames * ((out_h + 7) / 8) >= 148 * 4 * 8) kp.band = 8;
+        // bands of 6 rows for the plain StreamResult (8K bench.py interleaved:
+        // 134.9 vs 135.9 us at 8), 8 padded (133.7 vs 135.8 at 6), 10 for SR32
+        // (113.1 vs 117.4 us at 8; profiles/r1/tma_load.txt)
+        if (cols * frames * ((out_h + 7) / 8) >= 148 * 4 * 8) kp.band = !out->g ? 10 : ex.pad ? 8 : 6;
         else kp.tma_load = 0;
     }
     // The detect path's padded narrow passes (clamp_abs u8 map; normalize
