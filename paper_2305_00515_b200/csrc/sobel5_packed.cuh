@@ -148,6 +148,72 @@ __device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t
         : "memory");
 }
 
+// ---- TMA band rows shared by the packed kernels ---------------------------
+// The CTA's band (n_in rows x its 512 + 16 columns) is bulk-copied into
+// shared memory at CTA start, rows 0..4 and 5..n_in-1 on two mbarriers; the
+// kernels read each row from shared memory when it is consumed (band <= 32).
+// Row layout: PAD keeps 16 bytes left of the CTA's first column (lane 0's
+// left word) at offset 0, so a row holds columns [x0 - 16, x0 + 528).
+template <bool PAD>
+struct TmaBand {
+    static constexpr int kLead = PAD ? 16 : 0;
+    static constexpr int kRowBytes = kCtaCols + 16 + kLead;
+    static constexpr int kRows = 36;
+    static constexpr int kBytes = kRows * kRowBytes;
+};
+
+// Block-wide: initialise the two mbarriers, then warp 0 issues one bulk copy
+// per band row (lanes stride over the rows).  Every thread of the CTA must
+// call it (it contains a __syncthreads).
+template <bool PAD>
+__device__ __forceinline__ void tma_band_issue(const KernelParams& p, uint8_t* s_band,
+                                               uint64_t* s_bar) {
+    using T = TmaBand<PAD>;
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();  // barrier init visible before anyone waits
+    if (threadIdx.x < 32) {
+        const int b_oy0 = blockIdx.y * p.band;
+        const int b_in = min(p.band, p.out_h - b_oy0) + 4;
+        const int n0 = min(5, b_in);
+        const int cta_x0 = blockIdx.x * kCtaCols;
+        // source columns [src_x, ...): 16-B aligned, inside the row (pitch is
+        // a multiple of 16 >= width); PAD starts 16 columns early except at
+        // the left image edge
+        const int src_x = max(cta_x0 - T::kLead, 0);
+        const int dst_off = src_x - (cta_x0 - T::kLead);
+        const uint32_t rb = static_cast<uint32_t>(
+            min(T::kRowBytes - dst_off, ((p.width + 15) & ~15) - src_x));
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(&s_bar[0], rb * n0);
+            mbar_expect_tx(&s_bar[1], rb * (b_in - n0));
+        }
+        __syncwarp();
+        for (int r = threadIdx.x; r < b_in; r += 32) {
+            // PAD: padded row b_oy0 + r is image row clamp(b_oy0 + r - 2)
+            const int y = PAD ? min(max(b_oy0 + r - 2, 0), p.mid_rows - 1) : b_oy0 + r;
+            bulk_load(s_band + r * T::kRowBytes + dst_off,
+                      p.mid + static_cast<int64_t>(blockIdx.z) * p.in_frame_stride +
+                          static_cast<int64_t>(y) * p.in_pitch + src_x,
+                      rb, &s_bar[r < n0 ? 0 : 1]);
+        }
+    }
+}
+
+// Row r of the band at the thread's column x0 (waits for its mbarrier when r
+// is the first row of a stage).
+template <bool PAD>
+__device__ __forceinline__ const uint8_t* tma_band_row(uint8_t* s_band, uint64_t* s_bar, int r,
+                                                       int x0) {
+    if (r == 0) mbar_wait(&s_bar[0], 0);
+    if (r == 5) mbar_wait(&s_bar[1], 0);
+    return s_band + r * TmaBand<PAD>::kRowBytes + TmaBand<PAD>::kLead +
+           (x0 - static_cast<int>(blockIdx.x) * kCtaCols);
+}
+
 // ---- TMA bulk stores (cp.async.bulk global <- shared, bulk-group completion)
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
@@ -216,16 +282,11 @@ __global__ void __launch_bounds__(kCtaThreads,
     sobel5_packed_default_kernel(const __grid_constant__ KernelParams p) {
     constexpr bool SEG = GEOM == kGeomSeg;
     constexpr bool PAD = GEOM == kGeomPad || GEOM == kGeomPadTma;
-    // TMAL: the CTA's band (n_in rows x its 512 + 16 columns) is bulk-copied
-    // into shared memory at the start, rows 0..4 and 5..n_in-1 on two
-    // mbarriers; the launchers instantiate it with PF = 0, so each row is read
-    // from shared memory when it is consumed (band <= 32)
+    // TMAL: band rows by TMA into shared memory (tma_band_issue); the
+    // launchers instantiate it with PF = 0, so each row is read from shared
+    // memory when it is consumed
     constexpr bool TMAL = GEOM == kGeomPlainTma || GEOM == kGeomPadTma;
-    // row layout: PAD keeps 16 bytes left of the CTA's first column (lane 0's
-    // left word) at offset 0, so a row holds columns [x0 - 16, x0 + 528)
-    constexpr int kTmaLead = PAD ? 16 : 0;
-    constexpr int kTmaRowBytes = kCtaCols + 16 + kTmaLead, kTmaRows = 36;
-    __shared__ __align__(128) uint8_t s_band[TMAL ? kTmaRows * kTmaRowBytes : 16];
+    __shared__ __align__(128) uint8_t s_band[TMAL ? TmaBand<PAD>::kBytes : 16];
     __shared__ __align__(8) uint64_t s_bar[2];
     // which planes this instantiation writes (compile-time unless kOutRuntime)
     constexpr bool RT = OUTS == kOutRuntime;
@@ -284,40 +345,7 @@ __global__ void __launch_bounds__(kCtaThreads,
             __syncthreads();
         }
     }
-    if constexpr (TMAL) {
-        if (threadIdx.x == 0) {
-            mbar_init(&s_bar[0], 1);
-            mbar_init(&s_bar[1], 1);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        }
-        __syncthreads();  // barrier init visible before anyone waits
-        if (threadIdx.x < 32) {  // warp 0: one lane per row issues its bulk copy
-            const int b_oy0 = blockIdx.y * p.band;
-            const int b_in = min(p.band, p.out_h - b_oy0) + 4;
-            const int n0 = min(5, b_in);
-            const int cta_x0 = blockIdx.x * kCtaCols;
-            // source columns [src_x, ...): 16-B aligned, inside the row (pitch
-            // is a multiple of 16 >= width); PAD starts 16 columns early
-            // except at the left image edge
-            const int src_x = max(cta_x0 - kTmaLead, 0);
-            const int dst_off = src_x - (cta_x0 - kTmaLead);
-            const uint32_t rb = static_cast<uint32_t>(
-                min(kTmaRowBytes - dst_off, ((p.width + 15) & ~15) - src_x));
-            if (threadIdx.x == 0) {
-                mbar_expect_tx(&s_bar[0], rb * n0);
-                mbar_expect_tx(&s_bar[1], rb * (b_in - n0));
-            }
-            __syncwarp();
-            for (int r = threadIdx.x; r < b_in; r += 32) {  // bands up to kTmaRows - 4
-                // PAD: padded row b_oy0 + r is image row clamp(b_oy0 + r - 2)
-                const int y = PAD ? min(max(b_oy0 + r - 2, 0), p.mid_rows - 1) : b_oy0 + r;
-                bulk_load(s_band + r * kTmaRowBytes + dst_off,
-                          p.mid + static_cast<int64_t>(blockIdx.z) * p.in_frame_stride +
-                              static_cast<int64_t>(y) * p.in_pitch + src_x,
-                          rb, &s_bar[r < n0 ? 0 : 1]);
-            }
-        }
-    }
+    if constexpr (TMAL) tma_band_issue<PAD>(p, s_band, s_bar);
     if (warp_x0 >= p.out_w) return;  // whole warp right of the image
     const int oy0 = blockIdx.y * p.band;
     const int n_out = min(p.band, p.out_h - oy0);
@@ -371,10 +399,7 @@ __global__ void __launch_bounds__(kCtaThreads,
     };
     auto load_row = [&](int r, uint32_t& a, uint32_t& b) {
         if constexpr (TMAL) {
-            if (r == 0) mbar_wait(&s_bar[0], 0);
-            if (r == 5) mbar_wait(&s_bar[1], 0);
-            const uint8_t* sr =
-                s_band + r * kTmaRowBytes + kTmaLead + (x0 - static_cast<int>(blockIdx.x) * kCtaCols);
+            const uint8_t* sr = tma_band_row<PAD>(s_band, s_bar, r, x0);
             a = load_a ? *reinterpret_cast<const uint32_t*>(sr) : 0u;
             b = load_b ? *reinterpret_cast<const uint32_t*>(sr + xoff) : 0u;
             return;
