@@ -316,7 +316,10 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     // register ring, and so
     // does the runtime-taps packed kernel (171 vs 150 us at 8-row bands);
     // profiles/r1/tma_load.txt).  SOBEL5_TMA_LOAD=0 disables it.
-    kp.tma_load = (prefetch && (!ex.pad || env_int("SOBEL5_TMA_PAD", 1) != 0) && !top && !bot &&
+    // Stacked bands (C5, halos possibly in a peer GPU's memory): only the CTAs
+    // whose rows are all in `mid` bulk-copy them (kGeomSegTma).
+    kp.tma_load = (prefetch && (!ex.pad || env_int("SOBEL5_TMA_PAD", 1) != 0) &&
+                   ((!top && !bot) || env_int("SOBEL5_TMA_SEG", 1) != 0) &&
                    (out->g || out->g32) && taps_are_default(*taps) &&
                    env_int("SOBEL5_TMA_LOAD", 1) != 0 && env_int("SOBEL5_GENERIC", 0) == 0 &&
                    env_int("SOBEL5_DENSE", 0) == 0 && !(ex.u8_norm || ex.norm))
@@ -327,10 +330,16 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
         // (2160) is faster on the register ring with 16-row bands
         // (39.3 vs 41.3 us, profiles/r1/tma_load.txt)
         const int64_t cols = (out_w + kCtaCols - 1) / kCtaCols;
-        // bands of 6 rows for the plain StreamResult (8K bench.py interleaved:
-        // 134.9 vs 135.9 us at 8), 8 padded (133.7 vs 135.8 at 6), 10 for SR32
-        // (113.1 vs 117.4 us at 8; profiles/r1/tma_load.txt)
-        if (cols * frames * ((out_h + 7) / 8) >= 148 * 4 * 8) kp.band = !out->g ? 10 : ex.pad ? 8 : 6;
+        // bands of 6 rows for the plain StreamResult up to ~300 M output px
+        // (8K bench.py interleaved: 134.9 vs 135.9 us at 8), 8 above (C4
+        // 256 x 1080p: 238 vs 226 Gpx/s, C5 32K: 246 vs 235 -- long launches
+        // run into the power cap, and the shorter bands' extra halo reads
+        // cost more there), 8 padded (133.7 vs 135.8 at 6), 10 for SR32
+        // (113.1 vs 117.4 us at 8), 12 for big SR32 (C4: 269.8 vs 265 / 261
+        // Gpx/s at 10 / 8; profiles/r1/tma_load.txt)
+        const bool big = int64_t{out_w} * out_h * frames > (int64_t{300} << 20);
+        if (cols * frames * ((out_h + 7) / 8) >= 148 * 4 * 8)
+            kp.band = !out->g ? (big ? 12 : 10) : (ex.pad || big) ? 8 : 6;
         else kp.tma_load = 0;
     }
     // The detect path's padded narrow passes (clamp_abs u8 map; normalize

@@ -8,7 +8,12 @@ namespace sobel5_b200 {
 namespace {
 template <int PF, int OUTS>
 cudaError_t go(const KernelParams& kp, dim3 grid, cudaStream_t s) {
-    sobel5_packed_default_kernel<PF, kGeomSeg, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
+    // band rows by TMA for the CTAs whose rows are all in the local band
+    // (launch_common decides); the halo-touching CTAs load from global
+    if (PF > 0 && kp.tma_load)
+        sobel5_packed_default_kernel<0, kGeomSegTma, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
+    else
+        sobel5_packed_default_kernel<PF, kGeomSeg, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
     return cudaGetLastError();
 }
 

@@ -164,11 +164,17 @@ struct TmaBand {
 
 // Block-wide: initialise the two mbarriers, then warp 0 issues one bulk copy
 // per band row (lanes stride over the rows).  Every thread of the CTA must
-// call it (it contains a __syncthreads).
-template <bool PAD>
-__device__ __forceinline__ void tma_band_issue(const KernelParams& p, uint8_t* s_band,
+// call it (it contains a __syncthreads).  SEG (stacked [top; mid; bot]):
+// only CTAs whose rows all lie in `mid` use TMA -- the halo rows (possibly a
+// peer GPU's memory) are never bulk-copied; the return value says whether
+// this CTA's band is in shared memory (block-uniform).
+template <bool PAD, bool SEG = false>
+__device__ __forceinline__ bool tma_band_issue(const KernelParams& p, uint8_t* s_band,
                                                uint64_t* s_bar) {
     using T = TmaBand<PAD>;
+    const int b_oy0 = blockIdx.y * p.band;
+    const int b_in = min(p.band, p.out_h - b_oy0) + 4;
+    if (SEG && (b_oy0 < p.top_rows || b_oy0 + b_in > p.top_rows + p.mid_rows)) return false;
     if (threadIdx.x == 0) {
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
@@ -176,8 +182,6 @@ __device__ __forceinline__ void tma_band_issue(const KernelParams& p, uint8_t* s
     }
     __syncthreads();  // barrier init visible before anyone waits
     if (threadIdx.x < 32) {
-        const int b_oy0 = blockIdx.y * p.band;
-        const int b_in = min(p.band, p.out_h - b_oy0) + 4;
         const int n0 = min(5, b_in);
         const int cta_x0 = blockIdx.x * kCtaCols;
         // source columns [src_x, ...): 16-B aligned, inside the row (pitch is
@@ -193,14 +197,18 @@ __device__ __forceinline__ void tma_band_issue(const KernelParams& p, uint8_t* s
         }
         __syncwarp();
         for (int r = threadIdx.x; r < b_in; r += 32) {
-            // PAD: padded row b_oy0 + r is image row clamp(b_oy0 + r - 2)
-            const int y = PAD ? min(max(b_oy0 + r - 2, 0), p.mid_rows - 1) : b_oy0 + r;
+            // PAD: padded row b_oy0 + r is image row clamp(b_oy0 + r - 2);
+            // SEG: stacked row b_oy0 + r is mid row b_oy0 + r - top_rows
+            const int y = PAD   ? min(max(b_oy0 + r - 2, 0), p.mid_rows - 1)
+                          : SEG ? b_oy0 + r - p.top_rows
+                                : b_oy0 + r;
             bulk_load(s_band + r * T::kRowBytes + dst_off,
                       p.mid + static_cast<int64_t>(blockIdx.z) * p.in_frame_stride +
                           static_cast<int64_t>(y) * p.in_pitch + src_x,
                       rb, &s_bar[r < n0 ? 0 : 1]);
         }
     }
+    return true;
 }
 
 // Row r of the band at the thread's column x0 (waits for its mbarrier when r
@@ -280,12 +288,12 @@ template <int PF, int GEOM, int OUTS, bool RTAPS = false>
 __global__ void __launch_bounds__(kCtaThreads,
                                   (OUTS == kOutU8 && !RTAPS) ? SOBEL5_U8_MIN_CTAS : kMinCtasPerSm)
     sobel5_packed_default_kernel(const __grid_constant__ KernelParams p) {
-    constexpr bool SEG = GEOM == kGeomSeg;
+    constexpr bool SEG = GEOM == kGeomSeg || GEOM == kGeomSegTma;
     constexpr bool PAD = GEOM == kGeomPad || GEOM == kGeomPadTma;
     // TMAL: band rows by TMA into shared memory (tma_band_issue); the
     // launchers instantiate it with PF = 0, so each row is read from shared
     // memory when it is consumed
-    constexpr bool TMAL = GEOM == kGeomPlainTma || GEOM == kGeomPadTma;
+    constexpr bool TMAL = GEOM == kGeomPlainTma || GEOM == kGeomPadTma || GEOM == kGeomSegTma;
     __shared__ __align__(128) uint8_t s_band[TMAL ? TmaBand<PAD>::kBytes : 16];
     __shared__ __align__(8) uint64_t s_bar[2];
     // which planes this instantiation writes (compile-time unless kOutRuntime)
@@ -345,7 +353,8 @@ __global__ void __launch_bounds__(kCtaThreads,
             __syncthreads();
         }
     }
-    if constexpr (TMAL) tma_band_issue<PAD>(p, s_band, s_bar);
+    bool cta_tma = false;  // SEG: CTAs touching a halo row load from global
+    if constexpr (TMAL) cta_tma = tma_band_issue<PAD, SEG>(p, s_band, s_bar);
     if (warp_x0 >= p.out_w) return;  // whole warp right of the image
     const int oy0 = blockIdx.y * p.band;
     const int n_out = min(p.band, p.out_h - oy0);
@@ -399,10 +408,12 @@ __global__ void __launch_bounds__(kCtaThreads,
     };
     auto load_row = [&](int r, uint32_t& a, uint32_t& b) {
         if constexpr (TMAL) {
-            const uint8_t* sr = tma_band_row<PAD>(s_band, s_bar, r, x0);
-            a = load_a ? *reinterpret_cast<const uint32_t*>(sr) : 0u;
-            b = load_b ? *reinterpret_cast<const uint32_t*>(sr + xoff) : 0u;
-            return;
+            if (!SEG || cta_tma) {
+                const uint8_t* sr = tma_band_row<PAD>(s_band, s_bar, r, x0);
+                a = load_a ? *reinterpret_cast<const uint32_t*>(sr) : 0u;
+                b = load_b ? *reinterpret_cast<const uint32_t*>(sr + xoff) : 0u;
+                return;
+            }
         }
         const uint8_t* rp;
         if (!SEG && !PAD) {

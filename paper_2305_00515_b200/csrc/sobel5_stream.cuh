@@ -189,6 +189,7 @@ enum Geom : int {
     kGeomPad = 2,    // pad_replicate(img, 2) fused: same-size output (image_io.hpp:279-291)
     kGeomPlainTma = 3,  // plain, the CTA's band rows bulk-copied (TMA) into shared memory
     kGeomPadTma = 4,    // pad_replicate fused, band rows (clamped) bulk-copied likewise
+    kGeomSegTma = 5,    // stacked, band rows bulk-copied for CTAs whose rows are all in mid
 };
 
 // The 8-byte window (wa = input columns c..c+3, wb = c+4..c+7) a lane needs

@@ -162,14 +162,19 @@ def test_batch_launch(S, oracle):
             np.testing.assert_array_equal(out[k][f, :, : w - 4].cpu().numpy(), ref[k])
 
 
-@pytest.mark.parametrize("n_bands", [2, 3, 5])
-def test_row_band_partition_equals_whole(S, oracle, n_bands):
+@pytest.mark.parametrize("n_bands,band", [(2, ""), (3, ""), (5, ""), (2, "4"), (3, "6"),
+                                          (2, "8"), (3, "16")])
+def test_row_band_partition_equals_whole(S, oracle, monkeypatch, n_bands, band):
     """C5 row-band tiler: bands with 2-row halos above/below stitch to the
-    single-image result (the multi-GPU partition, exercised on one GPU)."""
+    single-image result (the multi-GPU partition, exercised on one GPU).
+    Forced CTA bands switch on the TMA rows (kGeomSegTma): CTAs whose rows
+    touch a halo load from global memory, the others from shared memory."""
     import torch
     from paper_2305_00515_b200 import api
+    if band:
+        monkeypatch.setenv("SOBEL5_BAND", band)
     rng = np.random.default_rng(4)
-    w, h = 523, 97
+    w, h = (1543, 157) if band else (523, 97)
     img = rng.integers(0, 256, (h, w), dtype=np.uint8)
     st, ref, _ = oracle.run_stream(img)
     bounds = np.linspace(0, h, n_bands + 1).astype(int)
