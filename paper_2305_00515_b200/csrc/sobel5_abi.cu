@@ -309,7 +309,7 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     const bool wide = out->gx || out->gy || out->gd || out->gdt || out->g || out->g32;
     kp.band = choose_band(out_w, out_h, frames, !wide);
     // Write-bound contracts of the default-taps kernel on plain images: the
-    // CTA's band rows come in by TMA bulk copies (kGeomPlainTma), with 8-row
+    // CTA's band rows come in by TMA bulk copies (kGeomPlainTma), with short
     // bands (8K SR: 142.2 us register ring, band 16 -> 137.1 us TMA, band 8;
     // with the rows read from shared memory when consumed SR32 gains too
     // (117.3 vs 119.1 us); the u8-only contract stays 4-8% faster on the

@@ -64,3 +64,61 @@ def test_random_launch_space(cuda, oracle, monkeypatch, seed):
                 assert ulps.max() <= 1, what
             else:
                 np.testing.assert_array_equal(got, ref[k], err_msg=f"{k} {what}")
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SOBEL5_STRESS_SEEDS", "6"))))
+def test_random_stacked_bands(cuda, oracle, monkeypatch, seed):
+    """Stacked row bands ([2 halo rows; body; 2 halo rows], the C5 partition)
+    over random sizes, cut points, contracts, kernel families, prefetch and
+    forced CTA bands (which switch on kGeomSegTma: body-only CTAs read their
+    rows by TMA, halo-touching CTAs from global memory)."""
+    import torch
+    from paper_2305_00515_b200 import api
+    rng = np.random.default_rng(5000 + seed)
+    for case in range(6):
+        w = int(rng.choice([9, 131, 517, 1029, 1543]))
+        h = int(rng.integers(12, 120))
+        planes = PLANE_SETS[int(rng.integers(0, len(PLANE_SETS)))]
+        prm = PARAMS[int(rng.integers(0, 3))]
+        pf = int(rng.integers(0, 2))
+        band = BANDS[int(rng.integers(0, len(BANDS)))]
+        if band:
+            monkeypatch.setenv("SOBEL5_BAND", band)
+        else:
+            monkeypatch.delenv("SOBEL5_BAND", raising=False)
+        img = (rng.integers(0, 256, (h, w), dtype=np.uint8) & 0x0F).astype(np.uint8)
+        st_t = oracle.make_stream_taps(*prm)
+        taps = api.Taps.from_dict(st_t.as_dict())
+        st, ref, _ = oracle.run_stream(img, st_t)
+        assert st == 0
+        r0 = int(rng.integers(0, h // 2))
+        r1 = int(rng.integers(max(r0 + 1, h // 2), h + 1))
+        body, pitch = api.alloc_input(w, r1 - r0)
+        body[:, :w].copy_(torch.from_numpy(img[r0:r1]))
+        top = bot = None
+        if r0 >= 2:
+            top, _ = api.alloc_input(w, 2)
+            top[:, :w].copy_(torch.from_numpy(img[r0 - 2:r0]))
+        if r1 + 2 <= h:
+            bot, _ = api.alloc_input(w, 2)
+            bot[:, :w].copy_(torch.from_numpy(img[r1:r1 + 2]))
+        stacked = (r1 - r0) + (2 if top is not None else 0) + (2 if bot is not None else 0)
+        if stacked < 5:
+            continue
+        rows = stacked - 4
+        out, op = api.alloc_planes(w - 4, rows, planes)
+        api.launch_band(top, body, bot, pitch, w, r1 - r0, taps, pf, out, op)
+        torch.cuda.synchronize()
+        y0 = r0 - 2 if top is not None else r0
+        what = f"{w}x{h} rows {r0}:{r1} {planes} {prm} pf={pf} band={band or 'auto'}"
+        for k in planes:
+            got = out[k][:, :w - 4].cpu().numpy()
+            want = ref["g"][y0:y0 + rows] if k in ("u8", "g32") else ref[k][y0:y0 + rows]
+            if k == "u8":
+                np.testing.assert_array_equal(got, oracle.clamp_abs(want), err_msg=what)
+            elif k == "g32":
+                ulps = np.abs(got.view(np.int32).astype(np.int64) -
+                              want.astype(np.float32).view(np.int32))
+                assert ulps.max() <= 1, what
+            else:
+                np.testing.assert_array_equal(got, want, err_msg=f"{k} {what}")
