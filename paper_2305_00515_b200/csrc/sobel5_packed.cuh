@@ -284,9 +284,16 @@ __device__ __forceinline__ uint32_t u8_normalize_s(uint32_t S, const uint32_t* t
 #ifndef SOBEL5_U8_MIN_CTAS
 #define SOBEL5_U8_MIN_CTAS kMinCtasPerSm
 #endif
+#ifndef SOBEL5_TMA_MIN_CTAS
+#define SOBEL5_TMA_MIN_CTAS kMinCtasPerSm
+#endif
 template <int PF, int GEOM, int OUTS, bool RTAPS = false>
 __global__ void __launch_bounds__(kCtaThreads,
-                                  (OUTS == kOutU8 && !RTAPS) ? SOBEL5_U8_MIN_CTAS : kMinCtasPerSm)
+                                  (OUTS == kOutU8 && !RTAPS) ? SOBEL5_U8_MIN_CTAS
+                                  : (GEOM == kGeomPlainTma || GEOM == kGeomPadTma ||
+                                     GEOM == kGeomSegTma)
+                                      ? SOBEL5_TMA_MIN_CTAS
+                                      : kMinCtasPerSm)
     sobel5_packed_default_kernel(const __grid_constant__ KernelParams p) {
     constexpr bool SEG = GEOM == kGeomSeg || GEOM == kGeomSegTma;
     constexpr bool PAD = GEOM == kGeomPad || GEOM == kGeomPadTma;
