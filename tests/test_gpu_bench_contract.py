@@ -39,3 +39,15 @@ def test_two_ranks_share_gpu(cuda, workload):
              "--no-cpu-baseline", "--no-e2e"])
     assert d["n_gpus"] == 2 and d["value"] > 0
     assert d["scaling"] == ("strong" if workload == "32k-bands" else "weak")
+
+
+def test_two_ranks_e2e(cuda):
+    """The e2e number at N > 1 is whole-job: every rank runs the host path on
+    its own image, the time is the max over ranks."""
+    d = run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+             "--master-addr", "127.0.0.1", "--master-port", "29538", "bench.py", "--gpus", "2",
+             "--steps", "4", "--warmup", "3", "--share-gpu", "--no-cpu-baseline"])
+    e = d["e2e"]
+    assert e["ranks"] == 2 and e["value"] > 0
+    assert e["h2d_bytes_per_step"] == 2 * 7680 * 4320
+    assert e["d2h_bytes_per_step"] == 2 * 7676 * 4316 * 24
