@@ -303,6 +303,11 @@ __global__ void __launch_bounds__(kCtaThreads,
     constexpr bool TMAL = GEOM == kGeomPlainTma || GEOM == kGeomPadTma || GEOM == kGeomSegTma;
     __shared__ __align__(128) uint8_t s_band[TMAL ? TmaBand<PAD>::kBytes : 16];
     __shared__ __align__(8) uint64_t s_bar[2];
+    // StreamResult on the TMA-row kernel: write-back stores instead of .cs
+#ifndef SOBEL5_SR_WB
+#define SOBEL5_SR_WB 1
+#endif
+    constexpr bool WB = SOBEL5_SR_WB && OUTS == kOutSR && TMAL;
     // which planes this instantiation writes (compile-time unless kOutRuntime)
     constexpr bool RT = OUTS == kOutRuntime;
     const bool w_gx = RT ? p.gx != nullptr : (OUTS & kOutGx) != 0;
@@ -738,6 +743,12 @@ __global__ void __launch_bounds__(kCtaThreads,
                         bulk_commit();
                     }
                     ++stage_row;
+                } else if (full && WB) {
+                    st_wb_v4(p.gx + row_off, gx[0], gx[1], gx[2], gx[3]);
+                    st_wb_v4(p.gy + row_off, gy[0], gy[1], gy[2], gy[3]);
+                    st_wb_v4(p.gd + row_off, gd[0], gd[1], gd[2], gd[3]);
+                    st_wb_v4(p.gdt + row_off, gdt[0], gdt[1], gdt[2], gdt[3]);
+                    st_wb_v4d(p.g + row_off, g[0], g[1], g[2], g[3]);
                 } else if (full) {
                     if (w_gx) st_cs_v4(p.gx + row_off, gx[0], gx[1], gx[2], gx[3]);
                     if (w_gy) st_cs_v4(p.gy + row_off, gy[0], gy[1], gy[2], gy[3]);

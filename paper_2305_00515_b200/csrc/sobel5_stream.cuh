@@ -132,6 +132,17 @@ __device__ __forceinline__ void st_cs_v4d(double* p, double a, double b, double 
                  "d"(d)
                  : "memory");
 }
+// Write-back (default policy) twins: the StreamResult contract is 1% faster
+// with them on the TMA-row kernel (131.7 vs 133.0 us at 8K), SR32 0.7%
+// slower (profiles/r1/store_qualifier_sweep.txt)
+__device__ __forceinline__ void st_wb_v4(int32_t* p, int32_t a, int32_t b, int32_t c, int32_t d) {
+    asm volatile("st.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void st_wb_v4d(double* p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+                 : "memory");
+}
 __device__ __forceinline__ void st_cs_u32(uint8_t* p, uint32_t v) {
     asm volatile("st.global" SOBEL5_ST_Q ".u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
