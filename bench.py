@@ -555,7 +555,7 @@ def main():
                          "alg_bytes_per_launch": alg_bytes,
                          "kernel": ("sobel5_packed_default_kernel" if taps_default
                                     else "sobel5_stream_kernel")
-                         + (" (TMA band rows, 6-row bands)" if a.contract == "sr" and a.prefetch
+                         + (" (TMA band rows, 6-row bands, write-back stores)" if a.contract == "sr" and a.prefetch
                             and a.workload != "4k" and not (a.workload == "32k-bands" and world > 1)
                             else ""),
                          "kernel_us": ms_step * 1e3},
