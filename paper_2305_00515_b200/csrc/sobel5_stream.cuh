@@ -304,7 +304,10 @@ __device__ __forceinline__ uint32_t normalize_u8(double g, double lo, double spa
 //   MAG    : MagMode;
 //   PAD    : fused pad_replicate(img, 2) (same-size output) vs valid mode.
 template <int PF, class TAPS, int MAG, bool PAD>
-__global__ void __launch_bounds__(kCtaThreads)
+#ifndef SOBEL5_GENERIC_MIN_CTAS
+#define SOBEL5_GENERIC_MIN_CTAS 1
+#endif
+__global__ void __launch_bounds__(kCtaThreads, SOBEL5_GENERIC_MIN_CTAS)
     sobel5_stream_kernel(const __grid_constant__ KernelParams p) {
     const TapSource<TAPS> T{p};
     const int lane = threadIdx.x & 31;
