@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(kCtaThreads,
 #ifndef SOBEL5_SR_WB
 #define SOBEL5_SR_WB 1
 #endif
-    constexpr bool WB = SOBEL5_SR_WB && OUTS == kOutSR && TMAL;
+    constexpr bool WB = (SOBEL5_SR_WB == 2 || (SOBEL5_SR_WB == 1 && TMAL)) && OUTS == kOutSR;
     // which planes this instantiation writes (compile-time unless kOutRuntime)
     constexpr bool RT = OUTS == kOutRuntime;
     const bool w_gx = RT ? p.gx != nullptr : (OUTS & kOutGx) != 0;
