@@ -24,6 +24,30 @@ struct Kernel5 {
     friend bool operator!=(const Kernel5& a, const Kernel5& b) { return !(a == b); }
 };
 
+/// 3x3 integer kernel of the classic two-direction operator (reference
+/// filter_algebra.hpp:25-39).
+struct Kernel3 {
+    std::array<std::array<std::int32_t, 3>, 3> w{};
+    std::int32_t at(int i, int j) const { return w[static_cast<std::size_t>(i)][static_cast<std::size_t>(j)]; }
+    friend bool operator==(const Kernel3& a, const Kernel3& b) { return a.w == b.w; }
+};
+
+namespace detail {
+/// Eq. 1: the 3x3 Sobel pair is smoothing [1, 2, 1] across the derivative
+/// [-1, 0, 1]; Gx differentiates along the row, Gy down the column.
+inline Kernel3 sobel3_outer(bool along_row) {
+    constexpr std::int32_t smooth[3] = {1, 2, 1}, deriv[3] = {-1, 0, 1};
+    Kernel3 k;
+    for (std::size_t i = 0; i < 3; ++i)
+        for (std::size_t j = 0; j < 3; ++j)
+            k.w[i][j] = along_row ? smooth[i] * deriv[j] : deriv[i] * smooth[j];
+    return k;
+}
+}  // namespace detail
+
+inline Kernel3 kernel3_x() { return detail::sobel3_outer(true); }
+inline Kernel3 kernel3_y() { return detail::sobel3_outer(false); }
+
 /// scale * (col outer row)
 struct SeparablePair {
     std::array<std::int32_t, 5> col{};

@@ -605,12 +605,36 @@ struct Sobel5Result {
     RealPlane g;
 };
 
+/// The oracle's own algorithm on the device (sobel5_dense_4d): four dense
+/// correlations with the materialised Kx, Ky, Kd, Kdt and the double
+/// magnitude, independent of the streaming kernels run_stream uses -- so a
+/// caller's verify flow (run_stream vs sobel5_4d) compares two algorithms,
+/// as with the reference.
 inline Sobel5Result sobel5_4d(const GrayPlane& img, const FilterParams& p) {
     if (img.width() < 5 || img.height() < 5)
         throw ImageTooSmall("conv2d_valid needs at least 5x5, got " + std::to_string(img.width()) + "x" +
                             std::to_string(img.height()));
-    auto r = run_stream(img, make_stream_taps(p), plan_strips(img.width(), img.width(), 2), Prefetch::on);
-    return Sobel5Result{std::move(r.gx), std::move(r.gy), std::move(r.gd), std::move(r.gdt), std::move(r.g)};
+    std::int32_t k[4 * 25];
+    const Direction dirs[4] = {Direction::X, Direction::Y, Direction::D, Direction::DT};
+    for (int d = 0; d < 4; ++d) {
+        const Kernel5 m = materialize(p, dirs[d]);
+        for (int i = 0; i < 5; ++i)
+            for (int j = 0; j < 5; ++j) k[d * 25 + i * 5 + j] = m.at(i, j);
+    }
+    const int ow = img.width() - 4, oh = img.height() - 4;
+    Sobel5Result r{SignedPlane(ow, oh), SignedPlane(ow, oh), SignedPlane(ow, oh), SignedPlane(ow, oh),
+                   RealPlane(ow, oh)};
+    sobel5_planes pl{};
+    pl.pitch = ow;
+    pl.gx = r.gx.data().data();
+    pl.gy = r.gy.data().data();
+    pl.gd = r.gd.data().data();
+    pl.gdt = r.gdt.data().data();
+    pl.g = r.g.data().data();
+    sobel5_ctx* c = gpu::thread_context().get();
+    const sobel5_status st = sobel5_dense_4d_host(c, img.data().data(), img.width(), img.height(), k, &pl);
+    if (st != SOBEL5_OK) gpu::raise(st, std::string("sobel5_4d (") + sobel5_ctx_last_error(c) + ")");
+    return r;
 }
 
 /// oracle.hpp:100-129: the diagonal responses through the Kd+/- sum and

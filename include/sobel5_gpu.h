@@ -125,6 +125,18 @@ const char* sobel5_status_string(int status);
 /* Number of kernel launches this process has issued through the library. */
 uint64_t sobel5_launch_count(void);
 
+/* Geometry the calling thread's last 5x5 stencil launch chose (diagnostics:
+ * lets tests assert which code path a configuration takes).  band = output
+ * rows per CTA, tma_load = 1 when the CTA's band rows came in by TMA bulk
+ * copies, kernel = sobel5_kernel_for_taps of the taps, grid = CTA grid. */
+typedef struct sobel5_launch_info {
+    int band;
+    int tma_load;
+    int kernel;
+    int grid_x, grid_y, grid_z;
+} sobel5_launch_info;
+sobel5_status sobel5_last_launch(sobel5_launch_info* out);
+
 /* ---- host-only helpers (no GPU needed) ------------------------------------ */
 
 /* make_stream_taps (pipeline.hpp:75-107) for integer (a, b, m, n), with the
@@ -349,6 +361,34 @@ sobel5_status sobel5_detect_host(sobel5_ctx* ctx, const uint8_t* h_in, int width
  * tightly packed plane (kind 0 double, 1 int32), h_u8 same size. */
 sobel5_status sobel5_quantize_host(sobel5_ctx* ctx, const void* h_plane, int kind, int width,
                                    int height, int save_mode, uint8_t* h_u8);
+
+/* ---- the oracle's dense correlation (oracle.hpp:19-49) ------------------
+ * conv2d_valid(img, Kernel5 / Kernel3): valid-mode correlation (no kernel
+ * flip) of a uint8 image with an arbitrary ksize x ksize int32 kernel
+ * (`kernel` is a HOST array, row-major), int32 result equal to the
+ * reference's int64 sum cast to int32.  ksize is 5 or 3; images smaller
+ * than the kernel give SOBEL5_IMAGE_TOO_SMALL.  d_in: in_pitch % 16 == 0,
+ * 16-byte aligned; d_out: (W-k+1) x (H-k+1) with row stride out_pitch
+ * elements. */
+sobel5_status sobel5_conv2d_valid(const uint8_t* d_in, int64_t in_pitch, int width, int height,
+                                  const int32_t* kernel, int ksize, int32_t* d_out,
+                                  int64_t out_pitch, void* stream);
+/* Host buffers (tightly packed W x H in, (W-k+1) x (H-k+1) out). */
+sobel5_status sobel5_conv2d_valid_host(sobel5_ctx* ctx, const uint8_t* h_in, int width,
+                                       int height, const int32_t* kernel, int ksize,
+                                       int32_t* h_out);
+/* sobel5_4d (oracle.hpp:82-98): the four dense 5x5 correlations with the
+ * materialised kernels Kx, Ky, Kd, Kdt (`kernels`: HOST array of 4 x 25
+ * int32, row-major, in that order) and the magnitude
+ * sqrt(gx*gx + gy*gy + gd*gd + gdt*gdt) in double with the reference's
+ * rounding sequence, all in one device pass -- the oracle's algorithm, not
+ * the streaming one.  d_out->g32 and ->u8 must be NULL; other planes may be
+ * NULL (skipped). */
+sobel5_status sobel5_dense_4d(const uint8_t* d_in, int64_t in_pitch, int width, int height,
+                              const int32_t* kernels, const sobel5_planes* d_out, void* stream);
+/* Host buffers: tightly packed planes (pitch == width-4). */
+sobel5_status sobel5_dense_4d_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
+                                   const int32_t* kernels, const sobel5_planes* h_out);
 
 #ifdef __cplusplus
 }

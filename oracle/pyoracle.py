@@ -97,6 +97,10 @@ class Oracle:
         L.oracle_pad_replicate.restype = C.c_int
         for fn in ("oracle_normalize_f64", "oracle_normalize_i32", "oracle_clamp_abs_i32"):
             getattr(L, fn).argtypes = [C.c_void_p, C.c_size_t, C.c_void_p]
+        L.oracle_conv2d_valid.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.oracle_conv2d_valid.restype = C.c_int
+        L.oracle_conv2d_valid3.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.oracle_conv2d_valid3.restype = C.c_int
         L.oracle_sobel3_2d.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 3
         L.oracle_sobel3_2d.restype = C.c_int
         L.oracle_stream3_counters.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_int,
@@ -134,6 +138,18 @@ class Oracle:
         if st:
             raise RuntimeError(f"oracle_sobel5_4d status {st}")
         return o
+
+    def conv2d_valid(self, img: np.ndarray, k: np.ndarray) -> np.ndarray:
+        """oracle.hpp:19-49 for a 5x5 or 3x3 int32 kernel."""
+        img = np.ascontiguousarray(img, np.uint8)
+        k = np.ascontiguousarray(k, np.int32)
+        ks = k.shape[0]
+        h, w = img.shape
+        out = np.empty((h - ks + 1, w - ks + 1), np.int32)
+        fn = self.lib.oracle_conv2d_valid if ks == 5 else self.lib.oracle_conv2d_valid3
+        if fn(_p(img), w, h, _p(k), _p(out)):
+            raise ValueError("image smaller than the kernel")
+        return out
 
     def clamp_abs(self, g: np.ndarray) -> np.ndarray:
         g = np.ascontiguousarray(g, np.float64)
@@ -230,6 +246,9 @@ class Reference:
         L.ref_run_stream_3x3.argtypes = [C.c_void_p] + [C.c_int] * 5 + [C.c_void_p] * 4 + E
         L.ref_measure_run_stream_3x3.argtypes = [C.c_void_p] + [C.c_int] * 6 + [C.c_void_p]
         L.ref_measure_run_stream_3x3.restype = C.c_double
+        L.ref_conv2d_valid.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                       C.c_void_p]
+        L.ref_conv2d_valid.restype = C.c_int
 
     @staticmethod
     def _err():
@@ -336,6 +355,15 @@ class Reference:
         h, w = plane.shape
         self.lib.ref_quantize(_p(plane), kind, w, h, 1 if mode == "normalize" else 0, _p(out))
         return out
+
+    def conv2d_valid(self, img, k):
+        img = np.ascontiguousarray(img, np.uint8)
+        k = np.ascontiguousarray(k, np.int32)
+        ks = k.shape[0]
+        h, w = img.shape
+        out = np.empty((max(h - ks + 1, 0), max(w - ks + 1, 0)), np.int32)
+        st = self.lib.ref_conv2d_valid(_p(img), w, h, _p(k), ks, _p(out))
+        return st, out
 
     def sobel3_2d(self, img):
         img = np.ascontiguousarray(img, np.uint8)

@@ -370,4 +370,28 @@ double ref_measure_run_stream_3x3(const std::uint8_t* img, int w, int h, int lan
     return rep.mean_s;
 }
 
+// conv2d_valid (oracle.hpp:19-49) with an arbitrary 5x5 / 3x3 kernel.
+int ref_conv2d_valid(const std::uint8_t* img, int w, int h, const std::int32_t* k, int ksize,
+                     std::int32_t* out) {
+    try {
+        const sobel5::GrayPlane g(w, h, std::vector<std::uint8_t>(img, img + std::size_t(w) * h));
+        sobel5::SignedPlane r;
+        if (ksize == 5) {
+            sobel5::Kernel5 kk;
+            for (int i = 0; i < 5; ++i)
+                for (int j = 0; j < 5; ++j) kk.w[i][j] = k[i * 5 + j];
+            r = sobel5::conv2d_valid(g, kk);
+        } else {
+            sobel5::Kernel3 kk;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) kk.w[i][j] = k[i * 3 + j];
+            r = sobel5::conv2d_valid(g, kk);
+        }
+        copy_plane(r, out);
+        return 0;
+    } catch (const std::exception& e) {
+        return classify(e);
+    }
+}
+
 }  // extern "C"

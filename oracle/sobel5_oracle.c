@@ -100,6 +100,22 @@ int oracle_conv2d_valid(const uint8_t* img, int w, int h, const int32_t k[25], i
     return 0;
 }
 
+/* conv2d_valid(GrayPlane, Kernel3): oracle.hpp:35-49 (the same window sum
+ * at radius 1). */
+int oracle_conv2d_valid3(const uint8_t* img, int w, int h, const int32_t k[9], int32_t* out) {
+    if (w < 3 || h < 3) return 1;
+    const int ow = w - 2, oh = h - 2;
+    for (int y = 0; y < oh; ++y)
+        for (int x = 0; x < ow; ++x) {
+            int64_t acc = 0;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j)
+                    acc += (int64_t)k[i * 3 + j] * img[(size_t)(y + i) * w + x + j];
+            out[(size_t)y * ow + x] = (int32_t)acc;
+        }
+    return 0;
+}
+
 /* Magnitude, oracle.hpp:89-96 and pipeline.hpp:401-407: left-to-right sum
  * of products in double, then sqrt. */
 static double magnitude(int32_t gx, int32_t gy, int32_t gd, int32_t gdt) {

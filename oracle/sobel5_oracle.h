@@ -49,6 +49,8 @@ void oracle_make_stream_taps(int64_t a, int64_t b, int64_t m, int64_t n, oracle_
 /* conv2d_valid(GrayPlane, Kernel5) (oracle.hpp:19-33): valid-mode
  * correlation, int64 accumulator cast to int32.  out is (w-4)*(h-4). */
 int oracle_conv2d_valid(const uint8_t* img, int w, int h, const int32_t k[25], int32_t* out);
+/* conv2d_valid(GrayPlane, Kernel3): oracle.hpp:35-49. */
+int oracle_conv2d_valid3(const uint8_t* img, int w, int h, const int32_t k[9], int32_t* out);
 
 /* sobel5_4d() (oracle.hpp:82-98).  Any output pointer may be NULL. */
 int oracle_sobel5_4d(const uint8_t* img, int w, int h, int64_t a, int64_t b, int64_t m,

@@ -56,6 +56,11 @@ class IpcHandle(C.Structure):
     _fields_ = [("bytes", C.c_ubyte * 64), ("offset", C.c_int64)]
 
 
+class LaunchInfo(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("band", "tma_load", "kernel", "grid_x", "grid_y",
+                                         "grid_z")]
+
+
 class Counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "row_conv5_f", "row_conv5_h", "row_conv5_k0", "row_conv5_k1",
@@ -79,7 +84,8 @@ EXPORTS = (
     "sobel3_launch", "sobel3_detect", "sobel3_plan_counters", "sobel3_run_host",
     "sobel5_quantize_host", "sobel5_run_host_begin", "sobel5_run_host_finish",
     "sobel5_run_host_chunk", "sobel5_run_host_staging", "sobel5_kernel_for_taps",
-    "sobel3_run_host_begin", "sobel5_ctx_trim",
+    "sobel3_run_host_begin", "sobel5_ctx_trim", "sobel5_last_launch",
+    "sobel5_conv2d_valid", "sobel5_conv2d_valid_host", "sobel5_dense_4d", "sobel5_dense_4d_host",
 )
 
 _lib = None
@@ -105,6 +111,16 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.sobel5_status_string.argtypes = [i32]
     L.sobel5_status_string.restype = C.c_char_p
     L.sobel5_launch_count.restype = C.c_uint64
+    L.sobel5_last_launch.argtypes = [C.POINTER(LaunchInfo)]
+    L.sobel5_last_launch.restype = i32
+    L.sobel5_conv2d_valid.argtypes = [vp, i64, i32, i32, vp, i32, vp, i64, vp]
+    L.sobel5_conv2d_valid.restype = i32
+    L.sobel5_conv2d_valid_host.argtypes = [vp, vp, i32, i32, vp, i32, vp]
+    L.sobel5_conv2d_valid_host.restype = i32
+    L.sobel5_dense_4d.argtypes = [vp, i64, i32, i32, vp, C.POINTER(Planes), vp]
+    L.sobel5_dense_4d.restype = i32
+    L.sobel5_dense_4d_host.argtypes = [vp, vp, i32, i32, vp, C.POINTER(Planes)]
+    L.sobel5_dense_4d_host.restype = i32
     L.sobel5_make_taps.argtypes = [i64] * 4 + [C.POINTER(Taps)]
     L.sobel5_make_taps.restype = i32
     L.sobel5_plan_counters.argtypes = [i32, vp, i32, C.POINTER(Taps), i32, C.POINTER(Counters)]

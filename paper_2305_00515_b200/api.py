@@ -12,6 +12,8 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import sys
+import threading
 from dataclasses import dataclass, field
 from fractions import Fraction
 
@@ -283,14 +285,31 @@ class Context:
         return st, u8, res, d
 
 
-_default_ctx: Context | None = None
+_tls = threading.local()
 
 
-def default_context() -> Context:
-    global _default_ctx
-    if _default_ctx is None:
-        _default_ctx = Context(0)
-    return _default_ctx
+def _current_device() -> int:
+    """The caller's current CUDA device (torch's, when torch is in use)."""
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_available():
+        return torch.cuda.current_device()
+    return 0
+
+
+def default_context(device: int | None = None) -> Context:
+    """One context per host thread and device, like the C++ mirror's
+    gpu::thread_context() (include/sobel5_b200/stream.hpp): a sobel5_ctx is
+    not thread-safe (pinned staging, streams, the pending split call), and
+    ctypes releases the GIL during the C call, so threads must not share
+    one.  The reference's run_stream is reentrant (pipeline.hpp:452)."""
+    dev = _current_device() if device is None else device
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    ctx = ctxs.get(dev)
+    if ctx is None:
+        ctx = ctxs[dev] = Context(dev)
+    return ctx
 
 
 def run_stream(img: np.ndarray, taps_or_params, plan: StripPlan, prefetch: Prefetch,
@@ -323,14 +342,46 @@ def run_stream(img: np.ndarray, taps_or_params, plan: StripPlan, prefetch: Prefe
                         plan_counters(h, plan, taps, prefetch))
 
 
-def sobel5_4d(img: np.ndarray, params: FilterParams = FilterParams()) -> StreamResult:
-    """oracle.hpp:82-98 (the dense 4-direction oracle): run_stream equals it
-    for every valid parameter set, so the planes come from the GPU path."""
+def conv2d_valid(img: np.ndarray, kernel, ctx: Context | None = None) -> np.ndarray:
+    """oracle.hpp:19-49 on the GPU (sobel5_conv2d_valid_host): valid-mode
+    correlation with a 5x5 or 3x3 integer kernel, int32 result."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    k = np.ascontiguousarray(kernel, dtype=np.int32)
+    if k.ndim != 2 or k.shape[0] != k.shape[1] or k.shape[0] not in (3, 5):
+        raise DimMismatch("kernel must be 5x5 or 3x3")
+    ks = k.shape[0]
+    h, w = img.shape
+    if w < ks or h < ks:
+        raise ImageTooSmall(f"conv2d_valid needs at least {ks}x{ks}, got {w}x{h}")
+    out = np.empty((h - ks + 1, w - ks + 1), np.int32)
+    ctx = ctx or default_context()
+    check(_abi.load().sobel5_conv2d_valid_host(ctx.handle, img.ctypes.data, w, h, k.ctypes.data, ks,
+                                               out.ctypes.data), "conv2d_valid")
+    return out
+
+
+def sobel5_4d(img: np.ndarray, params: FilterParams = FilterParams(),
+              ctx: Context | None = None) -> StreamResult:
+    """oracle.hpp:82-98: the four dense correlations with the materialised
+    kernels plus the double magnitude, on the GPU (sobel5_dense_4d_host) --
+    the oracle's algorithm, independent of run_stream's streaming kernels.
+    counters are empty (the oracle keeps none)."""
     img = np.ascontiguousarray(img, dtype=np.uint8)
     h, w = img.shape
     if w < 5 or h < 5:
         raise ImageTooSmall(f"conv2d_valid needs at least 5x5, got {w}x{h}")
-    return run_stream(img, params, plan_strips(w, w, 2), Prefetch.on)
+    validate_params(params)
+    k = np.ascontiguousarray(np.stack([materialize(params, d) for d in range(4)]), np.int32)
+    ow, oh = w - 4, h - 4
+    res = {n: np.empty((oh, ow), np.int32) for n in ("gx", "gy", "gd", "gdt")}
+    res["g"] = np.empty((oh, ow), np.float64)
+    pl = Planes(pitch=ow)
+    for n, v in res.items():
+        setattr(pl, n, v.ctypes.data)
+    ctx = ctx or default_context()
+    check(_abi.load().sobel5_dense_4d_host(ctx.handle, img.ctypes.data, w, h, k.ctypes.data,
+                                           C.byref(pl)), "sobel5_4d")
+    return StreamResult(res["gx"], res["gy"], res["gd"], res["gdt"], res["g"], {})
 
 
 def diag_via_sum_diff(img: np.ndarray, params: FilterParams = FilterParams()):
@@ -654,6 +705,14 @@ def detect3_device(d_in, in_pitch: int, width: int, height: int, prefetch: int, 
                                     C.byref(pl), out_frame_stride,
                                     None if scratch is None else scratch.data_ptr(), s),
           "sobel3_detect")
+
+
+def last_launch() -> dict:
+    """Geometry of this thread's last 5x5 stencil launch (sobel5_last_launch):
+    band, tma_load, kernel (index into KERNELS), grid_x/y/z."""
+    info = _abi.LaunchInfo()
+    check(_abi.load().sobel5_last_launch(C.byref(info)), "sobel5_last_launch")
+    return {n: int(getattr(info, n)) for n, _ in _abi.LaunchInfo._fields_}
 
 
 def launch_count() -> int:

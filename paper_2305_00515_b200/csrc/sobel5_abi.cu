@@ -26,6 +26,7 @@ using namespace sobel5_b200;
 namespace {
 
 std::atomic<uint64_t> g_launches{0};
+thread_local sobel5_launch_info t_last_launch{};
 
 constexpr int64_t kMaxWeight = int64_t{1} << 15;  // filter_algebra.hpp:148
 
@@ -379,6 +380,9 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
         if (kp.band > 32) kp.tma_load = 0;  // the shared-memory band holds 36 rows
     }
     const dim3 grid2(grid.x, static_cast<unsigned>((out_h + kp.band - 1) / kp.band), grid.z);
+    t_last_launch = sobel5_launch_info{kp.band, kp.tma_load, sobel5_kernel_for_taps(taps),
+                                       static_cast<int>(grid2.x), static_cast<int>(grid2.y),
+                                       static_cast<int>(grid2.z)};
     const cudaError_t e = dispatch(kp, grid2, prefetch, taps_are_default(*taps), choose_mag(*taps),
                                    static_cast<cudaStream_t>(stream));
     return map_cuda(e);
@@ -452,6 +456,12 @@ extern "C" {
 int sobel5_abi_version(void) { return SOBEL5_GPU_ABI_VERSION; }
 
 uint64_t sobel5_launch_count(void) { return g_launches.load(); }
+
+sobel5_status sobel5_last_launch(sobel5_launch_info* out) {
+    if (!out) return SOBEL5_INVALID_ARG;
+    *out = t_last_launch;
+    return SOBEL5_OK;
+}
 
 const char* sobel5_status_string(int status) {
     switch (status) {

@@ -232,11 +232,26 @@ void par_copy(sobel5_ctx* ctx, void* dst, const void* src, size_t n) {
     });
 }
 
+// Pinned staging one host call may use (the SOBEL5_STAGING_MAX_MB cap counts
+// the input and every plane of the call).  take(n) reserves n bytes if they
+// fit; what does not fit is copied straight from / to pageable memory (the
+// driver stages it: slower, but bounded).
+struct StageBudget {
+    size_t left = staging_cap();
+    bool take(size_t n) {
+        if (n > left) return false;
+        left -= n;
+        return true;
+    }
+};
+
 // A pageable input is first copied into pinned staging (in parallel) so the
 // uploads that follow are true asynchronous DMA; *src is what to upload.
-sobel5_status stage_input(sobel5_ctx* ctx, const uint8_t* h_in, size_t n, const uint8_t** src) {
+// Without room in the budget it is uploaded from pageable memory directly.
+sobel5_status stage_input(sobel5_ctx* ctx, const uint8_t* h_in, size_t n, const uint8_t** src,
+                          StageBudget& budget) {
     *src = h_in;
-    if (is_pinned(h_in)) return SOBEL5_OK;
+    if (is_pinned(h_in) || !budget.take(n)) return SOBEL5_OK;
     CK(ensure_host(&ctx->h_in_stage, &ctx->h_in_stage_bytes, n));
     par_copy(ctx, ctx->h_in_stage, h_in, n);
     *src = static_cast<const uint8_t*>(ctx->h_in_stage);
@@ -246,12 +261,14 @@ sobel5_status stage_input(sobel5_ctx* ctx, const uint8_t* h_in, size_t n, const 
 // Enqueues the download of `rows` rows of plane slot i (device pitch dpitch
 // elements) to tightly packed host memory: straight into a pinned dst, or
 // into the pinned staging h_stage[i], recorded in *staged for
-// finish_staged() once the stream has synchronised.
+// finish_staged() once the stream has synchronised (pageable destinations
+// beyond the staging budget are written by the driver directly).
 sobel5_status download_plane(sobel5_ctx* ctx, int i, void* dst, const void* d_src, int out_w,
-                             int rows, int64_t dpitch, cudaStream_t s, void* staged[7]) {
+                             int rows, int64_t dpitch, cudaStream_t s, void* staged[7],
+                             StageBudget& budget) {
     const size_t es = kElem[i], row = static_cast<size_t>(out_w) * es;
     void* to = dst;
-    if (!is_pinned(dst)) {
+    if (!is_pinned(dst) && budget.take(row * rows)) {
         CK(ensure_host(&ctx->h_stage[i], &ctx->h_stage_bytes[i], row * rows));
         to = ctx->h_stage[i];
         staged[i] = dst;
@@ -276,7 +293,8 @@ void finish_staged(sobel5_ctx* ctx, void* const staged[7], int out_w, int rows) 
 // two-direction one, sobel3_launch, taps unused.)
 sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
                              const sobel5_taps* taps, int prefetch, unsigned mask,
-                             void* const dst[7], int* chunk_out, int* n_chunks_out, int op = 5) {
+                             void* const dst[7], int* chunk_out, int* n_chunks_out,
+                             StageBudget& budget, int op = 5) {
     const int R = op == 3 ? 1 : 2;  // operator radius
     const int out_w = width - 2 * R, out_h = height - 2 * R;
     const int64_t in_pitch = round_up(width, 128);
@@ -284,7 +302,8 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
     CK(ensure(reinterpret_cast<void**>(&ctx->d_in), &ctx->d_in_bytes,
               static_cast<size_t>(in_pitch) * height));
     const uint8_t* src_in = nullptr;
-    if (const sobel5_status st = stage_input(ctx, h_in, static_cast<size_t>(width) * height, &src_in);
+    if (const sobel5_status st =
+            stage_input(ctx, h_in, static_cast<size_t>(width) * height, &src_in, budget);
         st != SOBEL5_OK)
         return st;
     sobel5_planes dp{};
@@ -481,25 +500,18 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     unsigned mask = 0;
     void* direct[7] = {};  // pinned destinations: DMA straight into them
     void* staged[7] = {};  // pageable ones: through pinned staging
-    size_t stage_bytes = 0;
+    StageBudget budget;    // the planes first, then the input if it still fits
     for (int i = 0; i < 7; ++i) {
         if (!hp[i]) continue;
         mask |= 1u << i;
-        if (is_pinned(hp[i])) {
-            direct[i] = hp[i];
-        } else {
-            const size_t b = static_cast<size_t>(out_w) * out_h * kElem[i];
-            if (stage_bytes + b <= staging_cap()) {
-                staged[i] = hp[i];
-                stage_bytes += b;
-            } else {
-                direct[i] = hp[i];  // over the staging cap: driver-staged pageable copy
-            }
-        }
+        if (!is_pinned(hp[i]) && budget.take(static_cast<size_t>(out_w) * out_h * kElem[i]))
+            staged[i] = hp[i];
+        else
+            direct[i] = hp[i];  // pinned, or over the staging cap: driver-staged copy
     }
     int chunk = 0, n_chunks = 0;
-    const sobel5_status st =
-        enqueue_stream(ctx, h_in, width, height, taps, prefetch, mask, direct, &chunk, &n_chunks);
+    const sobel5_status st = enqueue_stream(ctx, h_in, width, height, taps, prefetch, mask, direct,
+                                            &chunk, &n_chunks, budget);
     if (st != SOBEL5_OK) return st;
     return drain_stream(ctx, out_w, out_h, chunk, n_chunks, staged, diag_out);
 }
@@ -537,12 +549,13 @@ sobel5_status begin_common(sobel5_ctx* ctx, const uint8_t* h_in, int width, int 
     for (int i = 0; i < 7; ++i)
         if ((plane_mask >> i) & 1u)
             stage_bytes += static_cast<size_t>(width - 2 * R) * (height - 2 * R) * kElem[i];
-    if (stage_bytes > staging_cap()) return SOBEL5_OUT_OF_MEMORY;  // callers use run_host
+    StageBudget budget;  // the planes must fit; the input is staged if it still does
+    if (!budget.take(stage_bytes)) return SOBEL5_OUT_OF_MEMORY;  // callers use run_host
     CK(cudaSetDevice(ctx->device));
     void* none[7] = {};
     int chunk = 0, n_chunks = 0;
     const sobel5_status st = enqueue_stream(ctx, h_in, width, height, taps, prefetch, plane_mask,
-                                            none, &chunk, &n_chunks, op);
+                                            none, &chunk, &n_chunks, budget, op);
     if (st != SOBEL5_OK) {
         // drain whatever was enqueued so the context stays usable
         cudaStreamSynchronize(ctx->s_h2d);
@@ -660,8 +673,10 @@ sobel5_status sobel5_detect_host(sobel5_ctx* ctx, const uint8_t* h_in, int width
     CK(ensure(&ctx->d_scratch, &ctx->d_scratch_bytes,
               sobel5_detect_scratch_bytes(out_h, dpitch, 0, 1)));
     CK(cudaMemsetAsync(ctx->d_diag, 0, sizeof(sobel5_diag), ctx->s_comp));
+    StageBudget budget;
     const uint8_t* src_in = nullptr;
-    if (const sobel5_status st = stage_input(ctx, h_in, static_cast<size_t>(width) * height, &src_in);
+    if (const sobel5_status st =
+            stage_input(ctx, h_in, static_cast<size_t>(width) * height, &src_in, budget);
         st != SOBEL5_OK)
         return st;
     CK(cudaMemcpy2DAsync(ctx->d_in, in_pitch, src_in, width, width, height, cudaMemcpyHostToDevice,
@@ -677,7 +692,7 @@ sobel5_status sobel5_detect_host(sobel5_ctx* ctx, const uint8_t* h_in, int width
     for (int i = 0; i < 7; ++i) {
         if (!hp[i]) continue;
         if (const sobel5_status ds = download_plane(ctx, i, hp[i], ctx->d_plane[i], out_w, out_h,
-                                                    dpitch, ctx->s_comp, staged);
+                                                    dpitch, ctx->s_comp, staged, budget);
             ds != SOBEL5_OK)
             return ds;
     }
@@ -704,22 +719,19 @@ sobel5_status sobel3_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     unsigned mask = 0;
     void* direct[7] = {};
     void* staged[7] = {};
-    size_t stage_bytes = 0;
+    StageBudget budget;
     for (int i = 0; i < 7; ++i) {
         if (!hp[i]) continue;
         mask |= 1u << i;
-        const size_t b = static_cast<size_t>(out_w) * out_h * kElem[i];
-        if (!is_pinned(hp[i]) && stage_bytes + b <= staging_cap()) {
+        if (!is_pinned(hp[i]) && budget.take(static_cast<size_t>(out_w) * out_h * kElem[i]))
             staged[i] = hp[i];
-            stage_bytes += b;
-        } else {
+        else
             direct[i] = hp[i];
-        }
     }
     if (!mask) return SOBEL5_OK;
     int chunk = 0, n_chunks = 0;
     const sobel5_status st = enqueue_stream(ctx, h_in, width, height, nullptr, prefetch, mask,
-                                            direct, &chunk, &n_chunks, 3);
+                                            direct, &chunk, &n_chunks, budget, 3);
     if (st != SOBEL5_OK) return st;
     return drain_stream(ctx, out_w, out_h, chunk, n_chunks, staged, nullptr);
 }
@@ -736,8 +748,10 @@ sobel5_status sobel5_quantize_host(sobel5_ctx* ctx, const void* h_plane, int kin
     CK(ensure(&ctx->d_plane[4], &ctx->d_plane_bytes[4], n * 8));
     CK(ensure(&ctx->d_plane[6], &ctx->d_plane_bytes[6], n));
     CK(ensure(&ctx->d_scratch, &ctx->d_scratch_bytes, sobel5_detect_scratch_bytes(0, 0, 0, 1)));
+    StageBudget budget;
     const uint8_t* src = nullptr;
-    if (const sobel5_status ss = stage_input(ctx, static_cast<const uint8_t*>(h_plane), n * es, &src);
+    if (const sobel5_status ss =
+            stage_input(ctx, static_cast<const uint8_t*>(h_plane), n * es, &src, budget);
         ss != SOBEL5_OK)
         return ss;
     CK(cudaMemcpyAsync(ctx->d_plane[4], src, n * es, cudaMemcpyHostToDevice, ctx->s_comp));
@@ -748,11 +762,96 @@ sobel5_status sobel5_quantize_host(sobel5_ctx* ctx, const void* h_plane, int kin
     if (st != SOBEL5_OK) return st;
     void* staged[7] = {};
     if (const sobel5_status ds = download_plane(ctx, 6, h_u8, ctx->d_plane[6], width, height, width,
-                                                ctx->s_comp, staged);
+                                                ctx->s_comp, staged, budget);
         ds != SOBEL5_OK)
         return ds;
     CK(cudaStreamSynchronize(ctx->s_comp));
     finish_staged(ctx, staged, width, height);
+    return SOBEL5_OK;
+}
+
+sobel5_status sobel5_conv2d_valid_host(sobel5_ctx* ctx, const uint8_t* h_in, int width,
+                                       int height, const int32_t* kernel, int ksize,
+                                       int32_t* h_out) {
+    if (!ctx) return SOBEL5_INVALID_ARG;
+    if (ksize != 3 && ksize != 5) return SOBEL5_INVALID_ARG;
+    if (width < ksize || height < ksize) return SOBEL5_IMAGE_TOO_SMALL;  // oracle.hpp:20-22
+    if (!h_in || !kernel || !h_out || ctx->pend.active) return SOBEL5_INVALID_ARG;
+    CK(cudaSetDevice(ctx->device));
+    const int out_w = width - ksize + 1, out_h = height - ksize + 1;
+    const int64_t in_pitch = round_up(width, 128);
+    CK(ensure(reinterpret_cast<void**>(&ctx->d_in), &ctx->d_in_bytes,
+              static_cast<size_t>(in_pitch) * height));
+    // the int32 result goes through the gx slot, tightly packed
+    CK(ensure(&ctx->d_plane[0], &ctx->d_plane_bytes[0], static_cast<size_t>(out_w) * out_h * 4));
+    StageBudget budget;
+    const uint8_t* src_in = nullptr;
+    if (const sobel5_status st =
+            stage_input(ctx, h_in, static_cast<size_t>(width) * height, &src_in, budget);
+        st != SOBEL5_OK)
+        return st;
+    CK(cudaMemcpy2DAsync(ctx->d_in, in_pitch, src_in, width, width, height, cudaMemcpyHostToDevice,
+                         ctx->s_comp));
+    const sobel5_status st =
+        sobel5_conv2d_valid(ctx->d_in, in_pitch, width, height, kernel, ksize,
+                            static_cast<int32_t*>(ctx->d_plane[0]), out_w, ctx->s_comp);
+    if (st != SOBEL5_OK) return st;
+    void* staged[7] = {};
+    if (const sobel5_status ds = download_plane(ctx, 0, h_out, ctx->d_plane[0], out_w, out_h,
+                                                out_w, ctx->s_comp, staged, budget);
+        ds != SOBEL5_OK)
+        return ds;
+    CK(cudaStreamSynchronize(ctx->s_comp));
+    finish_staged(ctx, staged, out_w, out_h);
+    return SOBEL5_OK;
+}
+
+sobel5_status sobel5_dense_4d_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
+                                   const int32_t* kernels, const sobel5_planes* h_out) {
+    if (!ctx) return SOBEL5_INVALID_ARG;
+    if (width < 5 || height < 5) return SOBEL5_IMAGE_TOO_SMALL;  // oracle.hpp:20-22
+    if (!h_in || !kernels || !h_out || h_out->g32 || h_out->u8 || ctx->pend.active)
+        return SOBEL5_INVALID_ARG;
+    const int out_w = width - 4, out_h = height - 4;
+    if (h_out->pitch != out_w) return SOBEL5_INVALID_ARG;
+    CK(cudaSetDevice(ctx->device));
+    const int64_t in_pitch = round_up(width, 128);
+    CK(ensure(reinterpret_cast<void**>(&ctx->d_in), &ctx->d_in_bytes,
+              static_cast<size_t>(in_pitch) * height));
+    void* hp[7];
+    planes_array(h_out, hp);
+    sobel5_planes dp{};
+    dp.pitch = out_w;  // tightly packed device planes
+    void** dslots[5] = {reinterpret_cast<void**>(&dp.gx), reinterpret_cast<void**>(&dp.gy),
+                        reinterpret_cast<void**>(&dp.gd), reinterpret_cast<void**>(&dp.gdt),
+                        reinterpret_cast<void**>(&dp.g)};
+    for (int i = 0; i < 5; ++i) {
+        if (!hp[i]) continue;
+        CK(ensure(&ctx->d_plane[i], &ctx->d_plane_bytes[i],
+                  static_cast<size_t>(out_w) * out_h * kElem[i]));
+        *dslots[i] = ctx->d_plane[i];
+    }
+    StageBudget budget;
+    const uint8_t* src_in = nullptr;
+    if (const sobel5_status st =
+            stage_input(ctx, h_in, static_cast<size_t>(width) * height, &src_in, budget);
+        st != SOBEL5_OK)
+        return st;
+    CK(cudaMemcpy2DAsync(ctx->d_in, in_pitch, src_in, width, width, height, cudaMemcpyHostToDevice,
+                         ctx->s_comp));
+    const sobel5_status st = sobel5_dense_4d(ctx->d_in, in_pitch, width, height, kernels, &dp,
+                                             ctx->s_comp);
+    if (st != SOBEL5_OK) return st;
+    void* staged[7] = {};
+    for (int i = 0; i < 5; ++i) {
+        if (!hp[i]) continue;
+        if (const sobel5_status ds = download_plane(ctx, i, hp[i], ctx->d_plane[i], out_w, out_h,
+                                                    out_w, ctx->s_comp, staged, budget);
+            ds != SOBEL5_OK)
+            return ds;
+    }
+    CK(cudaStreamSynchronize(ctx->s_comp));
+    finish_staged(ctx, staged, out_w, out_h);
     return SOBEL5_OK;
 }
 

@@ -143,3 +143,23 @@ def test_oracle_vs_compiled_reference_random(oracle, reference):
         st, out, _ = oracle.run_stream(img, pyoracle.Taps.from_dict(KNOWN["default_taps"]))
         for k in PLANES:
             np.testing.assert_array_equal(out[k], ref[k], err_msg=f"{k} {w}x{h}")
+
+
+def test_conv2d_valid_restatement_matches_reference(oracle, reference):
+    """oracle_conv2d_valid / _valid3 (oracle.hpp:19-49) against the compiled
+    reference for arbitrary 5x5 and 3x3 kernels, int32 extremes included
+    (the int64 sum's cast to int32 wraps)."""
+    rng = np.random.default_rng(21)
+    for ks in (5, 3):
+        for t in range(24):
+            img = rng.integers(0, 256, (int(rng.integers(ks, 40)), int(rng.integers(ks, 70))),
+                               dtype=np.uint8)
+            if t % 3 == 0:
+                k = rng.integers(-2**31, 2**31, (ks, ks), dtype=np.int64).astype(np.int32)
+            else:
+                k = rng.integers(-60, 60, (ks, ks)).astype(np.int32)
+            st, ref = reference.conv2d_valid(img, k)
+            assert st == 0
+            np.testing.assert_array_equal(oracle.conv2d_valid(img, k), ref)
+        st, _ = reference.conv2d_valid(np.zeros((ks - 1, 9), np.uint8), np.zeros((ks, ks), np.int32))
+        assert st == 13  # ImageTooSmall

@@ -10,3 +10,7 @@ ${CXX:-g++} -std=c++20 -O2 -Wall -Wextra -I"$ROOT/include" "$ROOT/tests/cpp/test
 ${CXX:-g++} -std=c++20 -O2 -Wall -Wextra -I"$ROOT/include" -I/usr/local/cuda/include "$ROOT/tools/cpp_e2e.cpp" \
   -L"$LIB" -lsobel5_b200 -Wl,-rpath,"$LIB" -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,/usr/local/cuda/lib64 \
   -o "$ROOT/build/cpp_e2e"
+# SPEC acceptance criteria as a reference-style program (only "sobel5/*.hpp"
+# includes): the same source also builds against the reference headers
+${CXX:-g++} -std=c++20 -O2 -Wall -Wextra -I"$ROOT/include" "$ROOT/tests/cpp/acceptance.cpp" \
+  -L"$LIB" -lsobel5_b200 -Wl,-rpath,"$LIB" -o "$ROOT/build/acceptance"
