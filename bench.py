@@ -56,7 +56,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="8k", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: 8k (C3) at N=1, 32k-bands (C5, one image row-band "
+                         "partitioned over the ranks) at N>1")
     ap.add_argument("--contract", default="sr", choices=sorted(OUT_BYTES))
     ap.add_argument("--prefetch", type=int, default=1)
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl", "gloo"],
@@ -70,7 +72,23 @@ def parse():
                          "code path on a one-GPU box; numbers are not scaling numbers)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="budget of CPU work for the cpu_baseline sample")
-    return ap.parse_args()
+    ap.add_argument("--no-cpu-matrix", action="store_true",
+                    help="skip the BASELINE.md section 2 CPU matrix (C1-C3 x lanes x workers)")
+    a = ap.parse_args()
+    if a.workload is None:
+        a.workload = "32k-bands" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "8k"
+    return a
+
+
+def base_config(a, world: int) -> dict:
+    """The workload description both arms print (identical dicts)."""
+    wl = WORKLOADS[a.workload]
+    frames = wl["frames"] if wl["frames"] == 1 else max(1, wl["frames"] // world)
+    return {"workload": wl["name"], "frames_per_rank": frames,
+            "contract": a.contract + " (" + "+".join(CONTRACT_PLANES[a.contract]) + ")",
+            "prefetch": bool(a.prefetch),
+            "parallelism": (f"row-bands x{world} ({a.transport} halos)"
+                            if a.workload == "32k-bands" else f"batch-split x{world}")}
 
 
 def dist_env():
@@ -164,9 +182,11 @@ def cpu_reference(w, h, frames, seconds, max_iters=None):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
     cores = os.cpu_count() or 1
+    rows = h if w * h <= 40_000_000 else max(5, int(40_000_000 // w))  # 32K: a band of rows
+    unit = "frame" if rows == h else f"{rows}-row band of the frame"
     if pyoracle.ref_available():
         R = pyoracle.Reference()
-        img = R.synth_random(w, h, 1)
+        img = R.synth_random(w, rows, 1)
         t0 = time.perf_counter()
         mean1, _ = R.measure_run_stream(img, lanes=256, prefetch=True, workers=cores, iters=1)
         first = time.perf_counter() - t0
@@ -177,23 +197,30 @@ def cpu_reference(w, h, frames, seconds, max_iters=None):
                                         iters=iters)
         kind = "reference"
         sample = (f"{iters} timed + 1 warm-up reference run_stream calls (lanes 256, prefetch on, "
-                  f"workers {cores}) on one {w}x{h} synth_random frame; first call {first:.2f}s")
+                  f"workers {cores}) on one {w}x{rows} synth_random {unit}; first call "
+                  f"{first:.2f}s")
         cores_used = cores
     else:  # oracle port, single thread
         O = pyoracle.Oracle()
-        img = O.synth_random(w, h, 1)
+        img = O.synth_random(w, rows, 1)
         t0 = time.perf_counter()
         O.run_stream(img)
         mean = time.perf_counter() - t0
         sd, kind, cores_used = 0.0, "port", 1
-        sample = f"1 oracle-port run_stream call on one {w}x{h} frame (reference not built)"
-    gpx = w * h / mean / 1e9
+        sample = f"1 oracle-port run_stream call on one {w}x{rows} {unit} (reference not built)"
+    gpx = w * rows / mean / 1e9
     return {"value": gpx, "unit": UNIT, "cores": cores_used, "kind": kind, "sample": sample,
             "mean_s_per_frame": mean, "stddev_s": sd,
             "note": f"per-frame rate; a {frames}-frame workload scales linearly"}
 
 
 def run_reference_arm(a):
+    """The reference's own CPU implementation of the path (run_stream from its
+    headers, oracle/_ref; the C oracle port where it is absent) on this
+    host's cores, timed with the reference's measure(): W warm-up runs then
+    exactly K timed steps, each step a bounded sample of the workload --
+    whole frames (C3: one 8K frame; C4: frames of the batch) or, for the
+    32K image, a band of its rows -- sized to ~0.5 s.  Rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -202,36 +229,88 @@ def run_reference_arm(a):
     import pyoracle
     cores = os.cpu_count() or 1
     w, h = wl["w"], wl["h"]
-    if pyoracle.ref_available():
-        R = pyoracle.Reference()
-        img = R.synth_random(w, h, 1)
-        for _ in range(max(0, min(a.warmup, 2))):
-            R.measure_run_stream(img, lanes=256, prefetch=True, workers=cores, iters=1)
-        steps = max(1, min(a.steps, 20))
-        mean, sd = R.measure_run_stream(img, lanes=256, prefetch=True, workers=cores,
-                                        iters=steps)
-        kind = "reference"
-    else:
-        O = pyoracle.Oracle()
-        img = O.synth_random(w, h, 1)
-        steps = 1
+    have_ref = pyoracle.ref_available()
+    G = pyoracle.Reference() if have_ref else pyoracle.Oracle()
+    # sample: rows of the workload's image (a whole frame where it fits)
+    rows = h
+    if w * h > 40_000_000:  # the 32K image: a band of rows
+        rows = max(5, min(h, int(40_000_000 // w)))
+    img = G.synth_random(w, rows, 1)
+
+    def run_once():
+        if have_ref:
+            return G.measure_run_stream(img, lanes=256, prefetch=True, workers=cores, iters=1)[0]
         t0 = time.perf_counter()
-        O.run_stream(img)
-        mean, sd, kind, cores = time.perf_counter() - t0, 0.0, "port", 1
-    gpx = w * h / mean / 1e9
-    sample = (f"{steps} timed reference run_stream calls (lanes 256, prefetch on, workers "
-              f"{cores}) on one {w}x{h} frame, 1 frame per step")
+        G.run_stream(img)
+        return time.perf_counter() - t0
+
+    for _ in range(a.warmup):
+        run_once()
+    if have_ref:  # measure() adds one untimed call of its own
+        mean, sd = G.measure_run_stream(img, lanes=256, prefetch=True, workers=cores,
+                                        iters=a.steps)
+        kind, cores_used = "reference", cores
+    else:
+        ts = [run_once() for _ in range(a.steps)]
+        mean, sd = statistics.mean(ts), statistics.pstdev(ts)
+        kind, cores_used = "port", 1
+    gpx = w * rows / mean / 1e9
+    unit = "frame" if rows == h else f"band of {rows} rows"
+    sample = (f"each step: one reference run_stream call (lanes 256, prefetch on, workers "
+              f"{cores_used}) on a {w}x{rows} synth_random {unit} of the workload; "
+              f"{a.warmup} warm-up + {a.steps} timed steps")
     line = {"metric": METRIC, "value": gpx, "unit": UNIT, "impl": "reference", "n_gpus": world,
-            "steps": steps, "warmup": min(a.warmup, 2), "ms_per_step": mean * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": mean * 1e3,
+            "higher_is_better": True, "scaling": "strong" if a.workload == "32k-bands" else "weak",
+            "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (synth_random seed 1)",
-            "config": {"workload": wl["name"], "contract": "sr (4 x int32 + f64 g)",
-                       "stddev_s": sd},
-            "cpu_baseline": {"value": gpx, "unit": UNIT, "cores": cores, "kind": kind,
-                             "sample": sample},
+            "config": base_config(a, world),
+            "stddev_s": sd,
+            "cpu_baseline": {"value": gpx, "unit": UNIT, "cores": cores_used, "kind": kind,
+                             "sample": sample, "host": host_cpu()},
             "e2e": {"value": gpx, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def host_cpu() -> dict:
+    """nproc and the lscpu model of this host (for the CPU numbers)."""
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def cpu_matrix(budget_s: float = 60.0) -> dict:
+    """BASELINE.md section 2's CPU matrix: the reference's run_stream at
+    lanes 32 / 256 x workers 1 / nproc and its single-thread sobel5_4d
+    oracle, on C1-C3, each through the reference's measure() (1 warm-up + 2
+    timed calls), rows in its BenchReport CSV schema (metrics.hpp:129-139)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    if not pyoracle.ref_available():
+        return {"skipped": "oracle/_ref not built"}
+    R = pyoracle.Reference()
+    cores = os.cpu_count() or 1
+    rows, t_start = [], time.perf_counter()
+    for (w, h) in ((1920, 1080), (3840, 2160), (7680, 4320)):
+        img = R.synth_random(w, h, 1)
+        for which, lanes, workers in (("fast", 32, 1), ("fast", 256, 1), ("fast", 32, cores),
+                                      ("fast", 256, cores), ("oracle", 0, 1)):
+            if rows and time.perf_counter() - t_start > budget_s:
+                break
+            _, row = R.measure_csv(img, which, lanes or 32, True, workers, 2)
+            rows.append({"lanes": lanes or None, "workers": workers, "csv": row})
+    return {"csv_header": "label,width,height,iters,mean_s,stddev_s,mps,mps_per_core",
+            "rows": rows, "host": host_cpu(),
+            "note": "reference headers compiled -O3 -DNDEBUG (oracle/_ref); fast-5x5 = "
+                    "run_stream prefetch on, oracle-5x5 = sobel5_4d; mps = megapixels/s"}
 
 
 # ---- our arm ------------------------------------------------------------------------------
@@ -330,8 +409,9 @@ def main():
     # the device time of the steps without Python's per-launch host cost
     # between them, as a production loop over frames would issue them.
     # Host-synchronising transports (nccl / gloo halos) run as a plain loop.
-    use_graph = not a.no_graph and not (a.workload == "32k-bands" and a.transport != "peer"
-                                        and world > 1)
+    # (the peer transport orders ranks with per-step flag values, which a
+    # graph replay would freeze at their capture-time values)
+    use_graph = not a.no_graph and not (a.workload == "32k-bands" and world > 1)
     run_stream_obj = stream  # CUDAGraph.replay() launches on the current stream
     if use_graph:
         gs = torch.cuda.Stream(dev)
@@ -505,6 +585,55 @@ def main():
                        "overlap on 3 streams; every rank one image, max time over ranks"}
         ctx.close()
 
+    elif not a.no_e2e and a.workload == "32k-bands":
+        # C5 end to end, every rank at once over its own PCIe link: its band's
+        # input rows from pinned host memory, the band step (halo exchange
+        # included), and every output plane's rows streamed back into pinned
+        # host memory through a 256 MB staging buffer; wall clock, max over
+        # ranks.
+        h_body = torch.empty((plan.body_rows, pitch), dtype=torch.uint8, pin_memory=True)
+        h_body.copy_(body.cpu())
+        stage = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
+        cur = torch.cuda.current_stream(dev)
+
+        def e2e_step(i):
+            with torch.cuda.stream(cur):
+                body.copy_(h_body, non_blocking=True)
+            step(i, s_ptr)
+            with torch.cuda.stream(cur):
+                d2h = 0
+                for k, t in out.items():
+                    flat = t[: plan.out_rows].reshape(-1).view(torch.uint8)
+                    for o in range(0, flat.numel(), stage.numel()):
+                        n = min(stage.numel(), flat.numel() - o)
+                        stage[:n].copy_(flat[o:o + n], non_blocking=True)
+                        d2h += n
+            torch.cuda.synchronize()
+            return d2h
+
+        e2e_step(0)
+        n_e2e = max(2, min(a.steps, 4))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(n_e2e):
+            d2h = e2e_step(i + 1)
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device="cpu" if a.share_gpu else dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+            dd = torch.tensor([d2h], device="cpu" if a.share_gpu else dev, dtype=torch.float64)
+            dist.all_reduce(dd)
+            d2h = int(dd.item())
+        s_e2e = el / n_e2e
+        e2e = {"value": w * h / s_e2e / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": w * h, "d2h_bytes_per_step": d2h,
+               "ms_per_step": s_e2e * 1e3, "steps": n_e2e, "ranks": world,
+               "path": "RowBandPartition.run per rank: band rows H2D from pinned memory, band "
+                       "kernel with halos, every output plane D2H through a 256 MB pinned "
+                       "staging buffer; wall clock, max over ranks"}
+
     # the drop-in C++ API end to end (tools/cpp_e2e.cpp): sobel5::run_stream
     # returning freshly allocated StreamResult planes, as a reference user calls it
     e2e_cpp = None
@@ -528,8 +657,11 @@ def main():
             e2e_cpp = {"error": str(ex)[:200]}
 
     cpu = None
-    if rank == 0 and not a.no_cpu_baseline:
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:  # rank 0 at N=1 only
         cpu = cpu_reference(w, h, frames, a.cpu_seconds)
+        cpu["host"] = host_cpu()
+        if world == 1 and not a.no_cpu_matrix:
+            cpu["matrix"] = cpu_matrix()
 
     if rank == 0:
         line = {
@@ -537,16 +669,12 @@ def main():
             "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (synth_random generated on device, reference generator)",
-            "config": {"workload": wl["name"], "frames_per_rank": frames,
-                       "contract": a.contract + " (" + "+".join(planes_names) + ")",
-                       "prefetch": bool(a.prefetch),
-                       "timed_as": ("one CUDA graph of the K steps (captured after warm-up)"
+            "config": base_config(a, world),
+            "timing": {"timed_as": ("one CUDA graph of the K steps (captured after warm-up)"
                                     if use_graph else "Python launch loop"),
-                       "parallelism": (f"row-bands x{world} ({a.transport} halos)"
-                                       if a.workload == "32k-bands" else f"batch-split x{world}"),
                        "l2": f"inputs rotated over {n_in} buffers ({n_in * in_bytes / 1e6:.0f} MB)"
-                             f" + {ow * oh * frames * OUT_BYTES[a.contract] / 1e6:.0f} MB of "
-                             "outputs per step, both > 126 MB L2",
+                             f" + {rank_out_px * OUT_BYTES[a.contract] / 1e6:.0f} MB of "
+                             "outputs per step and rank, both > 126 MB L2",
                        "hbm_gbs_achieved": achieved},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,

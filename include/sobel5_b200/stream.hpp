@@ -595,6 +595,81 @@ inline StreamResult run_stream(const GrayPlane& img, const FilterParams& p, cons
     return run_stream(img, make_stream_taps(p), plan, prefetch, workers);
 }
 
+// ---- one image over several GPUs (config C5; sobel5_mgpu_* in the C ABI) -----
+
+namespace gpu {
+
+/// RAII over sobel5_mgpu: band k of devices.size() owns input rows
+/// [k*H/n, (k+1)*H/n) on devices[k] (devices may repeat).
+class BandPartition {
+public:
+    BandPartition(const std::vector<int>& devices, int width, int height, int transport = SOBEL5_MGPU_AUTO) {
+        sobel5_mgpu* m = nullptr;
+        raise(sobel5_mgpu_create(&m, devices.data(), static_cast<int>(devices.size()), width, height, transport),
+              "sobel5_mgpu_create");
+        m_.reset(m);
+    }
+    sobel5_mgpu* get() const { return m_.get(); }
+    sobel5_band_info band(int k) const {
+        sobel5_band_info b{};
+        raise(sobel5_mgpu_band(m_.get(), k, &b), "sobel5_mgpu_band");
+        return b;
+    }
+
+private:
+    struct Del {
+        void operator()(sobel5_mgpu* m) const { sobel5_mgpu_destroy(m); }
+    };
+    std::unique_ptr<sobel5_mgpu, Del> m_;
+};
+
+}  // namespace gpu
+
+/// run_stream with the image row-band partitioned over `devices` (one band
+/// per entry; the 2-row halos cross NVLink inside the kernels, or are copied
+/// device to device).  Same validation, planes and counters as run_stream
+/// (pipeline.hpp:452-477); the reference's strip thread pool
+/// (run_strips_parallel, pipeline.hpp:416-445) becomes one band per GPU.
+inline StreamResult run_stream_bands(const GrayPlane& img, const StreamTaps& taps, const StripPlan& plan,
+                                     Prefetch prefetch, const std::vector<int>& devices,
+                                     int transport = SOBEL5_MGPU_AUTO) {
+    if (img.width() < 5 || img.height() < 5)
+        throw ImageTooSmall("streaming filter needs at least 5x5, got " + std::to_string(img.width()) + "x" +
+                            std::to_string(img.height()));
+    if (plan.in_width != img.width() || plan.radius != 2)
+        throw DimMismatch("strip plan covers " + std::to_string(plan.in_width) + " columns at radius " +
+                          std::to_string(plan.radius) + ", image has " + std::to_string(img.width()));
+    gpu::BandPartition part(devices, img.width(), img.height(), transport);
+    const int ow = img.width() - 4, oh = img.height() - 4;
+    StreamResult out;
+    out.gx = SignedPlane(ow, oh);
+    out.gy = SignedPlane(ow, oh);
+    out.gd = SignedPlane(ow, oh);
+    out.gdt = SignedPlane(ow, oh);
+    out.g = RealPlane(ow, oh);
+    sobel5_planes pl{};
+    pl.pitch = ow;
+    pl.gx = out.gx.data().data();
+    pl.gy = out.gy.data().data();
+    pl.gd = out.gd.data().data();
+    pl.gdt = out.gdt.data().data();
+    pl.g = out.g.data().data();
+    const sobel5_taps t = gpu::to_abi(taps);
+    const sobel5_status st =
+        sobel5_mgpu_run_host(part.get(), img.data().data(), &t, prefetch == Prefetch::on ? 1 : 0, &pl);
+    sobel5_diag d{};
+    if (st == SOBEL5_PARITY_VIOLATION) sobel5_mgpu_last_diag(part.get(), &d);
+    gpu::raise(st, "run_stream_bands", &d);
+    out.counters = stream_counters(img.height(), plan, taps, prefetch);
+    return out;
+}
+
+inline StreamResult run_stream_bands(const GrayPlane& img, const FilterParams& p, const StripPlan& plan,
+                                     Prefetch prefetch, const std::vector<int>& devices,
+                                     int transport = SOBEL5_MGPU_AUTO) {
+    return run_stream_bands(img, make_stream_taps(p), plan, prefetch, devices, transport);
+}
+
 /// Same planes as the reference oracle's sobel5_4d (oracle.hpp:72-98), which
 /// run_stream equals for every valid parameter set; computed on the GPU.
 struct Sobel5Result {

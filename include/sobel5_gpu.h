@@ -390,6 +390,71 @@ sobel5_status sobel5_dense_4d(const uint8_t* d_in, int64_t in_pitch, int width, 
 sobel5_status sobel5_dense_4d_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
                                    const int32_t* kernels, const sobel5_planes* h_out);
 
+/* ---- one image row-band partitioned over several GPUs (config C5) --------
+ * SURVEY.md 8b/8e; replaces the reference's strip thread pool
+ * run_strips_parallel (pipeline.hpp:416-445) at device granularity.  One
+ * process drives n bands; band k owns input rows [k*H/n, (k+1)*H/n) on
+ * devices[k] and writes the output rows centred in it (no gather: output
+ * rows are disjoint).  devices may repeat (several bands on one GPU).
+ * Halo transport: PEER -- the band kernel reads the neighbours' 2 rows from
+ * their HBM over NVLink inside the stencil (needs peer access); COPY -- the
+ * 2-row halos are copied device to device while the interior computes, then
+ * two 2-row seams; AUTO -- PEER where every neighbour pair has peer access.
+ * Ordering uses events on the bands' streams only (no host barrier):
+ * run_bands waits for everything already enqueued on each band's stream
+ * before reading that band's rows, and afterwards every band's stream waits
+ * until its neighbours' kernels are done, so input rows the caller writes
+ * next on a band's stream never race the halo reads of the previous call. */
+enum { SOBEL5_MGPU_AUTO = -1, SOBEL5_MGPU_PEER = 0, SOBEL5_MGPU_COPY = 1 };
+
+typedef struct sobel5_mgpu sobel5_mgpu; /* opaque */
+
+typedef struct sobel5_band_info {
+    int device;
+    int r0, r1;         /* input rows [r0, r1) of the image held by the band */
+    int out_row0;       /* first row of the (W-4) x (H-4) output it writes */
+    int out_rows;       /* output rows it writes */
+    uint8_t* d_in;      /* its input rows on `device`, row stride in_pitch */
+    int64_t in_pitch;
+    void* stream;       /* cudaStream_t of the band (on `device`) */
+    int transport;      /* SOBEL5_MGPU_PEER or _COPY (AUTO resolved) */
+} sobel5_band_info;
+
+/* Errors: IMAGE_TOO_SMALL below 5x5, DIM_MISMATCH when a band would get
+ * fewer than 4 rows, INVALID_ARG for a bad device or PEER without peer
+ * access, NO_DEVICE without a GPU. */
+sobel5_status sobel5_mgpu_create(sobel5_mgpu** out, const int* devices, int n, int width,
+                                 int height, int transport);
+void sobel5_mgpu_destroy(sobel5_mgpu* m);
+sobel5_status sobel5_mgpu_band(const sobel5_mgpu* m, int k, sobel5_band_info* info);
+/* Enqueue each band's rows of a tightly packed W x H host image (pinned
+ * memory makes this asynchronous), or synth_random(W, H, seed) & mask
+ * generated on every band's device. */
+sobel5_status sobel5_mgpu_upload(sobel5_mgpu* m, const uint8_t* h_img);
+sobel5_status sobel5_mgpu_synth(sobel5_mgpu* m, uint64_t seed, uint8_t mask);
+/* Asynchronous: band k's output rows into d_out[k] (planes on devices[k],
+ * out_rows x pitch, same plane rules as sobel5_launch). */
+sobel5_status sobel5_mgpu_run_bands(sobel5_mgpu* m, const sobel5_taps* taps, int prefetch,
+                                    const sobel5_planes* d_out);
+sobel5_status sobel5_mgpu_sync(sobel5_mgpu* m);
+/* Host buffers end to end (the multi-GPU run_stream): upload, bands, and
+ * each band's rows downloaded over its own GPU's link into the tightly
+ * packed host planes (pitch == width-4). */
+sobel5_status sobel5_mgpu_run_host(sobel5_mgpu* m, const uint8_t* h_in, const sobel5_taps* taps,
+                                   int prefetch, const sobel5_planes* h_out);
+/* After run_host returned SOBEL5_PARITY_VIOLATION: the offending pair. */
+sobel5_status sobel5_mgpu_last_diag(const sobel5_mgpu* m, sobel5_diag* out);
+
+/* ---- stream-ordered flags (cross-process band ordering, bands.py) --------
+ * host_register maps host memory (e.g. a shared-memory segment several
+ * processes map) for device access; stream_write_u32 stores `value` to the
+ * flag when the stream reaches it; stream_wait_u32 blocks the stream (not
+ * the host) until (int32_t)(*flag - value) >= 0 (cuStreamWaitValue32 GEQ). */
+sobel5_status sobel5_host_register(void* p, size_t bytes, void** d_ptr);
+sobel5_status sobel5_host_unregister(void* p);
+sobel5_status sobel5_stream_write_u32(uint32_t* d_flag, uint32_t value, void* stream);
+sobel5_status sobel5_stream_wait_u32(const uint32_t* d_flag, uint32_t value, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

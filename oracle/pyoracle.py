@@ -249,6 +249,8 @@ class Reference:
         L.ref_conv2d_valid.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
                                        C.c_void_p]
         L.ref_conv2d_valid.restype = C.c_int
+        L.ref_measure_csv.argtypes = [C.c_void_p] + [C.c_int] * 7 + [C.c_void_p]
+        L.ref_measure_csv.restype = C.c_double
 
     @staticmethod
     def _err():
@@ -385,6 +387,20 @@ class Reference:
                                            _p(o["gx"]), _p(o["gy"]), _p(o["g"]), _p(cnt), e, 512)
         names = [n for n, _ in Counters._fields_]
         return code, o, dict(zip(names, (int(x) for x in cnt))), e.value.decode()
+
+    def measure_csv(self, img, which="fast", lanes=32, prefetch=True, workers=1, iters=1):
+        """(mean_s, csv_row) of the reference's measure() around run_stream
+        (which="fast") or the sobel5_4d oracle (which="oracle"); the row in
+        the reference's BenchReport CSV schema and number format
+        (metrics.hpp:129-139: setprecision 9 for the times, 6 for the rates)."""
+        img = np.ascontiguousarray(img, np.uint8)
+        h, w = img.shape
+        f = np.zeros(4, np.float64)
+        mean = self.lib.ref_measure_csv(_p(img), w, h, 0 if which == "fast" else 1, lanes,
+                                        int(prefetch), workers, iters, _p(f))
+        label = "fast-5x5" if which == "fast" else "oracle-5x5"
+        row = f"{label},{w},{h},{iters},{f[0]:.9g},{f[1]:.9g},{f[2]:.6g},{f[3]:.6g}"
+        return mean, row
 
     def measure_run_stream_3x3(self, img, lanes=256, prefetch=True, workers=1, iters=1):
         img = np.ascontiguousarray(img, np.uint8)

@@ -272,6 +272,37 @@ double ref_measure_run_stream(const std::uint8_t* img, int w, int h, int lanes, 
     return rep.mean_s;
 }
 
+// The reference CLI's bench rows (sobel5_cli.cpp:236-276): measure() of
+// run_stream ("fast-5x5", which = 0) or of the sobel5_4d oracle
+// ("oracle-5x5", which = 1, one worker).  out[0..3] = the BenchReport's
+// mean_s, stddev_s, mps, mps_per_core (pyoracle formats the reference's CSV
+// row, metrics.hpp:129-139, from them).  Returns mean_s.
+double ref_measure_csv(const std::uint8_t* img, int w, int h, int which, int lanes, int prefetch,
+                       int workers, int iters, double* out) {
+    sobel5::GrayPlane in(w, h, std::vector<std::uint8_t>(img, img + std::size_t(w) * h));
+    const sobel5::FilterParams p;
+    sobel5::BenchReport rep;
+    if (which == 0) {
+        const auto plan = sobel5::plan_strips(w, lanes, 2);
+        rep = sobel5::measure("fast-5x5", w, h, iters, workers, [&] {
+            auto r = sobel5::run_stream(in, p, plan,
+                                        prefetch ? sobel5::Prefetch::on : sobel5::Prefetch::off,
+                                        workers);
+            (void)r;
+        });
+    } else {
+        rep = sobel5::measure("oracle-5x5", w, h, iters, 1, [&] {
+            auto r = sobel5::sobel5_4d(in, p);
+            (void)r;
+        });
+    }
+    out[0] = rep.mean_s;
+    out[1] = rep.stddev_s;
+    out[2] = rep.mps;
+    out[3] = rep.mps_per_core;
+    return rep.mean_s;
+}
+
 double ref_measure_oracle(const std::uint8_t* img, int w, int h, int iters) {
     sobel5::GrayPlane in(w, h, std::vector<std::uint8_t>(img, img + std::size_t(w) * h));
     const auto rep = sobel5::measure("oracle-5x5", w, h, iters, 1, [&] {

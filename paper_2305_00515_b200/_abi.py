@@ -61,11 +61,19 @@ class LaunchInfo(C.Structure):
                                          "grid_z")]
 
 
+class BandInfo(C.Structure):
+    _fields_ = [("device", C.c_int), ("r0", C.c_int), ("r1", C.c_int), ("out_row0", C.c_int),
+                ("out_rows", C.c_int), ("d_in", C.c_void_p), ("in_pitch", C.c_int64),
+                ("stream", C.c_void_p), ("transport", C.c_int)]
+
+
 class Counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "row_conv5_f", "row_conv5_h", "row_conv5_k0", "row_conv5_k1",
         "row_diff", "row_conv3_f", "row_conv3_h", "mac")]
 
+
+MGPU_AUTO, MGPU_PEER, MGPU_COPY = -1, 0, 1
 
 PLANE_NAMES = ("gx", "gy", "gd", "gdt", "g", "g32", "u8")
 
@@ -86,6 +94,10 @@ EXPORTS = (
     "sobel5_run_host_chunk", "sobel5_run_host_staging", "sobel5_kernel_for_taps",
     "sobel3_run_host_begin", "sobel5_ctx_trim", "sobel5_last_launch",
     "sobel5_conv2d_valid", "sobel5_conv2d_valid_host", "sobel5_dense_4d", "sobel5_dense_4d_host",
+    "sobel5_mgpu_create", "sobel5_mgpu_destroy", "sobel5_mgpu_band", "sobel5_mgpu_upload",
+    "sobel5_mgpu_synth", "sobel5_mgpu_run_bands", "sobel5_mgpu_sync", "sobel5_mgpu_run_host", "sobel5_mgpu_last_diag",
+    "sobel5_host_register", "sobel5_host_unregister", "sobel5_stream_write_u32",
+    "sobel5_stream_wait_u32",
 )
 
 _lib = None
@@ -121,6 +133,32 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.sobel5_dense_4d.restype = i32
     L.sobel5_dense_4d_host.argtypes = [vp, vp, i32, i32, vp, C.POINTER(Planes)]
     L.sobel5_dense_4d_host.restype = i32
+    L.sobel5_mgpu_create.argtypes = [C.POINTER(vp), vp, i32, i32, i32, i32]
+    L.sobel5_mgpu_create.restype = i32
+    L.sobel5_mgpu_destroy.argtypes = [vp]
+    L.sobel5_mgpu_destroy.restype = None
+    L.sobel5_mgpu_band.argtypes = [vp, i32, C.POINTER(BandInfo)]
+    L.sobel5_mgpu_band.restype = i32
+    L.sobel5_mgpu_upload.argtypes = [vp, vp]
+    L.sobel5_mgpu_upload.restype = i32
+    L.sobel5_mgpu_synth.argtypes = [vp, C.c_uint64, C.c_uint8]
+    L.sobel5_mgpu_synth.restype = i32
+    L.sobel5_mgpu_run_bands.argtypes = [vp, C.POINTER(Taps), i32, vp]
+    L.sobel5_mgpu_run_bands.restype = i32
+    L.sobel5_mgpu_sync.argtypes = [vp]
+    L.sobel5_mgpu_sync.restype = i32
+    L.sobel5_mgpu_run_host.argtypes = [vp, vp, C.POINTER(Taps), i32, C.POINTER(Planes)]
+    L.sobel5_mgpu_run_host.restype = i32
+    L.sobel5_mgpu_last_diag.argtypes = [vp, C.POINTER(Diag)]
+    L.sobel5_mgpu_last_diag.restype = i32
+    L.sobel5_host_register.argtypes = [vp, C.c_size_t, C.POINTER(vp)]
+    L.sobel5_host_register.restype = i32
+    L.sobel5_host_unregister.argtypes = [vp]
+    L.sobel5_host_unregister.restype = i32
+    L.sobel5_stream_write_u32.argtypes = [vp, C.c_uint32, vp]
+    L.sobel5_stream_write_u32.restype = i32
+    L.sobel5_stream_wait_u32.argtypes = [vp, C.c_uint32, vp]
+    L.sobel5_stream_wait_u32.restype = i32
     L.sobel5_make_taps.argtypes = [i64] * 4 + [C.POINTER(Taps)]
     L.sobel5_make_taps.restype = i32
     L.sobel5_plan_counters.argtypes = [i32, vp, i32, C.POINTER(Taps), i32, C.POINTER(Counters)]

@@ -707,6 +707,101 @@ def detect3_device(d_in, in_pitch: int, width: int, height: int, prefetch: int, 
           "sobel3_detect")
 
 
+# ---- one image over several GPUs from one process (config C5) -------------------
+
+TRANSPORTS = {"auto": _abi.MGPU_AUTO, "peer": _abi.MGPU_PEER, "copy": _abi.MGPU_COPY}
+
+
+class MultiGpuBands:
+    """sobel5_mgpu: band k of len(devices) owns input rows [k*H/n, (k+1)*H/n)
+    on devices[k] (devices may repeat); halos by peer reads inside the
+    kernel or device-to-device copies."""
+
+    def __init__(self, devices, width: int, height: int, transport: str = "auto"):
+        self._lib = _abi.load()
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        check(self._lib.sobel5_mgpu_create(C.byref(h), devs, len(devices), width, height,
+                                           TRANSPORTS[transport]), "sobel5_mgpu_create")
+        self._h = h
+        self.width, self.height, self.n = width, height, len(devices)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.sobel5_mgpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def band(self, k: int) -> dict:
+        b = _abi.BandInfo()
+        check(self._lib.sobel5_mgpu_band(self._h, k, C.byref(b)), "sobel5_mgpu_band")
+        return {n: getattr(b, n) for n, _ in _abi.BandInfo._fields_}
+
+    def upload(self, img: np.ndarray) -> None:
+        img = np.ascontiguousarray(img, np.uint8)
+        check(self._lib.sobel5_mgpu_upload(self._h, img.ctypes.data), "sobel5_mgpu_upload")
+
+    def synth(self, seed: int, mask: int = 0xFF) -> None:
+        check(self._lib.sobel5_mgpu_synth(self._h, seed, mask), "sobel5_mgpu_synth")
+
+    def run_bands(self, taps: Taps, prefetch: int, planes: list, pitch: int) -> None:
+        """planes[k]: dict of band k's device tensors (on its device)."""
+        arr = (Planes * self.n)(*[planes_struct(p, pitch) for p in planes])
+        check(self._lib.sobel5_mgpu_run_bands(self._h, C.byref(taps), int(prefetch), arr),
+              "sobel5_mgpu_run_bands")
+
+    def sync(self) -> None:
+        check(self._lib.sobel5_mgpu_sync(self._h), "sobel5_mgpu_sync")
+
+    def run_host(self, img: np.ndarray, taps: Taps, prefetch: Prefetch,
+                 planes=("gx", "gy", "gd", "gdt", "g")) -> dict:
+        img = np.ascontiguousarray(img, np.uint8)
+        ow, oh = self.width - 4, self.height - 4
+        dt = {"gx": np.int32, "gy": np.int32, "gd": np.int32, "gdt": np.int32, "g": np.float64,
+              "g32": np.float32, "u8": np.uint8}
+        res = {k: np.empty((oh, ow), dt[k]) for k in planes}
+        pl = Planes(pitch=ow)
+        for k, v in res.items():
+            setattr(pl, k, v.ctypes.data)
+        st = self._lib.sobel5_mgpu_run_host(self._h, img.ctypes.data, C.byref(taps), int(prefetch),
+                                            C.byref(pl))
+        if st == _abi.PARITY_VIOLATION:
+            d = Diag()
+            self._lib.sobel5_mgpu_last_diag(self._h, C.byref(d))
+            raise ParityViolation(f"odd sum/difference pair ({d.sum}, {d.diff})")
+        check(st, "sobel5_mgpu_run_host")
+        return res
+
+
+def run_stream_bands(img: np.ndarray, taps_or_params, plan: StripPlan, prefetch: Prefetch,
+                     devices, transport: str = "auto") -> StreamResult:
+    """run_stream (pipeline.hpp:452-477) with the image row-band partitioned
+    over ``devices`` from this process (the C++ sobel5::run_stream_bands)."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    if img.ndim != 2:
+        raise DimMismatch("image must be 2-D")
+    h, w = img.shape
+    if w < 5 or h < 5:
+        raise ImageTooSmall(f"streaming filter needs at least 5x5, got {w}x{h}")
+    if plan.in_width != w or plan.radius != 2:
+        raise DimMismatch(f"strip plan covers {plan.in_width} columns at radius {plan.radius}, "
+                          f"image has {w}")
+    taps = taps_or_params if isinstance(taps_or_params, Taps) else make_stream_taps(
+        taps_or_params)
+    mg = MultiGpuBands(devices, w, h, transport)
+    try:
+        res = mg.run_host(img, taps, prefetch)
+    finally:
+        mg.close()
+    return StreamResult(res["gx"], res["gy"], res["gd"], res["gdt"], res["g"],
+                        plan_counters(h, plan, taps, prefetch))
+
+
 def last_launch() -> dict:
     """Geometry of this thread's last 5x5 stencil launch (sobel5_last_launch):
     band, tma_load, kernel (index into KERNELS), grid_x/y/z."""

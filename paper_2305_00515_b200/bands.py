@@ -11,7 +11,15 @@ Halo transports:
   IPC (sobel5_ipc_export), maps its neighbours' buffers once, and ONE kernel
   (sobel5_launch_band) reads the neighbour rows over NVLink/NVSwitch while it
   streams its own band: the exchange is fused into the compute, no copy and
-  no collective on the data path.
+  no collective on the data path.  Cross-process ordering is carried by
+  stream-ordered flags in a shared host page every rank maps (step
+  counters, cuStreamWriteValue32 / cuStreamWaitValue32 through
+  sobel5_stream_write_u32 / _wait_u32), without a host barrier per step:
+  ``ready[k] = s`` once rank k's input for step s is on its stream, the band
+  kernel waits for ``ready[k-1], ready[k+1] >= s``, then ``done[k] = s``, and
+  the stream waits for ``done[k-1], done[k+1] >= s`` before anything the
+  caller enqueues next (the next step's input) can overwrite rows a
+  neighbour is still reading.
 * ``"nccl"`` / ``"gloo"``: the 2-row halos are exchanged with
   torch.distributed point-to-point ops (batched isend/irecv).  The interior
   rows, which need no halo, are launched first so the exchange overlaps them;
@@ -86,10 +94,13 @@ class RowBandPartition:
         self.transport, self.group = transport, group
         self._peer = {}  # rank -> imported pointer
         self._dist = dist
+        self._flags = None  # (mmap, host address, device address) of the shared flag page
+        self._step = 0
         if transport not in ("peer", "nccl", "gloo"):
             raise ValueError(transport)
         if plan.world > 1 and transport == "peer":
             self._map_neighbours()
+            self._map_flags()
 
     # ---- peer mapping -----------------------------------------------------------
     def _map_neighbours(self):
@@ -109,11 +120,52 @@ class RowBandPartition:
                 self._peer[nb] = p.value
         self._dist.barrier(group=self.group)
 
+    # ---- shared flag page (cross-process stream ordering) ----------------------
+    _FLAG_BYTES = 4096
+    _DONE = 256  # byte offset of done[]; ready[] starts at 0 (uint32 per rank)
+
+    def _map_flags(self):
+        import mmap
+        import os
+        import uuid
+        L = _abi.load()
+        name = [f"/dev/shm/sobel5_bands_{uuid.uuid4().hex}" if self.plan.rank == 0 else None]
+        self._dist.broadcast_object_list(name, src=0, group=self.group)
+        path = name[0]
+        if self.plan.rank == 0:
+            with open(path, "wb") as f:
+                f.write(bytes(self._FLAG_BYTES))
+        self._dist.barrier(group=self.group)
+        fd = os.open(path, os.O_RDWR)
+        try:
+            mm = mmap.mmap(fd, self._FLAG_BYTES)
+        finally:
+            os.close(fd)
+        self._dist.barrier(group=self.group)
+        if self.plan.rank == 0:
+            os.unlink(path)  # every rank holds the mapping; nothing left behind
+        host = C.addressof(C.c_char.from_buffer(mm))
+        dev = C.c_void_p()
+        api.check(L.sobel5_host_register(host, self._FLAG_BYTES, C.byref(dev)),
+                  "sobel5_host_register")
+        self._flags = (mm, host, dev.value)
+
+    def _flag(self, which: int, rank: int) -> int:
+        return self._flags[2] + which + 4 * rank
+
     def close(self):
         L = _abi.load()
         for p in self._peer.values():
             L.sobel5_ipc_release(p)
         self._peer = {}
+        if self._flags is not None:
+            mm, host, _ = self._flags
+            L.sobel5_host_unregister(host)
+            self._flags = None
+            try:
+                mm.close()
+            except BufferError:  # a ctypes view still alive; the OS unmaps at exit
+                pass
 
     # ---- halo exchange through torch.distributed ---------------------------------
     def exchange(self):
@@ -155,12 +207,36 @@ class RowBandPartition:
                        stream=stream)
             return
         if self.transport == "peer":
+            import torch
+            L = _abi.load()
+            sp = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+            self._step = s = (self._step + 1) & 0xFFFFFFFF
+            nbrs = [r for r, has in ((p.rank - 1, p.has_top), (p.rank + 1, p.has_bot)) if has]
+
+            def flag_op(fn, which, rank):
+                api.check(fn(self._flag(which, rank), s, sp), fn.__name__)
+
+            flag_op(L.sobel5_stream_write_u32, 0, p.rank)  # my rows for step s are in place
+            for r in nbrs:
+                flag_op(L.sobel5_stream_wait_u32, 0, r)  # neighbours' rows too
             top = _row_ptr_int(self._peer.get(p.rank - 1), self._prev_rows() - HALO, self.pitch) \
                 if p.has_top else None
             bot = self._peer.get(p.rank + 1) if p.has_bot else None
             api.launch_band(top, self.body, bot, self.pitch, p.width, p.body_rows, taps, prefetch,
-                            planes, out_pitch, stream=stream)
+                            planes, out_pitch, stream=sp)
+            flag_op(L.sobel5_stream_write_u32, self._DONE, p.rank)  # done reading my halos
+            for r in nbrs:  # later writes to my rows wait for the neighbours' reads
+                flag_op(L.sobel5_stream_wait_u32, self._DONE, r)
             return
+        import torch
+        # torch.distributed orders its P2P ops and copies against the CURRENT
+        # stream: make that the caller's stream for the whole exchange
+        ext = torch.cuda.ExternalStream(stream) if stream is not None else None
+        with torch.cuda.stream(ext) if ext is not None else _nullcontext():
+            self._run_exchange(taps, planes, out_pitch, prefetch, stream)
+
+    def _run_exchange(self, taps, planes, out_pitch, prefetch, stream):
+        p = self.plan
         # interior first (no halo needed), overlapping the exchange
         top_rows = HALO if p.has_top else 0
         interior = p.body_rows - 4
@@ -180,6 +256,14 @@ class RowBandPartition:
     def _prev_rows(self) -> int:
         prev = plan_bands(self.plan.width, self.plan.height, self.plan.world, self.plan.rank - 1)
         return prev.body_rows
+
+
+class _nullcontext:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False
 
 
 def _row_ptr_int(base: int | None, row: int, pitch: int) -> int | None:

@@ -52,6 +52,7 @@ struct Band {
     uint8_t* d_halo = nullptr; // copy transport: 2 rows above + 2 rows below
     void* d_plane[7] = {};     // run_host: this band's output rows
     size_t d_plane_bytes[7] = {};
+    sobel5_diag* d_diag = nullptr;  // run_host: recover_diag parity record
     int rows() const { return r1 - r0; }
 };
 
@@ -84,6 +85,7 @@ struct sobel5_mgpu {
     int width = 0, height = 0, transport = 0;
     int64_t in_pitch = 0;
     std::vector<Band> bands;
+    sobel5_diag last_diag{};  // run_host's first parity violation
 };
 
 namespace {
@@ -112,7 +114,7 @@ sobel5_planes offset_planes(const sobel5_planes& p, int64_t rows) {
 // Enqueues band k's kernels on its stream (after waiting for its
 // neighbours' ready events).  `out` is the band's planes on its device.
 sobel5_status run_band(sobel5_mgpu* m, int k, const sobel5_taps* taps, int prefetch,
-                       const sobel5_planes& out) {
+                       const sobel5_planes& out, sobel5_diag* diag) {
     Band& b = m->bands[static_cast<size_t>(k)];
     const int n = static_cast<int>(m->bands.size());
     const bool has_top = k > 0, has_bot = k < n - 1;
@@ -129,14 +131,14 @@ sobel5_status run_band(sobel5_mgpu* m, int k, const sobel5_taps* taps, int prefe
         }
         if (has_bot) bot = m->bands[static_cast<size_t>(k + 1)].d_in;
         return sobel5_launch_band(top, b.d_in, bot, P, m->width, b.rows(), taps, prefetch, &out,
-                                  nullptr, b.stream);
+                                  diag, b.stream);
     }
     // copy transport: interior first (no halo needed), halos, then the seams
     const int top_rows = has_top ? 2 : 0;
     if (b.rows() > 4) {
         const sobel5_planes o = offset_planes(out, top_rows);
         if (sobel5_status st = sobel5_launch_band(nullptr, b.d_in, nullptr, P, m->width, b.rows(),
-                                                  taps, prefetch, &o, nullptr, b.stream);
+                                                  taps, prefetch, &o, diag, b.stream);
             st != SOBEL5_OK)
             return st;
     }
@@ -154,7 +156,7 @@ sobel5_status run_band(sobel5_mgpu* m, int k, const sobel5_taps* taps, int prefe
     }
     if (has_top) {  // centres r0, r0 + 1 from [halo; body rows 0..3]
         if (sobel5_status st = sobel5_launch_band(h_top, b.d_in, nullptr, P, m->width, 4, taps,
-                                                  prefetch, &out, nullptr, b.stream);
+                                                  prefetch, &out, diag, b.stream);
             st != SOBEL5_OK)
             return st;
     }
@@ -162,7 +164,7 @@ sobel5_status run_band(sobel5_mgpu* m, int k, const sobel5_taps* taps, int prefe
         const sobel5_planes o = offset_planes(out, b.c1 - b.c0 - 2);
         if (sobel5_status st = sobel5_launch_band(nullptr, b.d_in + static_cast<int64_t>(b.rows() - 4) * P,
                                                   h_bot, P, m->width, 4, taps, prefetch, &o,
-                                                  nullptr, b.stream);
+                                                  diag, b.stream);
             st != SOBEL5_OK)
             return st;
     }
@@ -255,6 +257,7 @@ void sobel5_mgpu_destroy(sobel5_mgpu* m) {
         if (cudaSetDevice(b.device) != cudaSuccess) continue;
         if (b.d_in) cudaFree(b.d_in);
         if (b.d_halo) cudaFree(b.d_halo);
+        if (b.d_diag) cudaFree(b.d_diag);
         for (void* p : b.d_plane)
             if (p) cudaFree(p);
         if (b.ready) cudaEventDestroy(b.ready);
@@ -304,16 +307,19 @@ sobel5_status sobel5_mgpu_synth(sobel5_mgpu* m, uint64_t seed, uint8_t mask) {
     return SOBEL5_OK;
 }
 
-sobel5_status sobel5_mgpu_run_bands(sobel5_mgpu* m, const sobel5_taps* taps, int prefetch,
-                                    const sobel5_planes* d_out) {
-    if (!m || !taps || !d_out) return SOBEL5_INVALID_ARG;
+}  // extern "C"
+
+namespace {
+sobel5_status run_bands_impl(sobel5_mgpu* m, const sobel5_taps* taps, int prefetch,
+                             const sobel5_planes* d_out, bool with_diag) {
     const int n = static_cast<int>(m->bands.size());
     for (Band& b : m->bands) {  // everything enqueued so far on band k's stream
         CKS(cudaSetDevice(b.device));
         CKS(cudaEventRecord(b.ready, b.stream));
     }
     for (int k = 0; k < n; ++k) {
-        if (sobel5_status st = run_band(m, k, taps, prefetch, d_out[k]); st != SOBEL5_OK) return st;
+        sobel5_diag* dg = with_diag ? m->bands[static_cast<size_t>(k)].d_diag : nullptr;
+        if (sobel5_status st = run_band(m, k, taps, prefetch, d_out[k], dg); st != SOBEL5_OK) return st;
         CKS(cudaEventRecord(m->bands[static_cast<size_t>(k)].done, m->bands[static_cast<size_t>(k)].stream));
     }
     // later writes to band k's rows (enqueued by the caller on its stream)
@@ -325,6 +331,15 @@ sobel5_status sobel5_mgpu_run_bands(sobel5_mgpu* m, const sobel5_taps* taps, int
         if (k < n - 1) CKS(cudaStreamWaitEvent(b.stream, m->bands[static_cast<size_t>(k + 1)].done, 0));
     }
     return SOBEL5_OK;
+}
+}  // namespace
+
+extern "C" {
+
+sobel5_status sobel5_mgpu_run_bands(sobel5_mgpu* m, const sobel5_taps* taps, int prefetch,
+                                    const sobel5_planes* d_out) {
+    if (!m || !taps || !d_out) return SOBEL5_INVALID_ARG;
+    return run_bands_impl(m, taps, prefetch, d_out, false);
 }
 
 sobel5_status sobel5_mgpu_sync(sobel5_mgpu* m) {
@@ -365,8 +380,13 @@ sobel5_status sobel5_mgpu_run_host(sobel5_mgpu* m, const uint8_t* h_in, const so
             *slots[i] = b.d_plane[i];
         }
     }
+    for (Band& b : m->bands) {
+        CKS(cudaSetDevice(b.device));
+        if (!b.d_diag) CKS(cudaMalloc(reinterpret_cast<void**>(&b.d_diag), sizeof(sobel5_diag)));
+        CKS(cudaMemsetAsync(b.d_diag, 0, sizeof(sobel5_diag), b.stream));
+    }
     if (sobel5_status st = sobel5_mgpu_upload(m, h_in); st != SOBEL5_OK) return st;
-    if (sobel5_status st = sobel5_mgpu_run_bands(m, taps, prefetch, dp.data()); st != SOBEL5_OK)
+    if (sobel5_status st = run_bands_impl(m, taps, prefetch, dp.data(), true); st != SOBEL5_OK)
         return st;
     for (size_t k = 0; k < m->bands.size(); ++k) {  // each band's rows over its own link
         Band& b = m->bands[k];
@@ -380,7 +400,23 @@ sobel5_status sobel5_mgpu_run_host(sobel5_mgpu* m, const uint8_t* h_in, const so
                                   static_cast<size_t>(b.c1 - b.c0), cudaMemcpyDeviceToHost, b.stream));
         }
     }
-    return sobel5_mgpu_sync(m);
+    if (sobel5_status st = sobel5_mgpu_sync(m); st != SOBEL5_OK) return st;
+    for (Band& b : m->bands) {  // recover_diag (pipeline.hpp:268-273), first band in row order
+        sobel5_diag d{};
+        CKS(cudaSetDevice(b.device));
+        CKS(cudaMemcpy(&d, b.d_diag, sizeof d, cudaMemcpyDeviceToHost));
+        if (d.violations) {
+            m->last_diag = d;
+            return SOBEL5_PARITY_VIOLATION;
+        }
+    }
+    return SOBEL5_OK;
+}
+
+sobel5_status sobel5_mgpu_last_diag(const sobel5_mgpu* m, sobel5_diag* out) {
+    if (!m || !out) return SOBEL5_INVALID_ARG;
+    *out = m->last_diag;
+    return SOBEL5_OK;
 }
 
 // ---- stream-ordered flags (cross-process ordering of the peer transport) ----

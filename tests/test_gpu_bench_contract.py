@@ -46,8 +46,24 @@ def test_two_ranks_e2e(cuda):
     its own image, the time is the max over ranks."""
     d = run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
              "--master-addr", "127.0.0.1", "--master-port", "29538", "bench.py", "--gpus", "2",
-             "--steps", "4", "--warmup", "3", "--share-gpu", "--no-cpu-baseline"])
+             "--steps", "4", "--warmup", "3", "--workload", "8k", "--share-gpu",
+             "--no-cpu-baseline"])
     e = d["e2e"]
     assert e["ranks"] == 2 and e["value"] > 0
     assert e["h2d_bytes_per_step"] == 2 * 7680 * 4320
     assert e["d2h_bytes_per_step"] == 2 * 7676 * 4316 * 24
+
+
+def test_two_ranks_default_is_c5_with_e2e(cuda):
+    """N > 1 defaults to the C5 strong-scaling workload (one 32768^2 image
+    row-band partitioned, peer halos ordered by stream flags); e2e moves
+    the band rows in and every output row out, max over ranks."""
+    d = run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+             "--master-addr", "127.0.0.1", "--master-port", "29539", "bench.py", "--gpus", "2",
+             "--steps", "3", "--warmup", "3", "--share-gpu", "--no-cpu-baseline"], timeout=900)
+    assert d["scaling"] == "strong" and "32768x32768" in d["config"]["workload"]
+    assert d["timing"]["timed_as"] == "Python launch loop"
+    e = d["e2e"]
+    assert e["ranks"] == 2 and e["h2d_bytes_per_step"] == 32768 * 32768
+    assert e["d2h_bytes_per_step"] >= 32764 * 32764 * 24
+    assert d["cpu_baseline"] is None  # rank 0 at N=1 only
