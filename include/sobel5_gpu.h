@@ -260,8 +260,9 @@ int sobel5_kernel_for_taps(const sobel5_taps* taps);
  * __dsqrt_rn((double)S); which = 1 compares the uint8 clamp_abs shortcut with
  * min(255, round(sqrt(S))); which = 2 checks the packed-float u8 epilogue
  * of the u8-only kernels on every integer S <= 65280 in range, and which = 3
- * on every float S >= 65281 whose bit pattern is in [lo, hi) (expects 255).
- * Adds the number of mismatches to *d_count (device pointer, unsigned
+ * on every float S >= 65281 whose bit pattern is in [lo, hi) (expects 255);
+ * which = 4 / 5 do the same for the sqrt + saturating round of the u8-only
+ * kernel (sobel5_u8.cuh).  Adds the number of mismatches to *d_count (device pointer, unsigned
  * 64-bit). */
 sobel5_status sobel5_selftest(int which, uint32_t lo, uint32_t hi, uint64_t* d_count,
                               void* stream);

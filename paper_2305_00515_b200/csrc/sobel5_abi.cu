@@ -17,6 +17,7 @@
 
 #include "sobel5_gpu.h"
 #include "sobel5_packed.cuh"
+#include "sobel5_u8.cuh"
 #include <algorithm>
 #include "sobel5_internal.h"
 #include "sobel5_stream.cuh"
@@ -305,6 +306,7 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     kp.top_rows = top_rows;
     kp.mid_rows = mid_rows;
     kp.width = width;
+    kp.frames = frames;
     kp.out_w = out_w;
     kp.out_h = out_h;
     const bool wide = out->gx || out->gy || out->gd || out->gdt || out->g || out->g32;
@@ -380,6 +382,24 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
         if (kp.band > 32) kp.tma_load = 0;  // the shared-memory band holds 36 rows
     }
     const dim3 grid2(grid.x, static_cast<unsigned>((out_h + kp.band - 1) / kp.band), grid.z);
+    // The u8-only clamp_abs edge map with default taps (plain / batch /
+    // replicate-padded): the issue-bound contract has its own kernel
+    // (sobel5_u8.cuh: packed pairs, ring vertical pass, TMA band rows).  SOBEL5_U8_FAST=0 keeps
+    // the general packed kernel (ablation).
+    if (prefetch && !top && !bot && out->u8 && !wide && !ex.minmax && !ex.norm && !ex.u8_norm &&
+        !ex.s32 && taps_are_default(*taps) && out->pitch % 8 == 0 && aligned(out->u8, 8) &&
+        (frames == 1 || out_frame_stride % 8 == 0) && env_int("SOBEL5_U8_FAST", 1) != 0 &&
+        env_int("SOBEL5_GENERIC", 0) == 0 && env_int("SOBEL5_DENSE", 0) == 0) {
+        kp.band = u8_fast_band(out_w, out_h, frames);
+        const int gy = (out_h + kp.band - 1) / kp.band;
+        if (gy <= 65535) {
+            kp.tma_load = 1;
+            t_last_launch = sobel5_launch_info{kp.band, 1, sobel5_kernel_for_taps(taps),
+                                               (out_w + u8_fast_cta_cols() - 1) / u8_fast_cta_cols(), gy, frames};
+            count_launch();
+            return map_cuda(launch_u8_fast(kp, frames, static_cast<cudaStream_t>(stream)));
+        }
+    }
     t_last_launch = sobel5_launch_info{kp.band, kp.tma_load, sobel5_kernel_for_taps(taps),
                                        static_cast<int>(grid2.x), static_cast<int>(grid2.y),
                                        static_cast<int>(grid2.z)};
@@ -436,6 +456,18 @@ __global__ void selftest_kernel(int which, uint32_t lo, uint32_t hi,
             uint32_t a, b;
             u8_from_sf2(make_float2(static_cast<float>(S), static_cast<float>(S)), a, b);
             bad += (a != want) + (b != want);
+        } else if (which == 4) {
+            // the u8-only kernel's sqrt + saturating round (sobel5_u8.cuh) on
+            // every exact integer sum S <= 65280
+            if (S > 65280u) continue;
+            const double r = round(__dsqrt_rn(static_cast<double>(S)));
+            const uint32_t want = r < 255.0 ? static_cast<uint32_t>(r) : 255u;
+            bad += (u8_round_sqrt(static_cast<float>(S)) & 0xffu) != want;
+        } else if (which == 5) {
+            // ... and on every float sum >= 65281 (S = float bit pattern)
+            const float f = __uint_as_float(S);
+            if (!(f >= 65281.0f) || isinf(f)) continue;
+            bad += (u8_round_sqrt(f) & 0xffu) != 255u;
         } else {
             // ... and on every float sum >= 65281 (S = float bit pattern)
             const float f = __uint_as_float(S);
@@ -595,7 +627,7 @@ int sobel5_kernel_for_taps(const sobel5_taps* t) {
 
 sobel5_status sobel5_selftest(int which, uint32_t lo, uint32_t hi, uint64_t* d_count,
                               void* stream) {
-    if (!d_count || hi < lo || which < 0 || which > 3) return SOBEL5_INVALID_ARG;
+    if (!d_count || hi < lo || which < 0 || which > 5) return SOBEL5_INVALID_ARG;
     if (which == 0 && hi > (1u << 30)) return SOBEL5_INVALID_ARG;
     selftest_kernel<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         which, lo, hi, reinterpret_cast<unsigned long long*>(d_count));

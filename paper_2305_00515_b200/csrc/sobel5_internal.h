@@ -22,6 +22,12 @@ cudaError_t launch_packed_rt_plain(const KernelParams& kp, dim3 grid, int pf, cu
 cudaError_t launch_packed_rt_seg(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
 cudaError_t launch_packed_rt_pad(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
 
+// u8-only clamp_abs contract, default taps (sobel5_u8.cuh): 8 px per lane,
+// TMA band rows; its own grid (1024 columns per CTA) and band.
+int u8_fast_band(int out_w, int out_h, int frames);
+int u8_fast_cta_cols();
+cudaError_t launch_u8_fast(const KernelParams& kp, int frames, cudaStream_t s);
+
 // Packed-FP32 kernel with runtime taps (sobel5_f32x2.cuh), every geometry.
 cudaError_t launch_f32(const KernelParams& kp, dim3 grid, int pf, MagMode mag, cudaStream_t s);
 

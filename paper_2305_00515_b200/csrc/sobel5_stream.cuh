@@ -84,6 +84,7 @@ struct KernelParams {
     // taps (kernel parameter space -> constant-bank operands)
     int32_t f[5], h[5], k0[5], k1[5], gx_v[5], gy_v[5], gdm_f[5], gdm_d[5];
     int tma_load;  // packed plain kernel: band rows bulk-copied into shared memory
+    int frames;    // frames of the launch (the persistent u8 stream kernel splits them)
     // the same taps as floats for the packed-FP32 kernel (sobel5_f32x2.cuh):
     // f, h, k0, k1, gx_v, gy_v, gdm_f, -gdm_d
     float tf[8][5];

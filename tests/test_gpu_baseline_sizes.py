@@ -101,7 +101,8 @@ def test_c5_sr_sampled_rows_vs_oracle(c5, oracle):
 
 
 def test_c5_u8_contract_vs_oracle_and_full_plane(c5, oracle):
-    """u8-only launch (packed-float epilogue): sampled rows vs the oracle,
+    """u8-only launch (the u8 kernel, sobel5_u8.cuh: TMA band rows, packed
+    pairs, float epilogue): sampled rows vs the oracle,
     the whole plane vs clamp_abs of the SR launch's g on the device (g has no
     ties at k + 0.5: it is the sqrt of an integer, so round-half-even equals
     std::round)."""
@@ -110,7 +111,8 @@ def test_c5_u8_contract_vs_oracle_and_full_plane(c5, oracle):
     w, h = c5["w"], c5["h"]
     out, op = api.alloc_planes(w - 4, h - 4, ("u8",))
     api.launch(c5["d_in"], c5["pitch"], w, h, api.make_stream_taps(), 1, out, op)
-    assert api.last_launch()["tma_load"] == 0  # register ring, packed-float epilogue
+    li = api.last_launch()
+    assert li["tma_load"] == 1 and li["band"] == 16  # sobel5_u8_kernel, 16-row bands
     torch.cuda.synchronize()
     u8 = out["u8"]
     for oy0, n in c5_windows(h):

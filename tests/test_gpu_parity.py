@@ -255,14 +255,18 @@ def test_misaligned_arguments_rejected(S):
     del torch
 
 
-@pytest.mark.parametrize("which,hi", [(0, 1 << 30), (1, 1 << 31), (2, 65281), (3, 0x7F800000)],
-                         ids=["sqrt_u30", "u8_from_s", "u8_float_exact", "u8_float_saturated"])
+@pytest.mark.parametrize("which,hi", [(0, 1 << 30), (1, 1 << 31), (2, 65281), (3, 0x7F800000),
+                                      (4, 65281), (5, 0x7F800000)],
+                         ids=["sqrt_u30", "u8_from_s", "u8_float_exact", "u8_float_saturated",
+                              "u8_sqrt_exact", "u8_sqrt_saturated"])
 def test_epilogue_arithmetic_exhaustive(S, which, hi):
     """The fast epilogue is bit-identical to IEEE sqrt (which=0) and to
     clamp_abs(round(sqrt)) (which=1) for EVERY integer sum of squares the
     packed kernel can produce (default taps: S <= 4 * 12240^2 < 2^30); the
     u8-only kernels' packed-float epilogue is exact for every integer S <=
-    65280 (which=2) and saturates for every float S >= 65281 (which=3)."""
+    65280 (which=2) and saturates for every float S >= 65281 (which=3); the
+    same for the u8-only kernel's sqrt + saturating round (which=4/5,
+    sobel5_u8.cuh)."""
     import torch
     from paper_2305_00515_b200 import _abi
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
