@@ -19,7 +19,7 @@ LIB = os.path.join(LIBDIR, "libsobel5_b200.so")
 SOURCES = ["sobel5_abi.cu", "sobel5_ctx.cu", "sobel5_ipc.cu", "sobel5_detect.cu",
            "sobel5_k_plain.cu", "sobel5_k_seg.cu", "sobel5_k_pad.cu", "sobel5_k_generic.cu",
            "sobel3_k.cu", "sobel5_k_rtaps.cu", "sobel5_k_f32.cu", "sobel5_k_dense.cu",
-           "sobel5_conv2d.cu", "sobel5_mgpu.cu", "sobel5_k_u8.cu"]
+           "sobel5_conv2d.cu", "sobel5_mgpu.cu", "sobel5_k_u8.cu", "sobel5_tmap.cu"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

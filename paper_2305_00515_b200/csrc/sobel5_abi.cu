@@ -355,6 +355,15 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
         ((out->u8 && !(ex.u8_norm || ex.norm)) || (ex.minmax && ex.s32)) && taps_are_default(*taps))
         kp.tma_load = 1;
     if (kp.band > 32) kp.tma_load = 0;  // the shared-memory band holds 36 rows
+    // Opt-in (SOBEL5_TS=1 per-CTA boxes, 2 per-warp boxes): the plain
+    // StreamResult with TMA band rows written by TMA tensor stores (two staged
+    // rows per box) instead of register stores.  Measured slower at every band
+    // (8K: 142.4 / 142.8 us at band 8 vs 131.7 us; 32768 x 8192: 1096 vs
+    // 1069 us; profiles/r2/tma_store.txt): the staging round trip and the
+    // per-CTA store drain cost more than the write pattern gains, so register
+    // stores stay the default.
+    const bool sr_only = out->gx && out->gy && out->gd && out->gdt && out->g && !out->g32 &&
+                         !out->u8 && !ex.minmax && !ex.s32 && !ex.norm && !ex.u8_norm;
     kp.gx = out->gx;
     kp.gy = out->gy;
     kp.gd = out->gd;
@@ -372,6 +381,14 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     kp.u8_norm = ex.u8_norm;
     kp.s32 = ex.s32;
     fill_taps(kp, *taps);
+    kp.tstore = 0;
+    if (kp.tma_load && sr_only && !ex.pad && !top && !bot && env_int("SOBEL5_TS", 0) != 0) {
+        if (env_int("SOBEL5_BAND", 0) <= 0) kp.band = env_int("SOBEL5_TS_BAND", 8);
+        const int mode = env_int("SOBEL5_TS", 0);  // 1: CTA boxes, 2: per-warp boxes
+        if (kp.band <= kTsBandRows - 4 && kp.band % kTsRows == 0 &&
+            build_store_maps(kp, frames, kTsRows, mode == 2 ? kWarpCols : kTsBoxCols))
+            kp.tstore = mode;
+    }
 
     const dim3 grid(static_cast<unsigned>((out_w + kCtaCols - 1) / kCtaCols),
                     static_cast<unsigned>((out_h + kp.band - 1) / kp.band),
@@ -380,6 +397,7 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
         // very tall images: grow the band until the grid fits
         kp.band = (out_h + 65534) / 65535;
         if (kp.band > 32) kp.tma_load = 0;  // the shared-memory band holds 36 rows
+        if (kp.band > kTsBandRows - 4 || kp.band % kTsRows != 0) kp.tstore = 0;
     }
     const dim3 grid2(grid.x, static_cast<unsigned>((out_h + kp.band - 1) / kp.band), grid.z);
     // The u8-only clamp_abs edge map with default taps (plain / batch /

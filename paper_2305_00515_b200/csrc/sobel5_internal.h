@@ -28,6 +28,10 @@ int u8_fast_band(int out_w, int out_h, int frames);
 int u8_fast_cta_cols();
 cudaError_t launch_u8_fast(const KernelParams& kp, int frames, cudaStream_t s);
 
+// Tensor maps of the StreamResult planes for the TMA-store kernel
+// (sobel5_tmap.cu); false if the driver entry point or the layout is missing.
+bool build_store_maps(KernelParams& kp, int frames, int rows, int box_cols);
+
 // Packed-FP32 kernel with runtime taps (sobel5_f32x2.cuh), every geometry.
 cudaError_t launch_f32(const KernelParams& kp, dim3 grid, int pf, MagMode mag, cudaStream_t s);
 

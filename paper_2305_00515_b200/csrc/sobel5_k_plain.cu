@@ -12,6 +12,25 @@ cudaError_t go(const KernelParams& kp, dim3 grid, cudaStream_t s) {
     // shared memory the kernel reads each one when it is consumed
     // (instantiated with PF = 0): no register ring, 112 instead of 118
     // registers, 134.1 vs 134.9 us at 8K (profiles/r1/tma_load.txt).
+    if constexpr (OUTS == kOutSR) {
+        if (PF > 0 && kp.tma_load && kp.tstore == 2) {
+            static const cudaError_t attr = cudaFuncSetAttribute(
+                sobel5_packed_default_kernel<0, kGeomPlainTmaTw, kOutSR>,
+                cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmemBytes);
+            if (attr != cudaSuccess) return attr;
+            sobel5_packed_default_kernel<0, kGeomPlainTmaTw, kOutSR><<<grid, kCtaThreads, kTsSmemBytes, s>>>(kp);
+            return cudaGetLastError();
+        }
+        if (PF > 0 && kp.tma_load && kp.tstore) {
+            // StreamResult through TMA tensor stores (staging in dynamic smem)
+            static const cudaError_t attr = cudaFuncSetAttribute(
+                sobel5_packed_default_kernel<0, kGeomPlainTmaTs, kOutSR>,
+                cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmemBytes);
+            if (attr != cudaSuccess) return attr;
+            sobel5_packed_default_kernel<0, kGeomPlainTmaTs, kOutSR><<<grid, kCtaThreads, kTsSmemBytes, s>>>(kp);
+            return cudaGetLastError();
+        }
+    }
     if (PF > 0 && kp.tma_load)
         sobel5_packed_default_kernel<0, kGeomPlainTma, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
     else

@@ -243,6 +243,29 @@ __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---- TMA tensor stores of the StreamResult (kGeomPlainTmaTs) ---------------
+// Each CTA stages kTsRows output rows of its 512-column tile for every plane
+// in shared memory (double-buffered), then one thread writes them with six
+// cp.async.bulk.tensor stores (gx, gy, gd, gdt as uint64 pairs: one 512-column
+// box each; g: two 256-column boxes), coordinates from blockIdx only.
+constexpr int kTsBoxCols = kCtaCols;  // 512
+constexpr int kTsRows = 2;            // output rows per staged box
+constexpr int kTsIntBytes = kTsRows * kTsBoxCols * 4;        // one int32 plane
+constexpr int kTsGBytes = kTsRows * (kTsBoxCols / 2) * 8;    // one g half
+constexpr int kTsBufBytes = 4 * kTsIntBytes + 2 * kTsGBytes;  // 24 KB
+constexpr int kTsSmemBytes = 2 * kTsBufBytes;                 // dynamic shared memory
+constexpr int kTsBandRows = 12;  // shared-memory input rows: bands <= 8
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, const void* ssrc, int x, int y,
+                                             int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(tm),
+        "r"(smem_addr(ssrc)), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // Four bytes (each < 256) packed little-endian with two byte permutes.
 __device__ __forceinline__ uint32_t pack_u8x4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
@@ -291,7 +314,8 @@ template <int PF, int GEOM, int OUTS, bool RTAPS = false>
 __global__ void __launch_bounds__(kCtaThreads,
                                   (OUTS == kOutU8 && !RTAPS) ? SOBEL5_U8_MIN_CTAS
                                   : (GEOM == kGeomPlainTma || GEOM == kGeomPadTma ||
-                                     GEOM == kGeomSegTma)
+                                     GEOM == kGeomSegTma || GEOM == kGeomPlainTmaTs ||
+                                     GEOM == kGeomPlainTmaTw)
                                       ? SOBEL5_TMA_MIN_CTAS
                                       : kMinCtasPerSm)
     sobel5_packed_default_kernel(const __grid_constant__ KernelParams p) {
@@ -300,14 +324,21 @@ __global__ void __launch_bounds__(kCtaThreads,
     // TMAL: band rows by TMA into shared memory (tma_band_issue); the
     // launchers instantiate it with PF = 0, so each row is read from shared
     // memory when it is consumed
-    constexpr bool TMAL = GEOM == kGeomPlainTma || GEOM == kGeomPadTma || GEOM == kGeomSegTma;
-    __shared__ __align__(128) uint8_t s_band[TMAL ? TmaBand<PAD>::kBytes : 16];
+    // TS: the StreamResult leaves through TMA tensor stores (shared-memory
+    // staging, sobel5_tmap.cu builds the maps)
+    constexpr bool TS = GEOM == kGeomPlainTmaTs || GEOM == kGeomPlainTmaTw;
+    constexpr bool TW = GEOM == kGeomPlainTmaTw;  // per-warp boxes, no CTA barrier
+    static_assert(!TS || OUTS == kOutSR, "tensor stores: StreamResult only");
+    constexpr bool TMAL = GEOM == kGeomPlainTma || GEOM == kGeomPadTma || GEOM == kGeomSegTma || TS;
+    __shared__ __align__(128)
+        uint8_t s_band[TS ? kTsBandRows * TmaBand<false>::kRowBytes : TMAL ? TmaBand<PAD>::kBytes : 16];
+    extern __shared__ __align__(128) uint8_t s_dyn[];  // TS staging (kTsSmemBytes)
     __shared__ __align__(8) uint64_t s_bar[2];
     // StreamResult on the TMA-row kernel: write-back stores instead of .cs
 #ifndef SOBEL5_SR_WB
 #define SOBEL5_SR_WB 1
 #endif
-    constexpr bool WB = (SOBEL5_SR_WB == 2 || (SOBEL5_SR_WB == 1 && TMAL)) && OUTS == kOutSR;
+    constexpr bool WB = (SOBEL5_SR_WB == 2 || (SOBEL5_SR_WB == 1 && TMAL)) && OUTS == kOutSR && !TS;
     // which planes this instantiation writes (compile-time unless kOutRuntime)
     constexpr bool RT = OUTS == kOutRuntime;
     const bool w_gx = RT ? p.gx != nullptr : (OUTS & kOutGx) != 0;
@@ -367,7 +398,9 @@ __global__ void __launch_bounds__(kCtaThreads,
     }
     bool cta_tma = false;  // SEG: CTAs touching a halo row load from global
     if constexpr (TMAL) cta_tma = tma_band_issue<PAD, SEG>(p, s_band, s_bar);
-    if (warp_x0 >= p.out_w) return;  // whole warp right of the image
+    // whole warp right of the image (TS: it still joins the staging barriers;
+    // its columns are clipped by the tensor stores)
+    if ((!TS || TW) && warp_x0 >= p.out_w) return;
     const int oy0 = blockIdx.y * p.band;
     const int n_out = min(p.band, p.out_h - oy0);
     const int n_in = n_out + 4;
@@ -705,7 +738,70 @@ __global__ void __launch_bounds__(kCtaThreads,
                                            : u8_from_s(S[j]);
                     }
                 }
-                if (TMA && warp_full) {
+                if constexpr (TW) {
+                    // per-warp staging: [gx gy gd gdt: kTsRows x 128 int32][g: kTsRows x 128]
+                    const int rv = r - 4;
+                    const int k = rv % kTsRows;
+                    constexpr int kI = kTsRows * kWarpCols * 4, kWarpBuf = 4 * kI + 2 * kI;
+                    uint8_t* sb = s_dyn + (warp * 2 + ((rv / kTsRows) & 1)) * kWarpBuf;
+                    uint8_t* si = sb + k * (kWarpCols * 4) + lane * 16;
+                    *reinterpret_cast<int4*>(si) = make_int4(gx[0], gx[1], gx[2], gx[3]);
+                    *reinterpret_cast<int4*>(si + kI) = make_int4(gy[0], gy[1], gy[2], gy[3]);
+                    *reinterpret_cast<int4*>(si + 2 * kI) = make_int4(gd[0], gd[1], gd[2], gd[3]);
+                    *reinterpret_cast<int4*>(si + 3 * kI) = make_int4(gdt[0], gdt[1], gdt[2], gdt[3]);
+                    double2* sg = reinterpret_cast<double2*>(sb + 4 * kI + k * (kWarpCols * 8) + lane * 32);
+                    sg[0] = make_double2(g[0], g[1]);
+                    sg[1] = make_double2(g[2], g[3]);
+                    if (k == kTsRows - 1 || rv == n_out - 1) {
+                        fence_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            const int y = oy0 + rv - k, z = blockIdx.z;
+                            tma_store_3d(&p.tmap[0], sb, warp_x0 / 2, y, z);
+                            tma_store_3d(&p.tmap[1], sb + kI, warp_x0 / 2, y, z);
+                            tma_store_3d(&p.tmap[2], sb + 2 * kI, warp_x0 / 2, y, z);
+                            tma_store_3d(&p.tmap[3], sb + 3 * kI, warp_x0 / 2, y, z);
+                            tma_store_3d(&p.tmap[4], sb + 4 * kI, warp_x0, y, z);
+                            bulk_commit();
+                            bulk_wait_read<1>();  // the other buffer is free for the next stage
+                        }
+                        __syncwarp();
+                    }
+                } else if constexpr (TS) {
+                    // stage row rv of the band in buffer (rv / kTsRows) & 1
+                    const int rv = r - 4;
+                    const int k = rv % kTsRows;
+                    uint8_t* sb = s_dyn + ((rv / kTsRows) & 1) * kTsBufBytes;
+                    const int col = warp * kWarpCols + lane * 4;
+                    uint8_t* si = sb + k * (kTsBoxCols * 4) + col * 4;
+                    *reinterpret_cast<int4*>(si) = make_int4(gx[0], gx[1], gx[2], gx[3]);
+                    *reinterpret_cast<int4*>(si + kTsIntBytes) = make_int4(gy[0], gy[1], gy[2], gy[3]);
+                    *reinterpret_cast<int4*>(si + 2 * kTsIntBytes) = make_int4(gd[0], gd[1], gd[2], gd[3]);
+                    *reinterpret_cast<int4*>(si + 3 * kTsIntBytes) =
+                        make_int4(gdt[0], gdt[1], gdt[2], gdt[3]);
+                    double* sg = reinterpret_cast<double*>(
+                        sb + 4 * kTsIntBytes + (warp >> 1) * kTsGBytes + k * (kTsBoxCols / 2) * 8) +
+                        (col & (kTsBoxCols / 2 - 1));
+                    reinterpret_cast<double2*>(sg)[0] = make_double2(g[0], g[1]);
+                    reinterpret_cast<double2*>(sg)[1] = make_double2(g[2], g[3]);
+                    if (k == kTsRows - 1 || rv == n_out - 1) {
+                        fence_async_smem();  // this thread's staging -> async proxy
+                        if (threadIdx.x == 0) bulk_wait_read<0>();  // the other buffer is free
+                        named_bar_sync(1, kCtaThreads);
+                        if (threadIdx.x == 0) {
+                            const int y = oy0 + rv - k, z = blockIdx.z;
+                            const int x2 = blockIdx.x * (kTsBoxCols / 2);  // uint64 columns
+                            tma_store_3d(&p.tmap[0], sb, x2, y, z);
+                            tma_store_3d(&p.tmap[1], sb + kTsIntBytes, x2, y, z);
+                            tma_store_3d(&p.tmap[2], sb + 2 * kTsIntBytes, x2, y, z);
+                            tma_store_3d(&p.tmap[3], sb + 3 * kTsIntBytes, x2, y, z);
+                            tma_store_3d(&p.tmap[4], sb + 4 * kTsIntBytes, blockIdx.x * kTsBoxCols, y, z);
+                            tma_store_3d(&p.tmap[4], sb + 4 * kTsIntBytes + kTsGBytes,
+                                         blockIdx.x * kTsBoxCols + kTsBoxCols / 2, y, z);
+                            bulk_commit();
+                        }
+                    }
+                } else if (TMA && warp_full) {
                     // Stage the warp's row of every wide plane in shared
                     // memory; lane 0 writes each as one bulk copy (TMA,
                     // cp.async.bulk.global.shared::cta).
@@ -789,6 +885,8 @@ __global__ void __launch_bounds__(kCtaThreads,
         }
     }
     if (TMA && warp_full && lane == 0) bulk_wait_all();  // smem must outlive the copies
+    if (TS && !TW && threadIdx.x == 0) bulk_wait_read<0>();  // staging read before the CTA exits
+    if (TW && lane == 0) bulk_wait_read<0>();
     if (w_mm) {  // normalize pass 1: frame min / max of g = sqrt(S), monotone in S
         s_min = __reduce_min_sync(0xffffffffu, s_min);
         s_max = __reduce_max_sync(0xffffffffu, s_max);

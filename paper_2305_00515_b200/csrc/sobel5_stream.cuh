@@ -28,6 +28,8 @@
 //     int32 narrowing cast, for ANY caller-supplied taps.
 #pragma once
 
+#include <cuda.h>
+
 #include <cstdint>
 
 #include "sobel5_gpu.h"
@@ -84,10 +86,14 @@ struct KernelParams {
     // taps (kernel parameter space -> constant-bank operands)
     int32_t f[5], h[5], k0[5], k1[5], gx_v[5], gy_v[5], gdm_f[5], gdm_d[5];
     int tma_load;  // packed plain kernel: band rows bulk-copied into shared memory
-    int frames;    // frames of the launch (the persistent u8 stream kernel splits them)
+    int frames;    // frames of the launch
+    int tstore;    // StreamResult by TMA tensor stores (tmap valid)
     // the same taps as floats for the packed-FP32 kernel (sobel5_f32x2.cuh):
     // f, h, k0, k1, gx_v, gy_v, gdm_f, -gdm_d
     float tf[8][5];
+    // StreamResult by TMA tensor stores (kGeomPlainTmaTs): gx, gy, gd, gdt
+    // (as uint64 pairs) and g, built on the host (sobel5_tmap.cu)
+    alignas(64) CUtensorMap tmap[5];
 };
 
 // Compile-time default taps, (a, b, m, n) = (1, 2, 6, 4) (make_stream_taps,
@@ -202,6 +208,8 @@ enum Geom : int {
     kGeomPlainTma = 3,  // plain, the CTA's band rows bulk-copied (TMA) into shared memory
     kGeomPadTma = 4,    // pad_replicate fused, band rows (clamped) bulk-copied likewise
     kGeomSegTma = 5,    // stacked, band rows bulk-copied for CTAs whose rows are all in mid
+    kGeomPlainTmaTs = 6,  // plain + TMA band rows, StreamResult written by TMA tensor stores
+    kGeomPlainTmaTw = 7,  // the same, each warp storing its own 128-column boxes
 };
 
 // The 8-byte window (wa = input columns c..c+3, wb = c+4..c+7) a lane needs
