@@ -455,15 +455,33 @@ def main():
     hbm_peak, peak_kind, peaks = measured_peaks()
     alg_bytes = rank_in_px + rank_out_px * OUT_BYTES[a.contract]  # per rank, per launch set
     achieved = alg_bytes / (ms_step * 1e-3) / 1e9
-    traffic = None
+    # steady-state ncu numbers per launch (tools/traffic.sh + tools/traffic.py):
+    # DRAM bytes and warp-instructions of the same kernel at the same size
+    traffic, traffic_ratio, prof = None, None, {}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
-                tr = json.load(f)
-            traffic = tr.get(f"{a.workload}/{a.contract}")
+                prof = json.load(f)
+            t = prof.get(f"{a.workload}/{a.contract}")
+            if isinstance(t, dict) and frames == 1 and world == 1:
+                traffic = t["traffic"]
+                traffic_ratio = t["traffic"] / alg_bytes
         except Exception:
-            traffic = None
+            traffic, prof = None, {}
+
+    def issue_frac(key, us):
+        """Issue-rate roofline of an issue-bound kernel: its ncu warp-instruction
+        count per launch over what 4 SMSPs x 148 SMs issue at the run's median SM
+        clock in the measured time (1.0 = one instruction per SMSP per cycle)."""
+        t = prof.get(key)
+        mhz = clocks.summary().get("sm_mhz") or 1965.0
+        if not isinstance(t, dict) or not us:
+            return None
+        return {"frac": t["inst_per_launch"] / (4 * 148 * mhz * us),
+                "inst_per_launch": t["inst_per_launch"],
+                "thread_inst_per_px": t["inst_per_launch"] * 32 / (ow * oh),
+                "source": "profiles/traffic.json (ncu smsp__inst_executed.sum)"}
 
     # ---- variants (same workload, other output contracts / paths) ----
     # Each is timed like the headline (CUDA events around n launches on the
@@ -536,6 +554,11 @@ def main():
                 lambda d, vo, vp, sp: api.launch3(d, pitch, w, h, 1, False, vo, vp, stream=sp))
         variant("sobel3_u8", ("u8",), w - 2, h - 2, 1,
                 lambda d, vo, vp, sp: api.launch3(d, pitch, w, h, 1, False, vo, vp, stream=sp))
+        if a.workload == "8k":
+            # the u8 contracts are issue-bound: add the issue-rate roofline
+            for name, key in (("u8", "8k/u8"), ("sobel3_u8", "8k/sobel3_u8")):
+                if name in variants:
+                    variants[name]["issue_roofline"] = issue_frac(key, variants[name]["us"])
         torch.cuda.empty_cache()
 
     # ---- e2e through the C ABI host entry with pinned buffers ----
@@ -678,6 +701,7 @@ def main():
                        "hbm_gbs_achieved": achieved},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
+                         "traffic_ratio": traffic_ratio,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
                          if peak_kind == "measured" else "fallback (B200_PROFILING.md)",
                          "alg_bytes_per_launch": alg_bytes,
