@@ -25,6 +25,7 @@
 #include <string>
 #include <thread>
 #include <type_traits>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -453,10 +454,21 @@ inline sobel5_status collect_pending(sobel5_ctx* c, int ow, int oh, const std::v
     auto fill = [&](std::size_t k, auto& v) {
         try {
             using T = typename std::decay_t<decltype(v)>::value_type;
-            const T* src = static_cast<const T*>(sobel5_run_host_staging(c, planes[k].slot));
+            const void* stage = sobel5_run_host_staging(c, planes[k].slot);
+            // int32 planes may arrive as int16 (the narrow D2H wire): widen
+            const bool narrow = std::is_same_v<T, std::int32_t> &&
+                                sobel5_run_host_staging_elem(c, planes[k].slot) == 2;
             int y0 = 0, y1 = 0;
-            for (int ch = 0; sobel5_run_host_chunk(c, ch, &y0, &y1) == SOBEL5_OK; ++ch)
-                v.insert(v.end(), src + static_cast<std::size_t>(y0) * ow, src + static_cast<std::size_t>(y1) * ow);
+            for (int ch = 0; sobel5_run_host_chunk(c, ch, &y0, &y1) == SOBEL5_OK; ++ch) {
+                const std::size_t a = static_cast<std::size_t>(y0) * ow, b = static_cast<std::size_t>(y1) * ow;
+                if (narrow) {
+                    const auto* src = static_cast<const std::int16_t*>(stage);
+                    v.insert(v.end(), src + a, src + b);
+                } else {
+                    const T* src = static_cast<const T*>(stage);
+                    v.insert(v.end(), src + a, src + b);
+                }
+            }
             short_plane[k] = v.size() != n;
         } catch (...) {
             errs[k] = std::current_exception();

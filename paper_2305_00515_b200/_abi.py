@@ -91,7 +91,8 @@ EXPORTS = (
     "sobel5_detect_scratch_bytes", "sobel5_quantize_plane", "sobel5_detect_host",
     "sobel3_launch", "sobel3_detect", "sobel3_plan_counters", "sobel3_run_host",
     "sobel5_quantize_host", "sobel5_run_host_begin", "sobel5_run_host_finish",
-    "sobel5_run_host_chunk", "sobel5_run_host_staging", "sobel5_kernel_for_taps",
+    "sobel5_run_host_chunk", "sobel5_run_host_staging", "sobel5_run_host_staging_elem",
+    "sobel5_kernel_for_taps",
     "sobel3_run_host_begin", "sobel5_ctx_trim", "sobel5_last_launch",
     "sobel5_conv2d_valid", "sobel5_conv2d_valid_host", "sobel5_dense_4d", "sobel5_dense_4d_host",
     "sobel5_mgpu_create", "sobel5_mgpu_destroy", "sobel5_mgpu_band", "sobel5_mgpu_upload",
@@ -197,6 +198,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.sobel5_run_host_chunk.restype = i32
     L.sobel5_run_host_staging.argtypes = [vp, i32]
     L.sobel5_run_host_staging.restype = vp
+    L.sobel5_run_host_staging_elem.argtypes = [vp, i32]
+    L.sobel5_run_host_staging_elem.restype = i32
     L.sobel5_ipc_export.argtypes = [vp, C.POINTER(IpcHandle)]
     L.sobel5_ipc_export.restype = i32
     L.sobel5_ipc_import.argtypes = [C.POINTER(IpcHandle), C.POINTER(vp)]

@@ -19,8 +19,10 @@ LIB = os.path.join(LIBDIR, "libsobel5_b200.so")
 SOURCES = ["sobel5_abi.cu", "sobel5_ctx.cu", "sobel5_ipc.cu", "sobel5_detect.cu",
            "sobel5_k_plain.cu", "sobel5_k_seg.cu", "sobel5_k_pad.cu", "sobel5_k_generic.cu",
            "sobel3_k.cu", "sobel5_k_rtaps.cu", "sobel5_k_f32.cu", "sobel5_k_dense.cu",
-           "sobel5_conv2d.cu", "sobel5_mgpu.cu", "sobel5_k_u8.cu", "sobel5_tmap.cu"]
+           "sobel5_conv2d.cu", "sobel5_mgpu.cu", "sobel5_k_u8.cu", "sobel5_tmap.cu",
+           "sobel5_wire.cpp"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
+# host-only translation units (.cpp) go through nvcc to the host compiler
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
@@ -56,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nv = nvcc()
 
     def compile_one(src):
-        obj = os.path.join(OBJDIR, src.replace(".cu", ".o"))
+        obj = os.path.join(OBJDIR, os.path.splitext(src)[0] + ".o")
         extra = os.environ.get("SOBEL5_NVCC_EXTRA", "").split()
         cmd = [nv] + NVCC_FLAGS + extra + (["-Xptxas=-v"] if verbose else []) + [
             "-c", os.path.join(CSRC, src), "-o", obj]

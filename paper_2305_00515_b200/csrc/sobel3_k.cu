@@ -20,10 +20,8 @@ constexpr int kOut3 = kOutGx | kOutGy | kOutG;  // Stream3Result
 template <int PF, bool PAD, int OUTS>
 cudaError_t go(const KernelParams& kp, dim3 grid, cudaStream_t s) {
     if (PF > 0 && kp.tma_load)  // band rows by TMA (sobel3_common decides)
-        sobel3_packed_kernel<0, PAD, OUTS, true><<<grid, kCtaThreads, 0, s>>>(kp);
-    else
-        sobel3_packed_kernel<PF, PAD, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
-    return cudaGetLastError();
+        return launch_kp(sobel3_packed_kernel<0, PAD, OUTS, true>, grid, kCtaThreads, 0, s, kp);
+    return launch_kp(sobel3_packed_kernel<PF, PAD, OUTS>, grid, kCtaThreads, 0, s, kp);
 }
 
 template <int PF, bool PAD>

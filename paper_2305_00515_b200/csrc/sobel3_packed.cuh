@@ -28,6 +28,7 @@ namespace sobel5_b200 {
 template <int PF, bool PAD, int OUTS, bool TMAL = false>
 __global__ void __launch_bounds__(kCtaThreads, OUTS == kOutU8 ? SOBEL5_U8_MIN_CTAS : kMinCtasPerSm)
     sobel3_packed_kernel(const __grid_constant__ KernelParams p) {
+    pdl_enter();
     constexpr int kTmaLead = PAD ? 16 : 0;  // PAD: lane 0's left word precedes the CTA's columns
     constexpr int kTmaRowBytes = kCtaCols + 16 + kTmaLead, kTmaRows = 34;
     __shared__ __align__(128) uint8_t s_band[TMAL ? kTmaRows * kTmaRowBytes : 16];

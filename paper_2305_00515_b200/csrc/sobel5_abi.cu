@@ -248,7 +248,16 @@ cudaError_t dispatch(const KernelParams& kp, dim3 grid, int prefetch, bool dflt,
 
 namespace sobel5_b200 {
 
+bool pdl_enabled() {
+    static const bool on = env_int("SOBEL5_PDL", 1) != 0;
+    return on;
+}
+
 bool taps_default(const sobel5_taps* t) { return taps_are_default(*t); }
+bool n16_wire_ok(const sobel5_taps* t) {
+    return t && taps_are_default(*t) && env_int("SOBEL5_WIRE16", 1) != 0 &&
+           env_int("SOBEL5_GENERIC", 0) == 0 && env_int("SOBEL5_DENSE", 0) == 0;
+}
 bool taps_packed(const sobel5_taps* t) {
     return env_int("SOBEL5_GENERIC", 0) == 0 && (taps_are_default(*t) || taps_fit_packed(*t));
 }
@@ -296,6 +305,10 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     // the S plane exists only for the packed kernels (exact integer S)
     if (ex.s32 && !taps_packed(taps)) return SOBEL5_INVALID_ARG;
     if (rows > (int64_t{1} << 30) || frames > 65535) return SOBEL5_INVALID_ARG;
+    if (ex.n16 && (top || bot || ex.pad || !n16_wire_ok(taps) || !out->gx || !out->gy ||
+                   !out->gd || !out->gdt || !out->g || out->g32 || out->u8 || ex.minmax ||
+                   ex.norm || ex.u8_norm || ex.s32))
+        return SOBEL5_INVALID_ARG;
 
     KernelParams kp{};
     kp.top = top;
@@ -363,7 +376,7 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     // per-CTA store drain cost more than the write pattern gains, so register
     // stores stay the default.
     const bool sr_only = out->gx && out->gy && out->gd && out->gdt && out->g && !out->g32 &&
-                         !out->u8 && !ex.minmax && !ex.s32 && !ex.norm && !ex.u8_norm;
+                         !out->u8 && !ex.minmax && !ex.s32 && !ex.norm && !ex.u8_norm && !ex.n16;
     kp.gx = out->gx;
     kp.gy = out->gy;
     kp.gd = out->gd;
@@ -380,6 +393,7 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     kp.norm = ex.norm;
     kp.u8_norm = ex.u8_norm;
     kp.s32 = ex.s32;
+    kp.n16 = ex.n16;
     fill_taps(kp, *taps);
     kp.tstore = 0;
     if (kp.tma_load && sr_only && !ex.pad && !top && !bot && env_int("SOBEL5_TS", 0) != 0) {

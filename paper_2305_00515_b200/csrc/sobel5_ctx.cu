@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "sobel5_gpu.h"
+#include "sobel5_internal.h"
 
 namespace {
 
@@ -131,6 +132,11 @@ struct sobel5_ctx {
     size_t h_in_stage_bytes = 0;
     void* h_stage[7] = {};
     size_t h_stage_bytes[7] = {};
+    // int16 wire (SOBEL5_WIRE16): gx gy gd gdt of the current call land here
+    // as int16 and are widened into the int32 destinations (sobel5_wire.cpp)
+    void* h_wire[4] = {};
+    size_t h_wire_bytes[4] = {};
+    bool wire = false;
     std::vector<cudaEvent_t> ev_in, ev_comp, ev_out;
     HostPool pool;
     // state between sobel5_run_host_begin and _finish
@@ -148,6 +154,23 @@ namespace {
 constexpr size_t kElem[7] = {4, 4, 4, 4, 8, 4, 1};  // gx gy gd gdt g g32 u8
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// bytes per element of plane slot i as it crosses PCIe in the current call
+size_t wire_elem(const sobel5_ctx* ctx, int i) { return ctx->wire && i < 4 ? 2 : kElem[i]; }
+
+// The int16 wire applies to a 5x5 call with exactly the StreamResult planes
+// and default taps (sobel5_b200::n16_wire_ok), if its int16 staging fits.
+// The split begin/_chunk form (the C++ drop-in, which fills freshly
+// allocated planes and is bound by page faults, not PCIe) uses it only when
+// SOBEL5_WIRE16=2: its consumers' int16 -> int32 appends measured slower
+// (8K run_stream 64 vs 55 ms).
+bool want_wire(unsigned mask, const sobel5_taps* taps, int op, bool split) {
+    if (split) {
+        const char* v = std::getenv("SOBEL5_WIRE16");
+        if (!v || std::atoi(v) < 2) return false;
+    }
+    return op == 5 && mask == 0x1fu && sobel5_b200::n16_wire_ok(taps);
+}
 
 sobel5_status fail(sobel5_ctx* c, cudaError_t e) {
     c->last_error = cudaGetErrorString(e);
@@ -294,8 +317,9 @@ void finish_staged(sobel5_ctx* ctx, void* const staged[7], int out_w, int rows) 
 sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
                              const sobel5_taps* taps, int prefetch, unsigned mask,
                              void* const dst[7], int* chunk_out, int* n_chunks_out,
-                             StageBudget& budget, int op = 5) {
+                             StageBudget& budget, int op = 5, bool wire = false) {
     const int R = op == 3 ? 1 : 2;  // operator radius
+    ctx->wire = wire;
     const int out_w = width - 2 * R, out_h = height - 2 * R;
     const int64_t in_pitch = round_up(width, 128);
     const int64_t dpitch = round_up(out_w, 32);  // elements; 128 B-aligned int rows
@@ -315,11 +339,14 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
     void* hdst[7] = {};
     for (int i = 0; i < 7; ++i) {
         if (!((mask >> i) & 1u)) continue;
-        const size_t plane_bytes = static_cast<size_t>(out_w) * out_h * kElem[i];
+        const size_t plane_bytes = static_cast<size_t>(out_w) * out_h * wire_elem(ctx, i);
         CK(ensure(&ctx->d_plane[i], &ctx->d_plane_bytes[i],
                   static_cast<size_t>(dpitch) * out_h * kElem[i]));
         *dslots[i] = ctx->d_plane[i];
-        if (dst[i]) {
+        if (wire && i < 4) {
+            CK(ensure_host(&ctx->h_wire[i], &ctx->h_wire_bytes[i], plane_bytes));
+            hdst[i] = ctx->h_wire[i];
+        } else if (dst[i]) {
             hdst[i] = dst[i];
         } else {
             CK(ensure_host(&ctx->h_stage[i], &ctx->h_stage_bytes[i], plane_bytes));
@@ -329,7 +356,10 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
 
     // Row chunks: enough to overlap copies with compute, few enough that
     // each kernel still fills the GPU.
-    int chunk = std::max(256, (out_h + 7) / 8);
+    // (16 with the int16 wire: the host widening of chunk k overlaps the
+    // download of chunk k+1, so shorter chunks expose less of it)
+    const int n_want = wire ? 16 : 8;
+    int chunk = std::max(256, (out_h + n_want - 1) / n_want);
     chunk = std::min(chunk, out_h);
     const int n_chunks = (out_h + chunk - 1) / chunk;
     CK(ensure_events(ctx->ev_in, static_cast<size_t>(n_chunks)));
@@ -349,19 +379,25 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
         CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_in[k], 0));
         sobel5_planes sub = dp;
         const int64_t off = static_cast<int64_t>(y0) * dpitch;
-        if (sub.gx) sub.gx += off;
-        if (sub.gy) sub.gy += off;
-        if (sub.gd) sub.gd += off;
-        if (sub.gdt) sub.gdt += off;
+        // int16 wire planes: the kernel addresses them as int16 at the int32
+        // pointer (dpitch is even, so the chunk starts on an int32 boundary)
+        const int64_t off_g = wire ? off / 2 : off;
+        if (sub.gx) sub.gx += off_g;
+        if (sub.gy) sub.gy += off_g;
+        if (sub.gd) sub.gd += off_g;
+        if (sub.gdt) sub.gdt += off_g;
         if (sub.g) sub.g += off;
         if (sub.g32) sub.g32 += off;
         if (sub.u8) sub.u8 += off;
         const uint8_t* d_rows = ctx->d_in + static_cast<int64_t>(y0) * in_pitch;
+        sobel5_b200::LaunchExtra ex;
+        ex.n16 = wire ? 1 : 0;
         const sobel5_status st =
             op == 3 ? sobel3_launch(d_rows, in_pitch, 0, width, y1 - y0 + 2, 1, prefetch, 0, &sub, 0,
                                     ctx->s_comp)
-                    : sobel5_launch(d_rows, in_pitch, width, y1 - y0 + 4, taps, prefetch, &sub,
-                                    ctx->d_diag, ctx->s_comp);
+                    : sobel5_b200::launch_common(nullptr, d_rows, nullptr, in_pitch, 0, width,
+                                                 y1 - y0 + 4, 1, taps, prefetch, &sub, 0,
+                                                 ctx->d_diag, ctx->s_comp, ex);
         if (st != SOBEL5_OK) {
             ctx->last_error = cudaGetErrorString(cudaGetLastError());
             return st;
@@ -370,7 +406,7 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
         CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_comp[k], 0));
         for (int i = 0; i < 7; ++i) {
             if (!hdst[i]) continue;
-            const size_t es = kElem[i];
+            const size_t es = wire_elem(ctx, i);
             CK(cudaMemcpy2DAsync(static_cast<char*>(hdst[i]) + static_cast<size_t>(y0) * out_w * es,
                                  static_cast<size_t>(out_w) * es,
                                  static_cast<char*>(ctx->d_plane[i]) +
@@ -398,7 +434,8 @@ sobel5_status drain_stream(sobel5_ctx* ctx, int out_w, int out_h, int chunk, int
     struct Piece {
         char* dst;
         const char* src;
-        size_t n;
+        size_t n;     // bytes of src
+        bool widen;   // int16 wire -> int32 destination
     };
     std::vector<Piece> pieces;
     for (int k = 0; k < n_chunks; ++k) {
@@ -407,19 +444,25 @@ sobel5_status drain_stream(sobel5_ctx* ctx, int out_w, int out_h, int chunk, int
         pieces.clear();
         for (int i = 0; i < 7; ++i) {
             if (!stage_dst[i]) continue;
-            const size_t row = static_cast<size_t>(out_w) * kElem[i];
+            const bool widen = ctx->wire && i < 4;
+            const size_t es = wire_elem(ctx, i), row = static_cast<size_t>(out_w) * es;
             const size_t off = static_cast<size_t>(y0) * row, n = static_cast<size_t>(y1 - y0) * row;
+            const char* src = static_cast<const char*>(widen ? ctx->h_wire[i] : ctx->h_stage[i]);
             for (size_t o = 0; o < n; o += kPiece)
-                pieces.push_back({static_cast<char*>(stage_dst[i]) + off + o,
-                                  static_cast<const char*>(ctx->h_stage[i]) + off + o,
-                                  std::min(kPiece, n - o)});
+                pieces.push_back({static_cast<char*>(stage_dst[i]) + (widen ? 2 : 1) * (off + o),
+                                  src + off + o, std::min(kPiece, n - o), widen});
         }
+        auto move = [&](const Piece& q) {
+            if (q.widen)
+                sobel5_b200::widen_i16(reinterpret_cast<int32_t*>(q.dst),
+                                       reinterpret_cast<const int16_t*>(q.src), q.n / 2);
+            else
+                std::memcpy(q.dst, q.src, q.n);
+        };
         if (pieces.size() == 1) {
-            std::memcpy(pieces[0].dst, pieces[0].src, pieces[0].n);
+            move(pieces[0]);
         } else if (!pieces.empty()) {
-            ctx->pool.run(static_cast<int>(pieces.size()), [&](int t) {
-                std::memcpy(pieces[t].dst, pieces[t].src, pieces[t].n);
-            });
+            ctx->pool.run(static_cast<int>(pieces.size()), [&](int t) { move(pieces[t]); });
         }
     }
     CK(cudaStreamSynchronize(ctx->s_d2h));
@@ -471,6 +514,8 @@ void sobel5_ctx_destroy(sobel5_ctx* ctx) {
         if (p) cudaFree(p);
     for (void* p : ctx->h_stage)
         if (p) cudaFreeHost(p);
+    for (void* p : ctx->h_wire)
+        if (p) cudaFreeHost(p);
     if (ctx->h_in_stage) cudaFreeHost(ctx->h_in_stage);
     if (ctx->d_diag) cudaFree(ctx->d_diag);
     if (ctx->d_scratch) cudaFree(ctx->d_scratch);
@@ -498,20 +543,27 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     void* hp[7];
     planes_array(h_out, hp);
     unsigned mask = 0;
+    for (int i = 0; i < 7; ++i)
+        if (hp[i]) mask |= 1u << i;
     void* direct[7] = {};  // pinned destinations: DMA straight into them
-    void* staged[7] = {};  // pageable ones: through pinned staging
+    void* staged[7] = {};  // pageable ones: through pinned staging (and the int16 wire planes)
     StageBudget budget;    // the planes first, then the input if it still fits
+    const size_t n_px = static_cast<size_t>(out_w) * out_h;
+    const bool wire = want_wire(mask, taps, 5, false) && budget.take(4 * n_px * 2);
     for (int i = 0; i < 7; ++i) {
         if (!hp[i]) continue;
-        mask |= 1u << i;
-        if (!is_pinned(hp[i]) && budget.take(static_cast<size_t>(out_w) * out_h * kElem[i]))
+        if (wire && i < 4) {
+            staged[i] = hp[i];  // widened from the int16 staging into the caller's plane
+            continue;
+        }
+        if (!is_pinned(hp[i]) && budget.take(n_px * kElem[i]))
             staged[i] = hp[i];
         else
             direct[i] = hp[i];  // pinned, or over the staging cap: driver-staged copy
     }
     int chunk = 0, n_chunks = 0;
     const sobel5_status st = enqueue_stream(ctx, h_in, width, height, taps, prefetch, mask, direct,
-                                            &chunk, &n_chunks, budget);
+                                            &chunk, &n_chunks, budget, 5, wire);
     if (st != SOBEL5_OK) return st;
     return drain_stream(ctx, out_w, out_h, chunk, n_chunks, staged, diag_out);
 }
@@ -524,6 +576,11 @@ void sobel5_ctx_trim(sobel5_ctx* ctx) {
         if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
         ctx->h_stage[i] = nullptr;
         ctx->h_stage_bytes[i] = 0;
+        if (i < 4) {
+            if (ctx->h_wire[i]) cudaFreeHost(ctx->h_wire[i]);
+            ctx->h_wire[i] = nullptr;
+            ctx->h_wire_bytes[i] = 0;
+        }
         if (ctx->d_plane[i]) cudaFree(ctx->d_plane[i]);
         ctx->d_plane[i] = nullptr;
         ctx->d_plane_bytes[i] = 0;
@@ -545,17 +602,19 @@ namespace {
 sobel5_status begin_common(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
                            const sobel5_taps* taps, int prefetch, unsigned plane_mask, int op) {
     const int R = op == 3 ? 1 : 2;
+    const bool wire = want_wire(plane_mask, taps, op, true);
     size_t stage_bytes = 0;
     for (int i = 0; i < 7; ++i)
         if ((plane_mask >> i) & 1u)
-            stage_bytes += static_cast<size_t>(width - 2 * R) * (height - 2 * R) * kElem[i];
+            stage_bytes += static_cast<size_t>(width - 2 * R) * (height - 2 * R) *
+                           (wire && i < 4 ? 2 : kElem[i]);
     StageBudget budget;  // the planes must fit; the input is staged if it still does
     if (!budget.take(stage_bytes)) return SOBEL5_OUT_OF_MEMORY;  // callers use run_host
     CK(cudaSetDevice(ctx->device));
     void* none[7] = {};
     int chunk = 0, n_chunks = 0;
     const sobel5_status st = enqueue_stream(ctx, h_in, width, height, taps, prefetch, plane_mask,
-                                            none, &chunk, &n_chunks, budget, op);
+                                            none, &chunk, &n_chunks, budget, op, wire);
     if (st != SOBEL5_OK) {
         // drain whatever was enqueued so the context stays usable
         cudaStreamSynchronize(ctx->s_h2d);
@@ -631,7 +690,13 @@ sobel5_status sobel5_run_host_chunk(sobel5_ctx* ctx, int chunk, int* y0, int* y1
 const void* sobel5_run_host_staging(const sobel5_ctx* ctx, int plane) {
     if (!ctx || !ctx->pend.active || plane < 0 || plane >= 7 || !((ctx->pend.mask >> plane) & 1u))
         return nullptr;
-    return ctx->h_stage[plane];
+    return ctx->wire && plane < 4 ? ctx->h_wire[plane] : ctx->h_stage[plane];
+}
+
+int sobel5_run_host_staging_elem(const sobel5_ctx* ctx, int plane) {
+    if (!ctx || !ctx->pend.active || plane < 0 || plane >= 7 || !((ctx->pend.mask >> plane) & 1u))
+        return 0;
+    return static_cast<int>(wire_elem(ctx, plane));
 }
 
 sobel5_status sobel5_detect_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,

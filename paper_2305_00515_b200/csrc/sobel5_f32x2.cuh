@@ -57,6 +57,7 @@ __device__ __forceinline__ float2 f2(float t) { return make_float2(t, t); }
 template <int PF, int GEOM, int MAG, int OUTS>
 __global__ void __launch_bounds__(kCtaThreads, SOBEL5_F32_MIN_CTAS)
     sobel5_f32x2_kernel(const __grid_constant__ KernelParams p) {
+    pdl_enter();
     constexpr bool SEG = GEOM == kGeomSeg;
     constexpr bool PAD = GEOM == kGeomPad;
     constexpr bool RT = OUTS == kOutRuntime;

@@ -12,6 +12,28 @@
 
 namespace sobel5_b200 {
 
+// PDL on the stream kernels (SOBEL5_PDL, default 1; see pdl_enter()).
+bool pdl_enabled();
+
+// Launches kernel k(kp) with the programmatic-stream-serialization
+// attribute when PDL is enabled (every kernel launched this way calls
+// pdl_enter() first).
+template <typename Kernel>
+cudaError_t launch_kp(Kernel k, dim3 grid, int threads, size_t smem, cudaStream_t s,
+                      const KernelParams& kp) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(static_cast<unsigned>(threads));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, kp);
+}
+
 // Packed default-taps kernel (sobel5_packed.cuh), one launcher per geometry.
 cudaError_t launch_packed_plain(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
 cudaError_t launch_packed_seg(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
@@ -49,7 +71,16 @@ struct LaunchExtra {
     const sobel5_norm_table* norm = nullptr;   // normalize pass 2
     int u8_norm = 0;
     uint32_t* s32 = nullptr;                   // exact g^2 plane (normalize pass 1)
+    int n16 = 0;                               // gx..gdt as int16 (host-path wire)
 };
+
+// The int16 D2H wire of the host path (sobel5_ctx.cu) applies: default taps
+// on the packed kernel (every gradient in [-2^15, 2^15)) and SOBEL5_WIRE16
+// not 0.  launch_common accepts n16 only for plain images with exactly the
+// StreamResult planes.
+bool n16_wire_ok(const sobel5_taps* taps);
+// Sign-extends n int16 into int32 (sobel5_wire.cpp: AVX2 streaming stores).
+void widen_i16(int32_t* dst, const int16_t* src, size_t n);
 
 // Common launch path (validation in the reference's order, geometry, kernel
 // selection) for plain, batched, band and detect launches.

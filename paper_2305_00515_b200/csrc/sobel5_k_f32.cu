@@ -10,10 +10,8 @@ template <int PF, int GEOM, int OUTS>
 cudaError_t go2(const KernelParams& kp, dim3 grid, MagMode mag, cudaStream_t s) {
     // every value is below 2^22, so S < 2^46: exact in uint64 (kMagU64)
     if (mag == kMagU32)
-        sobel5_f32x2_kernel<PF, GEOM, kMagU32, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
-    else
-        sobel5_f32x2_kernel<PF, GEOM, kMagU64, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
-    return cudaGetLastError();
+        return launch_kp(sobel5_f32x2_kernel<PF, GEOM, kMagU32, OUTS>, grid, kCtaThreads, 0, s, kp);
+    return launch_kp(sobel5_f32x2_kernel<PF, GEOM, kMagU64, OUTS>, grid, kCtaThreads, 0, s, kp);
 }
 
 template <int PF, int GEOM>

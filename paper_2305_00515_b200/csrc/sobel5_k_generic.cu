@@ -8,10 +8,8 @@ namespace {
 template <int PF, class TAPS, int MAG>
 cudaError_t go(const KernelParams& kp, dim3 grid, cudaStream_t s) {
     if (kp.pad)
-        sobel5_stream_kernel<PF, TAPS, MAG, true><<<grid, kCtaThreads, 0, s>>>(kp);
-    else
-        sobel5_stream_kernel<PF, TAPS, MAG, false><<<grid, kCtaThreads, 0, s>>>(kp);
-    return cudaGetLastError();
+        return launch_kp(sobel5_stream_kernel<PF, TAPS, MAG, true>, grid, kCtaThreads, 0, s, kp);
+    return launch_kp(sobel5_stream_kernel<PF, TAPS, MAG, false>, grid, kCtaThreads, 0, s, kp);
 }
 
 template <int PF>

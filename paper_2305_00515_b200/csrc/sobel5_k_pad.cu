@@ -10,10 +10,8 @@ namespace {
 template <int PF, int OUTS>
 cudaError_t go(const KernelParams& kp, dim3 grid, cudaStream_t s) {
     if (PF > 0 && kp.tma_load)  // band rows (clamped) by TMA (launch_common decides)
-        sobel5_packed_default_kernel<0, kGeomPadTma, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
-    else
-        sobel5_packed_default_kernel<PF, kGeomPad, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
-    return cudaGetLastError();
+        return launch_kp(sobel5_packed_default_kernel<0, kGeomPadTma, OUTS>, grid, kCtaThreads, 0, s, kp);
+    return launch_kp(sobel5_packed_default_kernel<PF, kGeomPad, OUTS>, grid, kCtaThreads, 0, s, kp);
 }
 
 template <int PF>

@@ -18,8 +18,7 @@ cudaError_t go(const KernelParams& kp, dim3 grid, cudaStream_t s) {
                 sobel5_packed_default_kernel<0, kGeomPlainTmaTw, kOutSR>,
                 cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmemBytes);
             if (attr != cudaSuccess) return attr;
-            sobel5_packed_default_kernel<0, kGeomPlainTmaTw, kOutSR><<<grid, kCtaThreads, kTsSmemBytes, s>>>(kp);
-            return cudaGetLastError();
+            return launch_kp(sobel5_packed_default_kernel<0, kGeomPlainTmaTw, kOutSR>, grid, kCtaThreads, kTsSmemBytes, s, kp);
         }
         if (PF > 0 && kp.tma_load && kp.tstore) {
             // StreamResult through TMA tensor stores (staging in dynamic smem)
@@ -27,15 +26,12 @@ cudaError_t go(const KernelParams& kp, dim3 grid, cudaStream_t s) {
                 sobel5_packed_default_kernel<0, kGeomPlainTmaTs, kOutSR>,
                 cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmemBytes);
             if (attr != cudaSuccess) return attr;
-            sobel5_packed_default_kernel<0, kGeomPlainTmaTs, kOutSR><<<grid, kCtaThreads, kTsSmemBytes, s>>>(kp);
-            return cudaGetLastError();
+            return launch_kp(sobel5_packed_default_kernel<0, kGeomPlainTmaTs, kOutSR>, grid, kCtaThreads, kTsSmemBytes, s, kp);
         }
     }
     if (PF > 0 && kp.tma_load)
-        sobel5_packed_default_kernel<0, kGeomPlainTma, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
-    else
-        sobel5_packed_default_kernel<PF, kGeomPlain, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
-    return cudaGetLastError();
+        return launch_kp(sobel5_packed_default_kernel<0, kGeomPlainTma, OUTS>, grid, kCtaThreads, 0, s, kp);
+    return launch_kp(sobel5_packed_default_kernel<PF, kGeomPlain, OUTS>, grid, kCtaThreads, 0, s, kp);
 }
 
 template <int PF>
@@ -43,6 +39,7 @@ cudaError_t outs(const KernelParams& kp, dim3 grid, cudaStream_t s) {
     // compile-time output sets for the common contracts, runtime otherwise
     switch (packed_out_set(kp)) {
         case kOutSR: return go<PF, kOutSR>(kp, grid, s);
+        case kOutSR | kOutN16: return go<PF, kOutSR | kOutN16>(kp, grid, s);
         case kOutSR | kOutU8: return go<PF, kOutSR | kOutU8>(kp, grid, s);
         case kOutU8: return go<PF, kOutU8>(kp, grid, s);
         case 15 | kOutG32: return go<PF, 15 | kOutG32>(kp, grid, s);

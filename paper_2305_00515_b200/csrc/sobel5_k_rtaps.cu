@@ -9,8 +9,7 @@ namespace sobel5_b200 {
 namespace {
 template <int PF, int GEOM, int OUTS>
 cudaError_t go(const KernelParams& kp, dim3 grid, cudaStream_t s) {
-    sobel5_packed_default_kernel<PF, GEOM, OUTS, true><<<grid, kCtaThreads, 0, s>>>(kp);
-    return cudaGetLastError();
+    return launch_kp(sobel5_packed_default_kernel<PF, GEOM, OUTS, true>, grid, kCtaThreads, 0, s, kp);
 }
 
 template <int PF, int GEOM>

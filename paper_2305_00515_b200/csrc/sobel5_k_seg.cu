@@ -11,10 +11,8 @@ cudaError_t go(const KernelParams& kp, dim3 grid, cudaStream_t s) {
     // band rows by TMA for the CTAs whose rows are all in the local band
     // (launch_common decides); the halo-touching CTAs load from global
     if (PF > 0 && kp.tma_load)
-        sobel5_packed_default_kernel<0, kGeomSegTma, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
-    else
-        sobel5_packed_default_kernel<PF, kGeomSeg, OUTS><<<grid, kCtaThreads, 0, s>>>(kp);
-    return cudaGetLastError();
+        return launch_kp(sobel5_packed_default_kernel<0, kGeomSegTma, OUTS>, grid, kCtaThreads, 0, s, kp);
+    return launch_kp(sobel5_packed_default_kernel<PF, kGeomSeg, OUTS>, grid, kCtaThreads, 0, s, kp);
 }
 
 template <int PF>

@@ -26,10 +26,8 @@ cudaError_t go(const KernelParams& kp, int frames, cudaStream_t s) {
                     static_cast<unsigned>((kp.out_h + kp.band - 1) / kp.band),
                     static_cast<unsigned>(frames));
     if (kp.pad)
-        sobel5_u8_kernel<NP, true><<<grid, kU8Threads, 0, s>>>(kp);
-    else
-        sobel5_u8_kernel<NP, false><<<grid, kU8Threads, 0, s>>>(kp);
-    return cudaGetLastError();
+        return launch_kp(sobel5_u8_kernel<NP, true>, grid, kU8Threads, 0, s, kp);
+    return launch_kp(sobel5_u8_kernel<NP, false>, grid, kU8Threads, 0, s, kp);
 }
 }  // namespace
 

@@ -41,6 +41,10 @@ namespace sobel5_b200 {
 enum : int {
     kOutGx = 1, kOutGy = 2, kOutGd = 4, kOutGdt = 8, kOutG = 16, kOutG32 = 32, kOutU8 = 64,
     kOutMinMax = 128, kOutNorm = 256, kOutS32 = 512,
+    // gx, gy, gd, gdt written as int16 (the host path's narrow D2H wire:
+    // every packed-kernel gradient lies in [-2^15, 2^15), sobel5_ctx.cu
+    // widens them into the caller's int32 planes)
+    kOutN16 = 1024,
     kOutSR = 31, kOutRuntime = -1
 };
 
@@ -49,7 +53,7 @@ inline int packed_out_set(const KernelParams& kp) {
     return (kp.gx ? kOutGx : 0) | (kp.gy ? kOutGy : 0) | (kp.gd ? kOutGd : 0) |
            (kp.gdt ? kOutGdt : 0) | (kp.g ? kOutG : 0) | (kp.g32 ? kOutG32 : 0) |
            (kp.u8 ? kOutU8 : 0) | (kp.minmax ? kOutMinMax : 0) |
-           (kp.u8 && kp.u8_norm ? kOutNorm : 0) | (kp.s32 ? kOutS32 : 0);
+           (kp.u8 && kp.u8_norm ? kOutNorm : 0) | (kp.s32 ? kOutS32 : 0) | (kp.n16 ? kOutN16 : 0);
 }
 
 // Double magnitude of an exact integer sum of squares S < 2^32: IEEE sqrt
@@ -319,6 +323,7 @@ __global__ void __launch_bounds__(kCtaThreads,
                                       ? SOBEL5_TMA_MIN_CTAS
                                       : kMinCtasPerSm)
     sobel5_packed_default_kernel(const __grid_constant__ KernelParams p) {
+    pdl_enter();
     constexpr bool SEG = GEOM == kGeomSeg || GEOM == kGeomSegTma;
     constexpr bool PAD = GEOM == kGeomPad || GEOM == kGeomPadTma;
     // TMAL: band rows by TMA into shared memory (tma_band_issue); the
@@ -352,6 +357,8 @@ __global__ void __launch_bounds__(kCtaThreads,
     const bool u8_norm = RT ? p.u8_norm != 0 : (OUTS & kOutNorm) != 0;
     const bool w_s = RT ? p.s32 != nullptr : (OUTS & kOutS32) != 0;
     const bool need_g = w_g || w_g32;
+    constexpr bool N16 = !RT && (OUTS & kOutN16) != 0;
+    static_assert(!N16 || !RTAPS, "int16 wire: default taps only");
     // the clamp_abs edge map alone: packed-float epilogue (u8_from_sf2)
     constexpr bool FU8 = !RTAPS && OUTS == kOutU8;
     const int lane = threadIdx.x & 31;
@@ -839,6 +846,29 @@ __global__ void __launch_bounds__(kCtaThreads,
                         bulk_commit();
                     }
                     ++stage_row;
+                } else if constexpr (N16) {
+                    // int16 wire: 4 columns = 8 bytes per plane and lane
+                    auto st16 = [&](int32_t* plane, const int32_t (&v)[4]) {
+                        int16_t* q = reinterpret_cast<int16_t*>(plane) + row_off;
+                        if (full) {
+                            st_wb_v2u(q, __byte_perm(v[0], v[1], 0x5410), __byte_perm(v[2], v[3], 0x5410));
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                if (x0 + j < p.out_w) q[j] = static_cast<int16_t>(v[j]);
+                        }
+                    };
+                    st16(p.gx, gx);
+                    st16(p.gy, gy);
+                    st16(p.gd, gd);
+                    st16(p.gdt, gdt);
+                    if (full) {
+                        st_wb_v4d(p.g + row_off, g[0], g[1], g[2], g[3]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (x0 + j < p.out_w) p.g[row_off + j] = g[j];
+                    }
                 } else if (full && WB) {
                     st_wb_v4(p.gx + row_off, gx[0], gx[1], gx[2], gx[3]);
                     st_wb_v4(p.gy + row_off, gy[0], gy[1], gy[2], gy[3]);

@@ -88,6 +88,7 @@ struct KernelParams {
     int tma_load;  // packed plain kernel: band rows bulk-copied into shared memory
     int frames;    // frames of the launch
     int tstore;    // StreamResult by TMA tensor stores (tmap valid)
+    int n16;       // gx gy gd gdt as int16 at the int32 pointers (host wire, kOutN16)
     // the same taps as floats for the packed-FP32 kernel (sobel5_f32x2.cuh):
     // f, h, k0, k1, gx_v, gy_v, gdm_f, -gdm_d
     float tf[8][5];
@@ -109,6 +110,19 @@ struct DefaultTaps {
     static constexpr int32_t gdm_f[5] = {6, 6, 2, 6, 6};
     static constexpr int32_t gdm_d[5] = {10, 0, -12, 0, 10};
 };
+
+// Programmatic dependent launch (PDL): the launchers set
+// cudaLaunchAttributeProgrammaticStreamSerialization, so the next kernel in
+// the stream may be scheduled once every CTA of this one has started
+// (launch_dependents as the first instruction), and this kernel waits for
+// its predecessor's completion and memory flush before touching global
+// memory (griddepcontrol.wait, before any load or store).  Back-to-back
+// frames thus overlap one launch's CTA scheduling with the previous tail.
+// Without the attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 
 __device__ __forceinline__ uint32_t ld_row_word(const uint8_t* p) {
     return __ldg(reinterpret_cast<const unsigned int*>(p));
@@ -149,6 +163,10 @@ __device__ __forceinline__ void st_wb_v4(int32_t* p, int32_t a, int32_t b, int32
 __device__ __forceinline__ void st_wb_v4d(double* p, double a, double b, double c, double d) {
     asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
                  : "memory");
+}
+// 4 int16 (8 bytes), write-back: the narrow StreamResult wire (kOutN16)
+__device__ __forceinline__ void st_wb_v2u(int16_t* p, uint32_t a, uint32_t b) {
+    asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(b) : "memory");
 }
 __device__ __forceinline__ void st_cs_u32(uint8_t* p, uint32_t v) {
     asm volatile("st.global" SOBEL5_ST_Q ".u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -318,6 +336,7 @@ template <int PF, class TAPS, int MAG, bool PAD>
 #endif
 __global__ void __launch_bounds__(kCtaThreads, SOBEL5_GENERIC_MIN_CTAS)
     sobel5_stream_kernel(const __grid_constant__ KernelParams p) {
+    pdl_enter();
     const TapSource<TAPS> T{p};
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;

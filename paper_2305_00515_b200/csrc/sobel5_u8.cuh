@@ -365,6 +365,7 @@ __device__ __forceinline__ void u8_band_compute(const KernelParams& p, const uin
 template <int NP, bool PAD>
 __global__ void __launch_bounds__(kU8Threads, U8Bounds<NP>::kMinBlocks)
     sobel5_u8_kernel(const __grid_constant__ KernelParams p) {
+    pdl_enter();
     __shared__ __align__(128) uint8_t s_band[U8Band<NP, PAD>::kBytes];
     __shared__ __align__(8) uint64_t s_bar[2];
     const int oy0 = blockIdx.y * p.band;
