@@ -137,16 +137,19 @@ inline PaddedPlane pad_replicate(const GrayPlane& img, int radius) {
 
 namespace detail {
 
-/// image_io.hpp:233-256, computed on the GPU (bit-exact).
+/// image_io.hpp:233-256, computed on the GPU (bit-exact) for the planes the
+/// reference instantiates it with: RealPlane, SignedPlane and GrayPlane.
+/// Like the reference, the output plane is constructed first, so an empty
+/// (0 x 0) plane throws DimMismatch from GrayPlane(0, 0).
 template <typename T>
 GrayPlane quantize(const Plane<T>& plane, SaveMode mode) {
-    static_assert(std::is_same_v<T, double> || std::is_same_v<T, std::int32_t>,
-                  "quantize: RealPlane or SignedPlane");
-    if (plane.empty()) throw EmptyPlane("cannot save an empty plane");
+    static_assert(std::is_same_v<T, double> || std::is_same_v<T, std::int32_t> ||
+                      std::is_same_v<T, std::uint8_t>,
+                  "quantize: RealPlane, SignedPlane or GrayPlane");
     GrayPlane out(plane.width(), plane.height());
     gpu::Context& ctx = gpu::thread_context();
-    const sobel5_status st = sobel5_quantize_host(ctx.get(), plane.data().data(),
-                                                  std::is_same_v<T, double> ? 0 : 1, plane.width(),
+    constexpr int kind = std::is_same_v<T, double> ? 0 : std::is_same_v<T, std::int32_t> ? 1 : 2;
+    const sobel5_status st = sobel5_quantize_host(ctx.get(), plane.data().data(), kind, plane.width(),
                                                   plane.height(), mode == SaveMode::normalize ? 1 : 0,
                                                   out.data().data());
     if (st != SOBEL5_OK) gpu::raise(st, std::string("quantize (") + sobel5_ctx_last_error(ctx.get()) + ")");

@@ -422,8 +422,13 @@ inline void prefault(const std::vector<std::pair<std::uintptr_t, std::uintptr_t>
                         kPopulateWrite) != 0)
                 return;  // unsupported kernel: the first touch faults instead
     };
-    std::thread th[3];
-    for (auto& t : th) t = std::thread(work);
+    // thread creation may fail (std::system_error): run with the threads
+    // that did start, the calling thread always works too
+    std::vector<std::thread> th;
+    try {
+        for (int i = 0; i < 3; ++i) th.emplace_back(work);
+    } catch (...) {
+    }
     work();
     for (auto& t : th) t.join();
 #else
@@ -492,8 +497,16 @@ inline sobel5_status collect_pending(sobel5_ctx* c, int ow, int oh, const std::v
         if (n < (std::size_t{1} << 18)) {
             for (std::size_t k = 0; k < planes.size(); ++k) run_one(k);
         } else {
+            // one thread per plane but the first; planes whose thread could
+            // not be created (std::system_error) run on the calling thread,
+            // and every started thread is joined before the call completes
             std::vector<std::thread> th;
-            for (std::size_t k = 1; k < planes.size(); ++k) th.emplace_back([&, k] { run_one(k); });
+            std::size_t k = 1;
+            try {
+                for (; k < planes.size(); ++k) th.emplace_back([&, k] { run_one(k); });
+            } catch (...) {
+            }
+            for (std::size_t j = k; j < planes.size(); ++j) run_one(j);
             run_one(0);
             for (auto& x : th) x.join();
         }
@@ -596,6 +609,8 @@ inline StreamResult run_stream(const GrayPlane& img, const StreamTaps& taps, con
         throw DimMismatch("strip plan covers " + std::to_string(plan.in_width) + " columns at radius " +
                           std::to_string(plan.radius) + ", image has " + std::to_string(img.width()));
     StreamResult out;
+    // the plan orders the reported ParityViolation pair (strip-major, workers = 1)
+    sobel5_ctx_set_strip_width(gpu::thread_context().get(), plan.lane_width - 2 * plan.radius);
     gpu::run_alloc(img, taps, prefetch, out);
     out.counters = stream_counters(img.height(), plan, taps, prefetch);
     return out;

@@ -78,14 +78,23 @@ typedef struct sobel5_planes {
     int64_t pitch;
 } sobel5_planes;
 
-/* Device-side diagnostics word set by the kernels (nullable).  Zero it
- * before the launch; violations != 0 means some pixel had an odd P+M
- * (recover_diag, pipeline.hpp:268-273) and (sum, diff) is one such pair. */
+/* Diagnostics set by the kernels (nullable; device copies 16-byte aligned).
+ * Zero it before the launch (strip_w may be set); violations != 0 means some
+ * pixel had an odd P+M (recover_diag, pipeline.hpp:268-273) and (sum, diff)
+ * is the pair the reference's run_stream with workers = 1 reports: the
+ * first odd pixel in strip order (strips of strip_w output columns, i.e. the
+ * plan's lane_width - 4; 0 = one strip), then row, then column
+ * (run_strips_parallel, pipeline.hpp:416-445), frames first to last.
+ * order is that pixel's position key (internal; 0 = none); order, sum and
+ * diff are updated together as one 16-byte word.  The host entry points take
+ * strip_w from *diag_out on entry. */
 typedef struct sobel5_diag {
     int32_t violations;
+    int32_t strip_w;
+    int32_t reserved[2];
+    uint64_t order;
     int32_t sum;
     int32_t diff;
-    int32_t reserved;
 } sobel5_diag;
 
 /* Reference-schedule tallies (sobel5::OpCounters, pipeline.hpp:26-51). */
@@ -217,7 +226,8 @@ sobel5_status sobel5_detect(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
                             void* stream);
 
 /* detail::quantize of a device plane (save_plane, image_io.hpp:258-268):
- * kind 0 = RealPlane (double), 1 = SignedPlane (int32); pitch in elements,
+ * kind 0 = RealPlane (double), 1 = SignedPlane (int32), 2 = GrayPlane
+ * (uint8); pitch in elements,
  * u8_pitch in bytes; save_mode as above. */
 sobel5_status sobel5_quantize_plane(const void* d_plane, int kind, int64_t pitch, int width,
                                     int height, int save_mode, uint8_t* d_u8, int64_t u8_pitch,
@@ -279,6 +289,10 @@ void sobel5_ctx_destroy(sobel5_ctx* ctx);
 void sobel5_ctx_trim(sobel5_ctx* ctx);
 /* Message of the last CUDA error seen by this context ("" if none). */
 const char* sobel5_ctx_last_error(const sobel5_ctx* ctx);
+/* Output columns per strip of the caller's StripPlan (lane_width - 4; 0 =
+ * one strip, the default): orders the ParityViolation pair the host calls
+ * report like the reference's run_stream with workers = 1 (sobel5_diag). */
+sobel5_status sobel5_ctx_set_strip_width(sobel5_ctx* ctx, int strip_w);
 
 /* Replaces sobel5::run_stream (pipeline.hpp:452-477: validation :454-460,
  * plane allocation :462-467, strip dispatch :416-445) for host buffers.
@@ -367,7 +381,7 @@ sobel5_status sobel5_detect_host(sobel5_ctx* ctx, const uint8_t* h_in, int width
                                  sobel5_diag* diag_out);
 
 /* Host-buffer detail::quantize (save_plane's export, image_io.hpp:233-268):
- * tightly packed plane (kind 0 double, 1 int32), h_u8 same size. */
+ * tightly packed plane (kind 0 double, 1 int32, 2 uint8), h_u8 same size. */
 sobel5_status sobel5_quantize_host(sobel5_ctx* ctx, const void* h_plane, int kind, int width,
                                    int height, int save_mode, uint8_t* h_u8);
 

@@ -48,8 +48,13 @@ class Planes(C.Structure):
 
 
 class Diag(C.Structure):
-    _fields_ = [("violations", C.c_int32), ("sum", C.c_int32), ("diff", C.c_int32),
-                ("reserved", C.c_int32)]
+    _fields_ = [("violations", C.c_int32), ("strip_w", C.c_int32), ("reserved", C.c_int32 * 2),
+                ("order", C.c_uint64), ("sum", C.c_int32), ("diff", C.c_int32)]
+
+
+# int32 words of a device-side sobel5_diag (a torch.int32 tensor of this many
+# elements; word 0 = violations, 1 = strip_w, 6 = sum, 7 = diff)
+DIAG_WORDS = 8
 
 
 class IpcHandle(C.Structure):
@@ -94,6 +99,7 @@ EXPORTS = (
     "sobel5_run_host_chunk", "sobel5_run_host_staging", "sobel5_run_host_staging_elem",
     "sobel5_kernel_for_taps",
     "sobel3_run_host_begin", "sobel5_ctx_trim", "sobel5_last_launch",
+    "sobel5_ctx_set_strip_width",
     "sobel5_conv2d_valid", "sobel5_conv2d_valid_host", "sobel5_dense_4d", "sobel5_dense_4d_host",
     "sobel5_mgpu_create", "sobel5_mgpu_destroy", "sobel5_mgpu_band", "sobel5_mgpu_upload",
     "sobel5_mgpu_synth", "sobel5_mgpu_run_bands", "sobel5_mgpu_sync", "sobel5_mgpu_run_host", "sobel5_mgpu_last_diag",
@@ -190,6 +196,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.sobel5_run_host_finish.restype = i32
     L.sobel5_ctx_trim.argtypes = [vp]
     L.sobel5_ctx_trim.restype = None
+    L.sobel5_ctx_set_strip_width.argtypes = [vp, i32]
+    L.sobel5_ctx_set_strip_width.restype = i32
     L.sobel3_run_host_begin.argtypes = [vp, vp, i32, i32, i32, C.c_uint32]
     L.sobel3_run_host_begin.restype = i32
     L.sobel5_kernel_for_taps.argtypes = [C.POINTER(Taps)]

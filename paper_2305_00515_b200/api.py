@@ -333,6 +333,10 @@ def run_stream(img: np.ndarray, taps_or_params, plan: StripPlan, prefetch: Prefe
     taps = taps_or_params if isinstance(taps_or_params, Taps) else make_stream_taps(
         taps_or_params)
     ctx = ctx or default_context()
+    # the plan orders the reported ParityViolation pair (strip-major, as the
+    # reference with workers = 1)
+    check(_abi.load().sobel5_ctx_set_strip_width(ctx.handle, plan.lane_width - 2 * plan.radius),
+          "sobel5_ctx_set_strip_width")
     st, res, d = ctx.run_host(img, taps, prefetch)
     if st == _abi.PARITY_VIOLATION:  # pipeline.hpp:269-271
         raise ParityViolation(f"odd sum/difference pair ({d.sum}, {d.diff})")
@@ -574,12 +578,14 @@ def detect_device(d_in, in_pitch: int, width: int, height: int, taps: Taps, pref
 
 def quantize_device(d_plane, pitch: int, width: int, height: int, save_mode: SaveMode, d_u8,
                     u8_pitch: int, scratch=None, stream=None) -> None:
-    """sobel5_quantize_plane on a float64 (RealPlane) or int32 (SignedPlane) tensor."""
+    """sobel5_quantize_plane on a float64 (RealPlane), int32 (SignedPlane) or
+    uint8 (GrayPlane) tensor."""
     import torch
     s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
-    kind = 0 if d_plane.dtype == torch.float64 else 1
-    if kind == 1 and d_plane.dtype != torch.int32:
-        raise DimMismatch("quantize needs a float64 or int32 plane")
+    kinds = {torch.float64: 0, torch.int32: 1, torch.uint8: 2}
+    if d_plane.dtype not in kinds:
+        raise DimMismatch("quantize needs a float64, int32 or uint8 plane")
+    kind = kinds[d_plane.dtype]
     check(_abi.load().sobel5_quantize_plane(d_plane.data_ptr(), kind, pitch, width, height,
                                             int(save_mode), d_u8.data_ptr(), u8_pitch,
                                             None if scratch is None else scratch.data_ptr(), s),
@@ -591,12 +597,13 @@ def quantize(plane: np.ndarray, mode: SaveMode) -> np.ndarray:
     plane = np.ascontiguousarray(plane)
     if plane.size == 0:
         raise EmptyPlane("cannot save an empty plane")
-    if plane.dtype not in (np.float64, np.int32):
-        raise DimMismatch("quantize needs a float64 or int32 plane")
+    kinds = {np.dtype(np.float64): 0, np.dtype(np.int32): 1, np.dtype(np.uint8): 2}
+    if plane.dtype not in kinds:
+        raise DimMismatch("quantize needs a float64, int32 or uint8 plane")
     h, w = plane.shape
     out = np.empty((h, w), np.uint8)
     ctx = default_context()
-    kind = 0 if plane.dtype == np.float64 else 1
+    kind = kinds[plane.dtype]
     check(_abi.load().sobel5_quantize_host(ctx.handle, plane.ctypes.data, kind, w, h, int(mode),
                                            out.ctypes.data), f"quantize ({ctx.last_error()})")
     return out

@@ -293,6 +293,7 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
         return SOBEL5_IMAGE_TOO_SMALL;
     }
     if (!taps || !mid || frames < 1) return SOBEL5_INVALID_ARG;
+    if (diag && !aligned(diag, 16)) return SOBEL5_INVALID_ARG;  // 16-byte CAS word
     if (in_pitch < round_up(width, 4) || in_pitch % 16 != 0) return SOBEL5_INVALID_ARG;
     if (!aligned(mid, 16) || (top && !aligned(top, 16)) || (bot && !aligned(bot, 16)))
         return SOBEL5_INVALID_ARG;

@@ -124,7 +124,8 @@ struct sobel5_ctx {
     void* d_plane[7] = {};
     size_t d_plane_bytes[7] = {};
     sobel5_diag* d_diag = nullptr;
-    sobel5_diag* h_diag = nullptr;  // pinned
+    sobel5_diag* h_diag = nullptr;  // pinned: [0] the call's result, [1] its initial value
+    int strip_w = 0;                // sobel5_ctx_set_strip_width (ParityViolation order)
     void* d_scratch = nullptr;      // detect / normalize scratch
     size_t d_scratch_bytes = 0;
     // pinned staging: the input image and the planes bound for pageable memory
@@ -154,6 +155,15 @@ namespace {
 constexpr size_t kElem[7] = {4, 4, 4, 4, 8, 4, 1};  // gx gy gd gdt g g32 u8
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// Zeroes the device diagnostics for a call, with the context's strip width
+// (the ParityViolation order key) -- an H2D copy of h_diag[1] on s_comp.
+cudaError_t reset_diag(sobel5_ctx* ctx) {
+    ctx->h_diag[1] = sobel5_diag{};
+    ctx->h_diag[1].strip_w = ctx->strip_w;
+    return cudaMemcpyAsync(ctx->d_diag, &ctx->h_diag[1], sizeof(sobel5_diag), cudaMemcpyHostToDevice,
+                           ctx->s_comp);
+}
 
 // bytes per element of plane slot i as it crosses PCIe in the current call
 size_t wire_elem(const sobel5_ctx* ctx, int i) { return ctx->wire && i < 4 ? 2 : kElem[i]; }
@@ -365,7 +375,7 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
     CK(ensure_events(ctx->ev_in, static_cast<size_t>(n_chunks)));
     CK(ensure_events(ctx->ev_comp, static_cast<size_t>(n_chunks)));
     CK(ensure_events(ctx->ev_out, static_cast<size_t>(n_chunks)));
-    CK(cudaMemsetAsync(ctx->d_diag, 0, sizeof(sobel5_diag), ctx->s_comp));
+    CK(reset_diag(ctx));
 
     int uploaded = 0;  // input rows already enqueued
     for (int k = 0; k < n_chunks; ++k) {
@@ -492,7 +502,7 @@ sobel5_status sobel5_ctx_create(sobel5_ctx** out, int device) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->s_comp, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->d_diag, sizeof(sobel5_diag));
-    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_diag, sizeof(sobel5_diag));
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_diag, 2 * sizeof(sobel5_diag));
     if (e != cudaSuccess) {
         sobel5_ctx_destroy(ctx);
         return e == cudaErrorMemoryAllocation ? SOBEL5_OUT_OF_MEMORY : SOBEL5_CUDA_ERROR;
@@ -523,6 +533,12 @@ void sobel5_ctx_destroy(sobel5_ctx* ctx) {
     for (auto s : {ctx->s_h2d, ctx->s_comp, ctx->s_d2h})
         if (s) cudaStreamDestroy(s);
     delete ctx;
+}
+
+sobel5_status sobel5_ctx_set_strip_width(sobel5_ctx* ctx, int strip_w) {
+    if (!ctx || strip_w < 0) return SOBEL5_INVALID_ARG;
+    ctx->strip_w = strip_w;
+    return SOBEL5_OK;
 }
 
 const char* sobel5_ctx_last_error(const sobel5_ctx* ctx) {
@@ -737,7 +753,7 @@ sobel5_status sobel5_detect_host(sobel5_ctx* ctx, const uint8_t* h_in, int width
     }
     CK(ensure(&ctx->d_scratch, &ctx->d_scratch_bytes,
               sobel5_detect_scratch_bytes(out_h, dpitch, 0, 1)));
-    CK(cudaMemsetAsync(ctx->d_diag, 0, sizeof(sobel5_diag), ctx->s_comp));
+    CK(reset_diag(ctx));
     StageBudget budget;
     const uint8_t* src_in = nullptr;
     if (const sobel5_status st =
@@ -805,9 +821,9 @@ sobel5_status sobel5_quantize_host(sobel5_ctx* ctx, const void* h_plane, int kin
                                    int height, int save_mode, uint8_t* h_u8) {
     if (!ctx) return SOBEL5_INVALID_ARG;
     if (width < 1 || height < 1) return SOBEL5_EMPTY_PLANE;  // image_io.hpp:259/265
-    if (!h_plane || !h_u8 || (kind != 0 && kind != 1)) return SOBEL5_INVALID_ARG;
+    if (!h_plane || !h_u8 || kind < 0 || kind > 2) return SOBEL5_INVALID_ARG;
     CK(cudaSetDevice(ctx->device));
-    const size_t es = kind == 0 ? sizeof(double) : sizeof(int32_t);
+    const size_t es = kind == 0 ? sizeof(double) : kind == 1 ? sizeof(int32_t) : 1;
     const size_t n = static_cast<size_t>(width) * height;
     // the plane goes through the g slot (8 B/elem covers both kinds), u8 through u8
     CK(ensure(&ctx->d_plane[4], &ctx->d_plane_bytes[4], n * 8));

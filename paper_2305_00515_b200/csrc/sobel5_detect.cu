@@ -379,7 +379,7 @@ sobel5_status sobel5_quantize_plane(const void* d_plane, int kind, int64_t pitch
                                     void* d_scratch, void* stream) {
     // save_plane (image_io.hpp:258-268): an empty plane throws EmptyPlane
     if (width < 1 || height < 1) return SOBEL5_EMPTY_PLANE;
-    if (!d_plane || !d_u8 || (kind != 0 && kind != 1) || (save_mode != 0 && save_mode != 1) ||
+    if (!d_plane || !d_u8 || kind < 0 || kind > 2 || (save_mode != 0 && save_mode != 1) ||
         pitch < width || u8_pitch < width)
         return SOBEL5_INVALID_ARG;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -395,8 +395,11 @@ sobel5_status sobel5_quantize_plane(const void* d_plane, int kind, int64_t pitch
         if (kind == 0)
             plane_minmax_kernel<<<blocks, 256, 0, s>>>(static_cast<const double*>(d_plane), pitch,
                                                        width, height, mm);
-        else
+        else if (kind == 1)
             plane_minmax_kernel<<<blocks, 256, 0, s>>>(static_cast<const int32_t*>(d_plane), pitch,
+                                                       width, height, mm);
+        else
+            plane_minmax_kernel<<<blocks, 256, 0, s>>>(static_cast<const uint8_t*>(d_plane), pitch,
                                                        width, height, mm);
         norm_table_kernel<<<1, 256, 0, s>>>(mm, tab, 0);
         count_launch(2);
@@ -405,8 +408,11 @@ sobel5_status sobel5_quantize_plane(const void* d_plane, int kind, int64_t pitch
     if (kind == 0)
         plane_map_kernel<<<blocks, 256, 0, s>>>(static_cast<const double*>(d_plane), pitch, width,
                                                 height, save_mode, tab, d_u8, u8_pitch);
-    else
+    else if (kind == 1)
         plane_map_kernel<<<blocks, 256, 0, s>>>(static_cast<const int32_t*>(d_plane), pitch, width,
+                                                height, save_mode, tab, d_u8, u8_pitch);
+    else
+        plane_map_kernel<<<blocks, 256, 0, s>>>(static_cast<const uint8_t*>(d_plane), pitch, width,
                                                 height, save_mode, tab, d_u8, u8_pitch);
     count_launch();
     return map_cuda(cudaGetLastError());

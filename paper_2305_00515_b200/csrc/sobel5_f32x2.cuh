@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kCtaThreads, SOBEL5_F32_MIN_CTAS)
                 const int sl = (s + 1) % 5;
                 int32_t gx[4], gy[4], gd[4], gdt[4];
                 bool odd_any = false;
-                int32_t odd_p = 0, odd_m = 0;
+                int32_t odd_p = 0, odd_m = 0, odd_x = 0;
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {  // pair q holds pixels (q, q + 2)
                     const float2 vx = __ffma2_rn(f2(p.tf[4][4]), F[q], ax[sl][q]);
@@ -204,19 +204,23 @@ __global__ void __launch_bounds__(kCtaThreads, SOBEL5_F32_MIN_CTAS)
                     gdt[q + 2] = d1 >> 1;
                     const bool odd0 = (s0 & 1) != 0 && x0 + q < p.out_w;
                     const bool odd1 = (s1 & 1) != 0 && x0 + q + 2 < p.out_w;
-                    if (!odd_any && (odd0 || odd1)) {  // report (P, M) = ((s+d)/2, (s-d)/2)
-                        const int32_t ss = odd0 ? s0 : s1, dd = odd0 ? d0 : d1;
-                        odd_p = (ss + dd) / 2;
-                        odd_m = (ss - dd) / 2;
+                    // report (P, M) = ((s+d)/2, (s-d)/2) of the leftmost odd
+                    // pixel of the lane (pair q holds columns q and q + 2)
+                    if (odd0 || odd1) {
+                        const int xq = x0 + q + (odd0 ? 0 : 2);
+                        if (!odd_any || xq < odd_x) {
+                            const int32_t ss = odd0 ? s0 : s1, dd = odd0 ? d0 : d1;
+                            odd_p = (ss + dd) / 2;
+                            odd_m = (ss - dd) / 2;
+                            odd_x = xq;
+                        }
                     }
                     odd_any |= odd0 || odd1;
                 }
                 const unsigned odd_mask = __ballot_sync(0xffffffffu, odd_any);
-                if (odd_mask && p.diag && lane == __ffs(odd_mask) - 1) {
-                    if (atomicAdd(&p.diag->violations, 1) == 0) {
-                        p.diag->sum = odd_p;
-                        p.diag->diff = odd_m;
-                    }
+                if (odd_mask && p.diag) {
+                    if (lane == __ffs(odd_mask) - 1) atomicAdd(&p.diag->violations, 1);
+                    if (odd_any) diag_report(p.diag, blockIdx.z, oy0 + r - 4, odd_x, odd_p, odd_m);
                 }
                 const int64_t row_off = out_off;
                 out_off += p.pitch;

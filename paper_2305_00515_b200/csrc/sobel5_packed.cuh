@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(kCtaThreads,
                     // (pipeline.hpp:268-282): gd = (P+M)/2, gdt = (P-M)/2
                     int32_t P[4], M[4];
                     bool odd_any = false;
-                    int32_t odd_p = 0, odd_m = 0;
+                    int32_t odd_p = 0, odd_m = 0, odd_j = 0;
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
                         gx[q] = lane_lo(ax[sl][q]);
@@ -679,21 +679,22 @@ __global__ void __launch_bounds__(kCtaThreads,
                     for (int j = 0; j < 4; ++j) {
                         const int32_t sum = P[j] + M[j];
                         const bool odd = (sum & 1) != 0 && x0 + j < p.out_w;
-                        if (odd && !odd_any) {
+                        if (odd && !odd_any) {  // pixels x0 + j in column order
                             odd_p = P[j];
                             odd_m = M[j];
+                            odd_j = j;
                         }
                         odd_any |= odd;
                         gd[j] = sum >> 1;
                         gdt[j] = (P[j] - M[j]) >> 1;
                     }
-                    // ParityViolation (pipeline.hpp:269-271), recorded once per warp
+                    // ParityViolation (pipeline.hpp:269-271): counted once per
+                    // warp, the reported pair is the reference's first one
                     const unsigned odd_mask = __ballot_sync(0xffffffffu, odd_any);
-                    if (odd_mask && p.diag && lane == __ffs(odd_mask) - 1) {
-                        if (atomicAdd(&p.diag->violations, 1) == 0) {
-                            p.diag->sum = odd_p;
-                            p.diag->diff = odd_m;
-                        }
+                    if (odd_mask && p.diag) {
+                        if (lane == __ffs(odd_mask) - 1) atomicAdd(&p.diag->violations, 1);
+                        if (odd_any)
+                            diag_report(p.diag, blockIdx.z, oy0 + r - 4, x0 + odd_j, odd_p, odd_m);
                     }
                 } else {
 #pragma unroll

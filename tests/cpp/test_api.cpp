@@ -365,6 +365,14 @@ static void gpu_checks_next_rows() {
     ties.data() = {0, 1, 2, 1};
     const GrayPlane tq = detail::quantize(ties, SaveMode::normalize);
     CHECK(tq.data()[1] == 128 && tq.data()[2] == 255);
+    // GrayPlane instantiation (image_io.hpp:233), and the reference's error
+    // for an empty plane: GrayPlane(0, 0) throws DimMismatch first
+    for (SaveMode m : {SaveMode::clamp_abs, SaveMode::normalize})
+        CHECK(detail::quantize(low, m) == quantize_ref(low, m == SaveMode::normalize));
+    CHECK(throws<DimMismatch>([] { detail::quantize(RealPlane(), SaveMode::clamp_abs); }) ==
+          "plane dimensions must be positive, got 0x0");
+    CHECK(throws<DimMismatch>([] { detail::quantize(GrayPlane(), SaveMode::normalize); }) ==
+          "plane dimensions must be positive, got 0x0");
 }
 
 int main(int argc, char** argv) {

@@ -65,7 +65,7 @@ def c5(cuda):
     d_in, pitch = api.alloc_input(w, h)
     api.synth_random_device(d_in, pitch, w, h, seed=1)
     out, op = api.alloc_planes(w - 4, h - 4, PLANES)
-    diag = torch.zeros(4, dtype=torch.int32, device="cuda")
+    diag = torch.zeros(8, dtype=torch.int32, device="cuda")
     api.launch(d_in, pitch, w, h, api.make_stream_taps(), 1, out, op, diag)
     info = api.last_launch()
     # > 300 M output px: 8-row bands of TMA-loaded rows (sobel5_abi.cu)

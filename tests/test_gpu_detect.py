@@ -288,7 +288,7 @@ def test_fault_injected_runtime_packed(api, oracle):
     assert st == 3
     d, pitch = to_dev(api, img)
     out, op = api.alloc_planes(66, 36, SR)
-    diag = torch.zeros(4, dtype=torch.int32, device="cuda")
+    diag = torch.zeros(8, dtype=torch.int32, device="cuda")
     api.launch(d, pitch, 70, 40, taps, 1, out, op, diag)
     torch.cuda.synchronize()
     assert diag[0].item() > 0

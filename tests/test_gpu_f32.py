@@ -51,7 +51,7 @@ def test_f32_valid(api, oracle, h, w, params, prefetch):
         out, op = api.alloc_planes(w - 4, h - 4, SR + ("u8",))
         for v in out.values():
             v.fill_(7)
-        diag = torch.zeros(4, dtype=torch.int32, device="cuda")
+        diag = torch.zeros(8, dtype=torch.int32, device="cuda")
         api.launch(d, pitch, w, h, taps, prefetch, out, op, diag)
         torch.cuda.synchronize()
         st, ref, _ = oracle.run_stream(img, st_t)
@@ -129,14 +129,15 @@ def test_f32_fault_injected_parity_violation(api, oracle):
         assert api.kernel_for(taps) == "f32x2_runtime_taps"
         d, pitch = to_dev(api, img)
         out, op = api.alloc_planes(86, 26, SR)
-        diag = torch.zeros(4, dtype=torch.int32, device="cuda")
+        diag = torch.zeros(8, dtype=torch.int32, device="cuda")
         api.launch(d, pitch, 90, 30, taps, 1, out, op, diag)
         torch.cuda.synchronize()
-        st, ref, _ = oracle.run_stream(img, st_t)
+        st, ref, bad = oracle.run_stream(img, st_t)
         if odd:
             assert st == 3 and diag[0].item() > 0  # oracle status 3: parity violation
-            P, M = diag[1].item(), diag[2].item()
+            P, M = diag[6].item(), diag[7].item()  # sobel5_diag.sum, .diff
             assert (P + M) % 2 != 0
+            assert (P, M) == bad  # the first odd pixel in row-major order (one strip)
         else:
             assert st == 0 and diag[0].item() == 0
             for p in SR:

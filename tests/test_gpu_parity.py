@@ -39,7 +39,7 @@ def run_device(S, img, taps, prefetch, planes=ALL):
     out, op = api.alloc_planes(w - 4, h - 4, planes)
     for v in out.values():
         v.fill_(0x5A if v.dtype == torch.uint8 else 7)  # poison: every pixel must be written
-    diag = torch.zeros(4, dtype=torch.int32, device="cuda")
+    diag = torch.zeros(8, dtype=torch.int32, device="cuda")
     api.launch(d_in, pitch, w, h, taps, prefetch, out, op, diag)
     torch.cuda.synchronize()
     return {k: v[:, : w - 4].cpu().numpy() for k, v in out.items()}, diag.cpu().tolist()
@@ -84,7 +84,8 @@ def test_golden_case_run_stream_api(S, i):
     if c["status"] == 17:
         with pytest.raises(S.ParityViolation) as ei:
             S.run_stream(img, taps, plan, S.Prefetch(c["prefetch"]))
-        assert str(ei.value).startswith("odd sum/difference pair (")
+        # the pair the reference reports (workers = 1: first in strip order)
+        assert str(ei.value) == c["message"]
         return
     r = S.run_stream(img, taps, plan, S.Prefetch(c["prefetch"]))
     for k in PLANES:
@@ -226,7 +227,7 @@ def test_golden_hashes_full_size(S, oracle, key):
     d_in, pitch = api.alloc_input(w, h)
     api.synth_random_device(d_in, pitch, w, h, e["seed"], e["mask"])
     out, op = api.alloc_planes(w - 4, h - 4, PLANES + ("u8",))
-    diag = torch.zeros(4, dtype=torch.int32, device="cuda")
+    diag = torch.zeros(8, dtype=torch.int32, device="cuda")
     api.launch(d_in, pitch, w, h, S.make_stream_taps(), 1, out, op, diag)
     torch.cuda.synchronize()
     assert diag[0].item() == 0
@@ -346,3 +347,29 @@ def test_tma_band_loads_any_band(S, oracle, monkeypatch, band):
             for k in PLANES:
                 got = out[k].view(n, h - 4, op)[f, :, : w - 4].cpu().numpy()
                 np.testing.assert_array_equal(got, ref[k], err_msg=f"band {band} {k} frame {f}")
+
+
+@pytest.mark.parametrize("lanes", [8, 37, 64, 4096])
+@pytest.mark.parametrize("kind", ["packed_runtime_taps", "f32x2_runtime_taps", "generic"])
+def test_parity_violation_pair_matches_reference(reference, lanes, kind):
+    """Fault-injected taps with odd pairs in many strips and rows: the pair
+    every GPU kernel family reports is the one the compiled reference's
+    run_stream raises with workers = 1 (first odd pixel in strip, row,
+    column order; sobel5_diag, pipeline.hpp:416-445 / 268-273)."""
+    from paper_2305_00515_b200 import api
+    rng = np.random.default_rng(lanes)
+    h, w = 97, 301
+    img = rng.integers(0, 256, (h, w), dtype=np.uint8)
+    params = {"packed_runtime_taps": (1, 1, 1, 1), "f32x2_runtime_taps": (2, 3, 5, 7),
+              "generic": (1, 32768, 1, 1)}[kind]
+    code, t, msg = reference.make_stream_taps(*params)
+    assert code == 0, msg
+    t.k1[2] += 1  # odd fault: P + M odd wherever the centre pixel is odd
+    taps = api.Taps.from_dict(t.as_dict())
+    assert api.kernel_for(taps) == kind
+    code, _, _, want = reference.run_stream(img, t, lanes=lanes, prefetch=True, workers=1)
+    assert code == 17 and want.startswith("odd sum/difference pair ("), (code, want)
+    plan = api.plan_strips(w, lanes, 2)
+    with pytest.raises(api.ParityViolation) as ei:
+        api.run_stream(img, taps, plan, api.Prefetch.on)
+    assert str(ei.value) == want
