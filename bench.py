@@ -600,19 +600,12 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
         s_e2e = el / n_e2e
-        # bytes that cross PCIe per plane, as the library stages them (an
-        # untimed begin/finish asks it: gx..gdt ride the int16 wire with the
+        # bytes that crossed PCIe device -> host in the last timed call, as
+        # the library counts its copies (gx..gdt ride the int16 wire with the
         # default taps), and the bytes of the int32/f64 result planes
-        mask = sum(1 << i for i, k in enumerate(("gx", "gy", "gd", "gdt", "g", "g32", "u8"))
-                   if k in h_out)
-        api.check(L.sobel5_run_host_begin(ctx.handle, h_in.data_ptr(), w, h, C.byref(taps),
-                                          a.prefetch, mask), "sobel5_run_host_begin")
-        slot = {"gx": 0, "gy": 1, "gd": 2, "gdt": 3, "g": 4, "g32": 5, "u8": 6}
-        wire_elem = {k: L.sobel5_run_host_staging_elem(ctx.handle, slot[k]) for k in h_out}
-        api.check(L.sobel5_run_host_finish(ctx.handle, None, C.byref(diag)), "finish")
-        d2h = sum(v.numel() * wire_elem[k] for k, v in h_out.items())
+        d2h = int(L.sobel5_ctx_last_d2h_bytes(ctx.handle))
         result = sum(v.numel() * v.element_size() for v in h_out.values())
-        narrow = [k for k, v in h_out.items() if wire_elem[k] < v.element_size()]
+        narrow = ["gx", "gy", "gd", "gdt"] if d2h < result else []
         e2e = {"value": world * w * h / s_e2e / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": world * w * h, "d2h_bytes_per_step": world * d2h,
                "result_bytes_per_step": world * result,

@@ -293,6 +293,9 @@ const char* sobel5_ctx_last_error(const sobel5_ctx* ctx);
  * one strip, the default): orders the ParityViolation pair the host calls
  * report like the reference's run_stream with workers = 1 (sobel5_diag). */
 sobel5_status sobel5_ctx_set_strip_width(sobel5_ctx* ctx, int strip_w);
+/* Bytes of result planes the last sobel5_run_host / _begin / sobel3 host
+ * call moved device -> host (the int16 wire included), for accounting. */
+uint64_t sobel5_ctx_last_d2h_bytes(const sobel5_ctx* ctx);
 
 /* Replaces sobel5::run_stream (pipeline.hpp:452-477: validation :454-460,
  * plane allocation :462-467, strip dispatch :416-445) for host buffers.

@@ -126,6 +126,7 @@ struct sobel5_ctx {
     sobel5_diag* d_diag = nullptr;
     sobel5_diag* h_diag = nullptr;  // pinned: [0] the call's result, [1] its initial value
     int strip_w = 0;                // sobel5_ctx_set_strip_width (ParityViolation order)
+    uint64_t last_d2h = 0;          // bytes the last stream call moved device -> host
     void* d_scratch = nullptr;      // detect / normalize scratch
     size_t d_scratch_bytes = 0;
     // pinned staging: the input image and the planes bound for pageable memory
@@ -377,6 +378,7 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
     CK(ensure_events(ctx->ev_out, static_cast<size_t>(n_chunks)));
     CK(reset_diag(ctx));
 
+    ctx->last_d2h = 0;
     int uploaded = 0;  // input rows already enqueued
     for (int k = 0; k < n_chunks; ++k) {
         const int y0 = k * chunk, y1 = std::min(out_h, y0 + chunk);
@@ -417,6 +419,7 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
         for (int i = 0; i < 7; ++i) {
             if (!hdst[i]) continue;
             const size_t es = wire_elem(ctx, i);
+            ctx->last_d2h += static_cast<uint64_t>(out_w) * es * static_cast<uint64_t>(y1 - y0);
             CK(cudaMemcpy2DAsync(static_cast<char*>(hdst[i]) + static_cast<size_t>(y0) * out_w * es,
                                  static_cast<size_t>(out_w) * es,
                                  static_cast<char*>(ctx->d_plane[i]) +
@@ -534,6 +537,8 @@ void sobel5_ctx_destroy(sobel5_ctx* ctx) {
         if (s) cudaStreamDestroy(s);
     delete ctx;
 }
+
+uint64_t sobel5_ctx_last_d2h_bytes(const sobel5_ctx* ctx) { return ctx ? ctx->last_d2h : 0; }
 
 sobel5_status sobel5_ctx_set_strip_width(sobel5_ctx* ctx, int strip_w) {
     if (!ctx || strip_w < 0) return SOBEL5_INVALID_ARG;
