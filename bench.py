@@ -561,6 +561,63 @@ def main():
                     variants[name]["issue_roofline"] = issue_frac(key, variants[name]["us"])
         torch.cuda.empty_cache()
 
+    # ---- smaller single images (C1 1080p, C2 4K), StreamResult contract ----
+    # throughput: 50 launches in one CUDA graph over 4 rotating inputs (a
+    # frame stream); latency: one launch then a host synchronize, wall clock
+    # (the single-image case, launch overhead included), and the device time
+    # of one launch alone (CUDA events), medians of 30
+    sizes = {}
+    if rank == 0 and frames == 1 and a.workload == "8k" and a.contract == "sr":
+        for (sw, sh) in ((1920, 1080), (3840, 2160)):
+            s_ins = []
+            for i in range(4):
+                d, sp_ = api.alloc_input(sw, sh, dev)
+                api.synth_random_device(d, sp_, sw, sh, seed=77 + i, stream=s_ptr)
+                s_ins.append(d)
+            so, sop = api.alloc_planes(sw - 4, sh - 4, planes_names, dev)
+
+            def one(i, st, sp_=sp_):
+                api.launch(s_ins[i % 4], sp_, sw, sh, taps, a.prefetch, so, sop, stream=st)
+            for i in range(5):
+                one(i, s_ptr)
+            torch.cuda.synchronize()
+            n = 50
+            vs = torch.cuda.Stream(dev)
+            vs.wait_stream(stream)
+            vg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(vg, stream=vs):
+                for i in range(n):
+                    one(i, vs.cuda_stream)
+            vg.replay()
+            torch.cuda.synchronize()
+            v0, v1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            v0.record(stream)
+            vg.replay()
+            v1.record(stream)
+            torch.cuda.synchronize()
+            us_stream = v0.elapsed_time(v1) / n * 1e3
+            del vg
+            wall, dev_us = [], []
+            for i in range(30):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                one(i, s_ptr)
+                torch.cuda.synchronize()
+                wall.append((time.perf_counter() - t0) * 1e6)
+                v0.record(stream)
+                one(i + 1, s_ptr)
+                v1.record(stream)
+                torch.cuda.synchronize()
+                dev_us.append(v0.elapsed_time(v1) * 1e3)
+            sb = sw * sh + (sw - 4) * (sh - 4) * OUT_BYTES[a.contract]
+            sizes[f"{sw}x{sh}"] = {
+                "stream_us_per_image": us_stream, "gpx_s": sw * sh / us_stream / 1e3,
+                "frac": sb / us_stream / 1e3 / hbm_peak,
+                "latency_us_wall": float(np.median(wall)),
+                "latency_us_device": float(np.median(dev_us)), "alg_bytes": sb}
+            del so, s_ins
+        torch.cuda.empty_cache()
+
     # ---- e2e through the C ABI host entry with pinned buffers ----
     # Every rank runs it on its own image at the same time (each GPU has its
     # own PCIe link); the time is the max over ranks and the value the whole
@@ -724,6 +781,7 @@ def main():
             **({"share_gpu": "testing mode: all ranks on cuda:0 over gloo"} if a.share_gpu else {}),
             "clocks": clocks.summary(),
             "variants": variants,
+            "sizes": sizes or None,
             "e2e": e2e,
             "e2e_cpp_api": e2e_cpp,
             "cpu_baseline": cpu,

@@ -51,7 +51,10 @@ def test_two_ranks_e2e(cuda):
     e = d["e2e"]
     assert e["ranks"] == 2 and e["value"] > 0
     assert e["h2d_bytes_per_step"] == 2 * 7680 * 4320
-    assert e["d2h_bytes_per_step"] == 2 * 7676 * 4316 * 24
+    # gx..gdt cross PCIe as int16 (the default-taps wire), the result planes
+    # the caller receives are the full int32/f64 StreamResult
+    assert e["d2h_bytes_per_step"] == 2 * 7676 * 4316 * 16
+    assert e["result_bytes_per_step"] == 2 * 7676 * 4316 * 24
 
 
 def test_two_ranks_default_is_c5_with_e2e(cuda):
