@@ -597,23 +597,38 @@ def main():
             torch.cuda.synchronize()
             us_stream = v0.elapsed_time(v1) / n * 1e3
             del vg
-            wall, dev_us = [], []
+            # single image: (a) the Python API call + synchronize, wall
+            # clock; (b) the same launch as a one-node CUDA graph (what a
+            # latency-bound C/C++ caller replays), replay + synchronize wall
+            # clock and its device time (events around the replay)
+            g1 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g1, stream=vs):
+                one(0, vs.cuda_stream)
+            g1.replay()
+            torch.cuda.synchronize()
+            wall_api, wall_graph, dev_us = [], [], []
             for i in range(30):
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 one(i, s_ptr)
                 torch.cuda.synchronize()
-                wall.append((time.perf_counter() - t0) * 1e6)
+                wall_api.append((time.perf_counter() - t0) * 1e6)
+                t0 = time.perf_counter()
+                g1.replay()
+                torch.cuda.synchronize()
+                wall_graph.append((time.perf_counter() - t0) * 1e6)
                 v0.record(stream)
-                one(i + 1, s_ptr)
+                g1.replay()
                 v1.record(stream)
                 torch.cuda.synchronize()
                 dev_us.append(v0.elapsed_time(v1) * 1e3)
+            del g1
             sb = sw * sh + (sw - 4) * (sh - 4) * OUT_BYTES[a.contract]
             sizes[f"{sw}x{sh}"] = {
                 "stream_us_per_image": us_stream, "gpx_s": sw * sh / us_stream / 1e3,
                 "frac": sb / us_stream / 1e3 / hbm_peak,
-                "latency_us_wall": float(np.median(wall)),
+                "latency_us_wall_api": float(np.median(wall_api)),
+                "latency_us_wall_graph": float(np.median(wall_graph)),
                 "latency_us_device": float(np.median(dev_us)), "alg_bytes": sb}
             del so, s_ins
         torch.cuda.empty_cache()

@@ -111,7 +111,8 @@ _lib = None
 
 
 def lib_path() -> str:
-    return _build.LIB
+    # SOBEL5_LIB: an alternative in-tree build (tools/build_variant.sh, A/B experiments)
+    return os.environ.get("SOBEL5_LIB") or _build.LIB
 
 
 def load(build_if_missing: bool = True) -> C.CDLL:

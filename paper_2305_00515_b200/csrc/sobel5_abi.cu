@@ -423,14 +423,15 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
         !ex.s32 && taps_are_default(*taps) && out->pitch % 8 == 0 && aligned(out->u8, 8) &&
         (frames == 1 || out_frame_stride % 8 == 0) && env_int("SOBEL5_U8_FAST", 1) != 0 &&
         env_int("SOBEL5_GENERIC", 0) == 0 && env_int("SOBEL5_DENSE", 0) == 0) {
-        kp.band = u8_fast_band(out_w, out_h, frames);
+        const U8Plan u8p = u8_fast_plan(out_w, out_h, frames);
+        kp.band = u8p.band;
         const int gy = (out_h + kp.band - 1) / kp.band;
         if (gy <= 65535) {
             kp.tma_load = 1;
             t_last_launch = sobel5_launch_info{kp.band, 1, sobel5_kernel_for_taps(taps),
-                                               (out_w + u8_fast_cta_cols() - 1) / u8_fast_cta_cols(), gy, frames};
+                                               (out_w + u8p.cta_cols - 1) / u8p.cta_cols, gy, frames};
             count_launch();
-            return map_cuda(launch_u8_fast(kp, frames, static_cast<cudaStream_t>(stream)));
+            return map_cuda(launch_u8_fast(kp, frames, u8p, static_cast<cudaStream_t>(stream)));
         }
     }
     t_last_launch = sobel5_launch_info{kp.band, kp.tma_load, sobel5_kernel_for_taps(taps),

@@ -44,11 +44,13 @@ cudaError_t launch_packed_rt_plain(const KernelParams& kp, dim3 grid, int pf, cu
 cudaError_t launch_packed_rt_seg(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
 cudaError_t launch_packed_rt_pad(const KernelParams& kp, dim3 grid, int pf, cudaStream_t s);
 
-// u8-only clamp_abs contract, default taps (sobel5_u8.cuh): 8 px per lane,
-// TMA band rows; its own grid (1024 columns per CTA) and band.
-int u8_fast_band(int out_w, int out_h, int frames);
-int u8_fast_cta_cols();
-cudaError_t launch_u8_fast(const KernelParams& kp, int frames, cudaStream_t s);
+// u8-only clamp_abs contract, default taps (sobel5_u8.cuh): 2NP px per lane,
+// TMA band rows; its own grid (W warps x 32 x 2NP columns per CTA) and band.
+struct U8Plan {
+    int np = 4, warps = 4, band = 16, cta_cols = 1024;
+};
+U8Plan u8_fast_plan(int out_w, int out_h, int frames);
+cudaError_t launch_u8_fast(const KernelParams& kp, int frames, const U8Plan& plan, cudaStream_t s);
 
 // Tensor maps of the StreamResult planes for the TMA-store kernel
 // (sobel5_tmap.cu); false if the driver entry point or the layout is missing.

@@ -36,21 +36,21 @@
 
 namespace sobel5_b200 {
 
-constexpr int kU8Warps = 4;
-constexpr int kU8Threads = 32 * kU8Warps;
 constexpr int kU8MaxBand = 32;  // output rows per CTA (<=)
 
-template <int NP>
+// W warps per CTA side by side (W = 1, 2, 4: the launcher picks by size).
+template <int NP, int W>
 struct U8Geom {
+    static constexpr int kThreads = 32 * W;
     static constexpr int kLaneCols = 2 * NP;
-    static constexpr int kCtaCols = kU8Threads * kLaneCols;  // 512 / 1024
+    static constexpr int kCtaCols = kThreads * kLaneCols;
 };
 
 // Shared-memory band: rows of the CTA's columns [x0c - lead, x0c + cols + 16).
-template <int NP, bool PAD>
+template <int NP, bool PAD, int W>
 struct U8Band {
     static constexpr int kLead = PAD ? 16 : 0;
-    static constexpr int kRowBytes = U8Geom<NP>::kCtaCols + 16 + kLead;
+    static constexpr int kRowBytes = U8Geom<NP, W>::kCtaCols + 16 + kLead;
     static constexpr int kRows = kU8MaxBand + 4;
     static constexpr int kBytes = kRows * kRowBytes;
 };
@@ -89,13 +89,13 @@ __device__ __forceinline__ void u8_round_sqrt2(float2 S, uint32_t& a, uint32_t& 
 }
 
 // One band's rows by TMA: rows 0..4 complete on bar[0], the rest on bar[1].
-template <int NP, bool PAD>
+template <int NP, bool PAD, int W>
 struct U8BandCopy {
-    using T = U8Band<NP, PAD>;
+    using T = U8Band<NP, PAD, W>;
     int src_x, dst_off, n0, b_in;
     uint32_t rb;
     __device__ __forceinline__ U8BandCopy(const KernelParams& p, int tx, int b_in_) {
-        const int cta_x0 = tx * U8Geom<NP>::kCtaCols;
+        const int cta_x0 = tx * U8Geom<NP, W>::kCtaCols;
         src_x = max(cta_x0 - T::kLead, 0);
         dst_off = src_x - (cta_x0 - T::kLead);
         rb = static_cast<uint32_t>(min(T::kRowBytes - dst_off, ((p.width + 15) & ~15) - src_x));
@@ -122,7 +122,7 @@ struct U8BandCopy {
 
 // Block-wide: barrier init, then warp 0 issues one bulk copy per band row.
 // Every thread must call it (__syncthreads inside).
-template <int NP, bool PAD>
+template <int NP, bool PAD, int W>
 __device__ __forceinline__ void u8_band_issue(const KernelParams& p, uint8_t* s_band,
                                               uint64_t* s_bar, int b_in) {
     if (threadIdx.x == 0) {
@@ -132,7 +132,7 @@ __device__ __forceinline__ void u8_band_issue(const KernelParams& p, uint8_t* s_
     }
     __syncthreads();
     if (threadIdx.x < 32) {
-        const U8BandCopy<NP, PAD> bc(p, blockIdx.x, b_in);
+        const U8BandCopy<NP, PAD, W> bc(p, blockIdx.x, b_in);
         if (threadIdx.x == 0) bc.arm(s_bar);
         __syncwarp();
         bc.copy(p, s_band, s_bar, blockIdx.y * p.band, blockIdx.z, threadIdx.x, 32);
@@ -267,6 +267,14 @@ __device__ __forceinline__ void u8_step(const U8Row (&h)[NP], uint32_t (&F)[5][N
         const uint32_t gy = (H[s][j] - H[s0][j] + kB) + 2u * (H[s3][j] - H[s1][j]);
         const float2 fx = u8_pair_float<0x8000u>(gx);
         const float2 fy = u8_pair_float<0x8000u>(gy);
+#if SOBEL5_U8_GD
+        // gd = N - Q (bias 0x6800 per half: n's 0x6800 - q's 0x8000 + kB)
+        // and gdt = -N - Q (bias 0x8000 per half: + 0x16800 (1 + 2^16) mod 2^32)
+        const uint32_t gd = n - q + kB, gdt = 0x68016800u - n - q;
+        const float2 fd = u8_pair_float<0x6800u>(gd);
+        const float2 ft = u8_pair_float<0x8000u>(gdt);
+        const float2 Sq = __ffma2_rn(ft, ft, __ffma2_rn(fd, fd, __ffma2_rn(fy, fy, __fmul2_rn(fx, fx))));
+#else
         const float2 fn = u8_pair_float<0x6800u>(n);
         const float2 fq = u8_pair_float<0x8000u>(q);
         // S = gx^2 + gy^2 + 2 (N^2 + Q^2): every partial sum is an exact
@@ -276,6 +284,7 @@ __device__ __forceinline__ void u8_step(const U8Row (&h)[NP], uint32_t (&F)[5][N
         const float2 a = __ffma2_rn(fy, fy, __fmul2_rn(fx, fx));
         const float2 b = __ffma2_rn(fq, fq, __fmul2_rn(fn, fn));
         const float2 Sq = __ffma2_rn(b, make_float2(2.0f, 2.0f), a);
+#endif
         const int c = j < 2 ? j : j + 2;  // pair j = pixels (c, c + 2)
         u8_round_sqrt2(Sq, u[c], u[c + 2]);
     }
@@ -303,21 +312,21 @@ __device__ __forceinline__ void u8_store(uint8_t* out, const uint32_t (&u)[2 * N
     }
 }
 
-template <int NP>
+template <int NP, int W>
 struct U8Bounds {  // resident CTAs per SM the register budget is set for
-    static constexpr int kMinBlocks = NP == 4 ? 4 : 6;
+    static constexpr int kMinBlocks = (NP == 4 ? 16 : 24) / W;
 };
 
 // One band of one CTA from shared memory: rows 0..4 wait on bar[0], row 5 on
 // bar[1] (phase `par`), outputs rows oy0 .. oy0 + n_out - 1 of column tile tx.
-template <int NP, bool PAD>
+template <int NP, bool PAD, int W>
 __device__ __forceinline__ void u8_band_compute(const KernelParams& p, const uint8_t* s_band,
                                                 uint64_t* s_bar, uint32_t par, int tx, int oy0,
                                                 int frame, int n_out) {
-    using T = U8Band<NP, PAD>;
-    constexpr int kLaneCols = U8Geom<NP>::kLaneCols;
+    using T = U8Band<NP, PAD, W>;
+    constexpr int kLaneCols = U8Geom<NP, W>::kLaneCols;
     const int n_in = n_out + 4;
-    const int x0 = tx * U8Geom<NP>::kCtaCols + threadIdx.x * kLaneCols;
+    const int x0 = tx * U8Geom<NP, W>::kCtaCols + threadIdx.x * kLaneCols;
     if ((x0 & ~(kLaneCols * 32 - 1)) >= p.out_w) return;  // whole warp right of the image
     const bool full = x0 + kLaneCols <= p.out_w;
     const uint8_t* srow = s_band + T::kLead + threadIdx.x * kLaneCols;
@@ -361,17 +370,17 @@ __device__ __forceinline__ void u8_band_compute(const KernelParams& p, const uin
     }
 }
 
-// The kernel: grid = (column tiles of 4 * 32 * 2NP, bands, frames).
-template <int NP, bool PAD>
-__global__ void __launch_bounds__(kU8Threads, U8Bounds<NP>::kMinBlocks)
+// The kernel: grid = (column tiles of W * 32 * 2NP, bands, frames).
+template <int NP, bool PAD, int W>
+__global__ void __launch_bounds__(U8Geom<NP, W>::kThreads, U8Bounds<NP, W>::kMinBlocks)
     sobel5_u8_kernel(const __grid_constant__ KernelParams p) {
     pdl_enter();
-    __shared__ __align__(128) uint8_t s_band[U8Band<NP, PAD>::kBytes];
+    __shared__ __align__(128) uint8_t s_band[U8Band<NP, PAD, W>::kBytes];
     __shared__ __align__(8) uint64_t s_bar[2];
     const int oy0 = blockIdx.y * p.band;
     const int n_out = min(p.band, p.out_h - oy0);
-    u8_band_issue<NP, PAD>(p, s_band, s_bar, n_out + 4);
-    u8_band_compute<NP, PAD>(p, s_band, s_bar, 0u, blockIdx.x, oy0, blockIdx.z, n_out);
+    u8_band_issue<NP, PAD, W>(p, s_band, s_bar, n_out + 4);
+    u8_band_compute<NP, PAD, W>(p, s_band, s_bar, 0u, blockIdx.x, oy0, blockIdx.z, n_out);
 }
 
 }  // namespace sobel5_b200

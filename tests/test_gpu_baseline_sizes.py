@@ -112,7 +112,9 @@ def test_c5_u8_contract_vs_oracle_and_full_plane(c5, oracle):
     out, op = api.alloc_planes(w - 4, h - 4, ("u8",))
     api.launch(c5["d_in"], c5["pitch"], w, h, api.make_stream_taps(), 1, out, op)
     li = api.last_launch()
-    assert li["tma_load"] == 1 and li["band"] == 16  # sobel5_u8_kernel, 16-row bands
+    # sobel5_u8_kernel, 24-row bands above 96 M output pixels, 4-warp CTAs
+    # (1024 columns: 32 column tiles)
+    assert li["tma_load"] == 1 and li["band"] == 24 and li["grid_x"] == 32
     torch.cuda.synchronize()
     u8 = out["u8"]
     for oy0, n in c5_windows(h):
