@@ -20,7 +20,7 @@ SOURCES = ["sobel5_abi.cu", "sobel5_ctx.cu", "sobel5_ipc.cu", "sobel5_detect.cu"
            "sobel5_k_plain.cu", "sobel5_k_seg.cu", "sobel5_k_pad.cu", "sobel5_k_generic.cu",
            "sobel3_k.cu", "sobel5_k_rtaps.cu", "sobel5_k_f32.cu", "sobel5_k_dense.cu",
            "sobel5_conv2d.cu", "sobel5_mgpu.cu", "sobel5_k_u8.cu", "sobel5_tmap.cu",
-           "sobel5_wire.cpp"]
+           "sobel3_k_u8.cu", "sobel5_wire.cpp"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 # host-only translation units (.cpp) go through nvcc to the host compiler
 

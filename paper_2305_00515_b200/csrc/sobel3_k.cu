@@ -105,6 +105,21 @@ sobel5_status sobel3_common(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
         (wide || (out->u8 && !ex.u8_norm) || (ex.minmax && ex.s32)))
         kp.tma_load = 1;
     if (kp.band > 32) kp.tma_load = 0;  // the shared-memory band holds 34 rows
+    // the clamp_abs edge map alone: its own kernel (sobel3_u8.cuh: TMA band
+    // rows, 8 px per lane as packed pairs, float epilogue); SOBEL5_U8_FAST=0
+    // keeps kernel C (ablation)
+    const char* fv = std::getenv("SOBEL5_U8_FAST");
+    if (prefetch && out->u8 && !wide && !ex.minmax && !ex.norm && !ex.u8_norm && !ex.s32 &&
+        out->pitch % 8 == 0 && reinterpret_cast<uintptr_t>(out->u8) % 8 == 0 &&
+        (frames == 1 || out_frame_stride % 8 == 0) && !(fv && *fv && std::atoi(fv) == 0)) {
+        const U8Plan up = u3_fast_plan(out_w, out_h, frames);
+        if ((out_h + up.band - 1) / up.band <= 65535) {
+            kp.band = up.band;
+            kp.tma_load = 1;
+            count_launch();
+            return map_cuda(launch_u3_fast(kp, frames, up, static_cast<cudaStream_t>(stream)));
+        }
+    }
     const dim3 grid(static_cast<unsigned>((out_w + kCtaCols - 1) / kCtaCols), gy,
                     static_cast<unsigned>(frames));
     count_launch();

@@ -51,6 +51,9 @@ struct U8Plan {
 };
 U8Plan u8_fast_plan(int out_w, int out_h, int frames);
 cudaError_t launch_u8_fast(const KernelParams& kp, int frames, const U8Plan& plan, cudaStream_t s);
+// The same for the 3x3 operator's u8-only contract (sobel3_u8.cuh).
+U8Plan u3_fast_plan(int out_w, int out_h, int frames);
+cudaError_t launch_u3_fast(const KernelParams& kp, int frames, const U8Plan& plan, cudaStream_t s);
 
 // Tensor maps of the StreamResult planes for the TMA-store kernel
 // (sobel5_tmap.cu); false if the driver entry point or the layout is missing.

@@ -46,12 +46,13 @@ struct U8Geom {
     static constexpr int kCtaCols = kThreads * kLaneCols;
 };
 
-// Shared-memory band: rows of the CTA's columns [x0c - lead, x0c + cols + 16).
-template <int NP, bool PAD, int W>
+// Shared-memory band: rows of the CTA's columns [x0c - lead, x0c + cols + 16)
+// (R = operator radius: 2 for the 5x5 operator, 1 for the 3x3 one).
+template <int NP, bool PAD, int W, int R = 2>
 struct U8Band {
     static constexpr int kLead = PAD ? 16 : 0;
     static constexpr int kRowBytes = U8Geom<NP, W>::kCtaCols + 16 + kLead;
-    static constexpr int kRows = kU8MaxBand + 4;
+    static constexpr int kRows = kU8MaxBand + 2 * R;
     static constexpr int kBytes = kRows * kRowBytes;
 };
 
@@ -88,10 +89,10 @@ __device__ __forceinline__ void u8_round_sqrt2(float2 S, uint32_t& a, uint32_t& 
     b = __float_as_uint(r.y);
 }
 
-// One band's rows by TMA: rows 0..4 complete on bar[0], the rest on bar[1].
-template <int NP, bool PAD, int W>
+// One band's rows by TMA: rows 0..2R complete on bar[0], the rest on bar[1].
+template <int NP, bool PAD, int W, int R = 2>
 struct U8BandCopy {
-    using T = U8Band<NP, PAD, W>;
+    using T = U8Band<NP, PAD, W, R>;
     int src_x, dst_off, n0, b_in;
     uint32_t rb;
     __device__ __forceinline__ U8BandCopy(const KernelParams& p, int tx, int b_in_) {
@@ -100,7 +101,7 @@ struct U8BandCopy {
         dst_off = src_x - (cta_x0 - T::kLead);
         rb = static_cast<uint32_t>(min(T::kRowBytes - dst_off, ((p.width + 15) & ~15) - src_x));
         b_in = b_in_;
-        n0 = min(5, b_in);
+        n0 = min(2 * R + 1, b_in);
     }
     // one thread: arm both barriers with the bytes they will receive
     __device__ __forceinline__ void arm(uint64_t* bar) const {
@@ -111,7 +112,7 @@ struct U8BandCopy {
     __device__ __forceinline__ void copy(const KernelParams& p, uint8_t* s_band, uint64_t* bar,
                                          int oy0, int frame, int t, int nt) const {
         for (int r = t; r < b_in; r += nt) {
-            const int y = PAD ? min(max(oy0 + r - 2, 0), p.mid_rows - 1) : oy0 + r;
+            const int y = PAD ? min(max(oy0 + r - R, 0), p.mid_rows - 1) : oy0 + r;
             bulk_load(s_band + r * T::kRowBytes + dst_off,
                       p.mid + static_cast<int64_t>(frame) * p.in_frame_stride +
                           static_cast<int64_t>(y) * p.in_pitch + src_x,
@@ -122,7 +123,7 @@ struct U8BandCopy {
 
 // Block-wide: barrier init, then warp 0 issues one bulk copy per band row.
 // Every thread must call it (__syncthreads inside).
-template <int NP, bool PAD, int W>
+template <int NP, bool PAD, int W, int R = 2>
 __device__ __forceinline__ void u8_band_issue(const KernelParams& p, uint8_t* s_band,
                                               uint64_t* s_bar, int b_in) {
     if (threadIdx.x == 0) {
@@ -132,7 +133,7 @@ __device__ __forceinline__ void u8_band_issue(const KernelParams& p, uint8_t* s_
     }
     __syncthreads();
     if (threadIdx.x < 32) {
-        const U8BandCopy<NP, PAD, W> bc(p, blockIdx.x, b_in);
+        const U8BandCopy<NP, PAD, W, R> bc(p, blockIdx.x, b_in);
         if (threadIdx.x == 0) bc.arm(s_bar);
         __syncwarp();
         bc.copy(p, s_band, s_bar, blockIdx.y * p.band, blockIdx.z, threadIdx.x, 32);
@@ -168,10 +169,11 @@ __device__ __forceinline__ void u8_fix_right(uint32_t (&w)[NW], int nv) {
 // pass of its NP pairs.  Valid mode: window = columns x0 .. x0 + 2NP + 3.
 // PAD: it starts 2 columns left of x0, built from the words left and right
 // of the lane's own bytes; columns outside the image take the edge pixel.
-template <int NP, bool PAD>
-__device__ __forceinline__ void u8_row(const uint8_t* srow, int x0, int width, U8Row (&o)[NP]) {
+// The lane's NW window words of one row: columns x0 - R*PAD ... (radius R).
+template <int NP, bool PAD, int R = 2>
+__device__ __forceinline__ void u8_window(const uint8_t* srow, int x0, int width,
+                                          uint32_t (&w)[NP / 2 + 1]) {
     constexpr int NW = NP / 2 + 1;  // window words
-    uint32_t w[NW];
     if constexpr (!PAD) {
         if constexpr (NP == 4) {
             const uint2 a = *reinterpret_cast<const uint2*>(srow);
@@ -193,11 +195,20 @@ __device__ __forceinline__ void u8_row(const uint8_t* srow, int x0, int width, U
         }
         r[NW] = *reinterpret_cast<const uint32_t*>(srow + 4 * (NW - 1));
         if (x0 == 0) r[0] = __byte_perm(r[1], 0u, 0x0000);  // left of column 0
+        // window starts R bytes left of x0: bytes 4-R .. 7-R of (r[k], r[k+1])
+        constexpr uint32_t kSel = R == 2 ? 0x5432u : 0x6543u;
 #pragma unroll
-        for (int k = 0; k < NW; ++k) w[k] = __byte_perm(r[k], r[k + 1], 0x5432);
-        const int nv = width - (x0 - 2);  // window bytes inside the image
+        for (int k = 0; k < NW; ++k) w[k] = __byte_perm(r[k], r[k + 1], kSel);
+        const int nv = width - (x0 - R);  // window bytes inside the image
         if (nv < 4 * NW) u8_fix_right<NW>(w, nv);
     }
+}
+
+template <int NP, bool PAD>
+__device__ __forceinline__ void u8_row(const uint8_t* srow, int x0, int width, U8Row (&o)[NP]) {
+    constexpr int NW = NP / 2 + 1;  // window words
+    uint32_t w[NW];
+    u8_window<NP, PAD, 2>(srow, x0, width, w);
     // E_k = byte k | byte k+2 << 16, k = 0 .. 2NP + 1
     uint32_t e[2 * NP + 2];
 #pragma unroll

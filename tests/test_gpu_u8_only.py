@@ -135,3 +135,43 @@ def test_sobel3_u8_only(api, oracle, h, w, pad):
         np.testing.assert_array_equal(out["u8"][:, :ow].cpu().numpy(),
                                       oracle.quantize(ref["g"], "clamp_abs"),
                                       err_msg=f"mask {mask:#x}")
+
+
+@pytest.mark.parametrize("warps", ["1", "2", "4"])
+@pytest.mark.parametrize("band", ["4", "13", "32"])
+@pytest.mark.parametrize("op", [5, 3])
+@pytest.mark.parametrize("pad", [False, True])
+def test_u8_kernels_every_cta_width_and_band(api, oracle, monkeypatch, warps, band, op, pad):
+    """The u8-only kernels (sobel5_u8.cuh, sobel3_u8.cuh) at every CTA width
+    (1, 2, 4 warps: 256 / 512 / 1024 columns) and band height the size rules
+    can pick or a caller can force, valid and padded, on a ragged image that
+    spans several column tiles and a partial last band."""
+    import torch
+    monkeypatch.setenv("SOBEL5_U8_WARPS", warps)
+    monkeypatch.setenv("SOBEL5_BAND", band)
+    h, w = 157, 2333
+    for k, mask in enumerate((0xFF, 0x07)):
+        img = img_of(h, w, 7 * k + op, mask)
+        r = (op - 1) // 2
+        ow, oh = (w, h) if pad else (w - 2 * r, h - 2 * r)
+        d, pitch = to_dev(api, img)
+        out, op_ = api.alloc_planes(ow, oh, ("u8",))
+        out["u8"].fill_(0x5A)
+        if op == 5:
+            api.launch_ex(d, pitch, w, h, api.make_stream_taps(), 1, pad, out, op_)
+        else:
+            api.launch3(d, pitch, w, h, 1, pad, out, op_)
+        torch.cuda.synchronize()
+        src = img
+        if pad:
+            st, src = oracle.pad_replicate(img, r)
+            assert st == 0
+        if op == 5:
+            st, ref, _ = oracle.run_stream(src)
+            want = oracle.clamp_abs(ref["g"])
+        else:
+            st, ref = oracle.sobel3_2d(src)
+            want = oracle.quantize(ref["g"], "clamp_abs")
+        assert st == 0
+        np.testing.assert_array_equal(out["u8"][:, :ow].cpu().numpy(), want,
+                                      err_msg=f"op {op} mask {mask:#x}")
