@@ -58,6 +58,8 @@ template <int PF, int GEOM, int MAG, int OUTS>
 __global__ void __launch_bounds__(kCtaThreads, SOBEL5_F32_MIN_CTAS)
     sobel5_f32x2_kernel(const __grid_constant__ KernelParams p) {
     pdl_enter();
+    __shared__ OddSlot s_odd[kCtaThreads];  // ParityViolation
+    if (p.diag) odd_init(s_odd);
     constexpr bool SEG = GEOM == kGeomSeg;
     constexpr bool PAD = GEOM == kGeomPad;
     constexpr bool RT = OUTS == kOutRuntime;
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(kCtaThreads, SOBEL5_F32_MIN_CTAS)
                 const unsigned odd_mask = __ballot_sync(0xffffffffu, odd_any);
                 if (odd_mask && p.diag) {
                     if (lane == __ffs(odd_mask) - 1) atomicAdd(&p.diag->violations, 1);
-                    if (odd_any) diag_report(p.diag, blockIdx.z, oy0 + r - 4, odd_x, odd_p, odd_m);
+                    if (odd_any) odd_note(s_odd, p.diag, blockIdx.z, oy0 + r - 4, odd_x, odd_p, odd_m);
                 }
                 const int64_t row_off = out_off;
                 out_off += p.pitch;
@@ -323,6 +325,7 @@ __global__ void __launch_bounds__(kCtaThreads, SOBEL5_F32_MIN_CTAS)
             atomicMax(reinterpret_cast<unsigned long long*>(&mm->hi_key), g_max);
         }
     }
+    if (p.diag) odd_flush(s_odd, p.diag);
 }
 
 }  // namespace sobel5_b200

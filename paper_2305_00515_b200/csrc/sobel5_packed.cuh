@@ -324,6 +324,10 @@ __global__ void __launch_bounds__(kCtaThreads,
                                       : kMinCtasPerSm)
     sobel5_packed_default_kernel(const __grid_constant__ KernelParams p) {
     pdl_enter();
+    __shared__ OddSlot s_odd[RTAPS ? kCtaThreads : 1];  // ParityViolation (runtime taps)
+    if constexpr (RTAPS) {
+        if (p.diag) odd_init(s_odd);
+    }
     constexpr bool SEG = GEOM == kGeomSeg || GEOM == kGeomSegTma;
     constexpr bool PAD = GEOM == kGeomPad || GEOM == kGeomPadTma;
     // TMAL: band rows by TMA into shared memory (tma_band_issue); the
@@ -694,7 +698,7 @@ __global__ void __launch_bounds__(kCtaThreads,
                     if (odd_mask && p.diag) {
                         if (lane == __ffs(odd_mask) - 1) atomicAdd(&p.diag->violations, 1);
                         if (odd_any)
-                            diag_report(p.diag, blockIdx.z, oy0 + r - 4, x0 + odd_j, odd_p, odd_m);
+                            odd_note(s_odd, p.diag, blockIdx.z, oy0 + r - 4, x0 + odd_j, odd_p, odd_m);
                     }
                 } else {
 #pragma unroll
@@ -928,6 +932,9 @@ __global__ void __launch_bounds__(kCtaThreads,
             atomicMax(reinterpret_cast<unsigned long long*>(&mm->hi_key),
                       dkey(sqrt_u30(s_max)));
         }
+    }
+    if constexpr (RTAPS) {
+        if (p.diag) odd_flush(s_odd, p.diag);
     }
 }
 

@@ -124,17 +124,25 @@ __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
-// ParityViolation bookkeeping (recover_diag, pipeline.hpp:268-273) for the
-// odd pixel (frame, y, x) of this lane with pair (P, M): the pair kept is the
-// one the reference reports with workers = 1 -- strips of d->strip_w output
-// columns left to right, then rows top to bottom, then columns
-// (run_strips_parallel :416-445 walks the strips in order, run_strip the
-// rows, recover_diag the columns).  The position key (frame 10 bits, strip
-// 16, row 22, column in strip 16, each saturated) is stored inverted so a
-// zeroed word means "none", and {~key, sum, diff} changes as one 16-byte CAS.
-// Rare path: only fault-injected taps produce odd pairs.
-static __device__ __noinline__ void diag_report(sobel5_diag* d, int frame, int y, int x, int32_t P,
-                                         int32_t M) {
+// ParityViolation bookkeeping (recover_diag, pipeline.hpp:268-273).  The
+// pair kept is the one the reference reports with workers = 1 -- strips of
+// d->strip_w output columns left to right, then rows top to bottom, then
+// columns (run_strips_parallel :416-445 walks the strips in order, run_strip
+// the rows, recover_diag the columns).  Position key: frame 10 bits, strip
+// 16, row 22, column in strip 16, each saturated.
+//
+// Kept off the row loop's registers: a thread notes its first odd pixel in
+// its own shared-memory slot (rare path, no extra live registers in the
+// hot loop) and publishes it once at the end of the kernel, where the
+// device word {~key, sum, diff} changes by one 16-byte CAS (stored inverted
+// so a zeroed word means "none").  Only fault-injected taps produce odd pairs.
+struct OddSlot {
+    unsigned long long key;  // ~0 = none
+    int32_t p, m;
+};
+__device__ __forceinline__ void odd_init(OddSlot* s) { s[threadIdx.x] = OddSlot{~0ull, 0, 0}; }
+__device__ __forceinline__ void odd_note(OddSlot* s, const sobel5_diag* d, int frame, int y, int x,
+                                         int32_t P, int32_t M) {
     const int sw = *reinterpret_cast<volatile const int32_t*>(&d->strip_w);
     const uint64_t strip = sw > 0 ? static_cast<uint64_t>(x / sw) : 0u;
     const uint64_t col = sw > 0 ? static_cast<uint64_t>(x % sw) : static_cast<uint64_t>(x);
@@ -142,6 +150,10 @@ static __device__ __noinline__ void diag_report(sobel5_diag* d, int frame, int y
     const uint64_t key = (sat(static_cast<uint64_t>(frame), 1023) << 54) | (sat(strip, 65535) << 38) |
                          (sat(static_cast<uint64_t>(y), (uint64_t{1} << 22) - 1) << 16) |
                          sat(col, 65535);
+    OddSlot& o = s[threadIdx.x];
+    if (key < o.key) o = OddSlot{key, P, M};
+}
+static __device__ __noinline__ void diag_publish(sobel5_diag* d, uint64_t key, int32_t P, int32_t M) {
     const uint64_t inv = ~key;
     unsigned __int128* w = reinterpret_cast<unsigned __int128*>(&d->order);
     const unsigned __int128 nv = static_cast<unsigned __int128>(inv) |
@@ -154,6 +166,11 @@ static __device__ __noinline__ void diag_report(sobel5_diag* d, int frame, int y
         if (seen == old) return;
         old = seen;
     }
+}
+// end of the kernel (nothing else live): publish this thread's slot
+__device__ __forceinline__ void odd_flush(const OddSlot* s, sobel5_diag* d) {
+    const OddSlot o = s[threadIdx.x];
+    if (o.key != ~0ull) diag_publish(d, o.key, o.p, o.m);
 }
 
 __device__ __forceinline__ uint32_t ld_row_word(const uint8_t* p) {
@@ -369,6 +386,8 @@ template <int PF, class TAPS, int MAG, bool PAD>
 __global__ void __launch_bounds__(kCtaThreads, SOBEL5_GENERIC_MIN_CTAS)
     sobel5_stream_kernel(const __grid_constant__ KernelParams p) {
     pdl_enter();
+    __shared__ OddSlot s_odd[kCtaThreads];  // ParityViolation
+    if (p.diag) odd_init(s_odd);
     const TapSource<TAPS> T{p};
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -517,7 +536,7 @@ __global__ void __launch_bounds__(kCtaThreads, SOBEL5_GENERIC_MIN_CTAS)
                 const unsigned odd_mask = __ballot_sync(0xffffffffu, odd_any);
                 if (odd_mask && p.diag) {
                     if (lane == __ffs(odd_mask) - 1) atomicAdd(&p.diag->violations, 1);
-                    if (odd_any) diag_report(p.diag, blockIdx.z, oy0 + v, x0 + odd_j, odd_p, odd_m);
+                    if (odd_any) odd_note(s_odd, p.diag, blockIdx.z, oy0 + v, x0 + odd_j, odd_p, odd_m);
                 }
 
                 const int64_t row_off = out_frame + static_cast<int64_t>(oy0 + v) * p.pitch + x0;
@@ -604,6 +623,7 @@ __global__ void __launch_bounds__(kCtaThreads, SOBEL5_GENERIC_MIN_CTAS)
             atomicMax(reinterpret_cast<unsigned long long*>(&mm->hi_key), g_max);
         }
     }
+    if (p.diag) odd_flush(s_odd, p.diag);
 }
 
 }  // namespace sobel5_b200
