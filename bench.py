@@ -623,10 +623,36 @@ def main():
                 torch.cuda.synchronize()
                 dev_us.append(v0.elapsed_time(v1) * 1e3)
             del g1
+            # the same frames as ONE batched launch (sobel5_launch_batch, the
+            # C4 path): 16 frames per launch, 4 launches in a graph
+            nb = 16
+            bi, bp = api.alloc_input(sw, sh, dev, frames=nb)
+            for f_ in range(nb):
+                api.synth_random_device(bi[f_], bp, sw, sh, seed=500 + f_, stream=s_ptr)
+            bo, bop = api.alloc_planes(sw - 4, sh - 4, planes_names, dev, frames=nb)
+
+            def batch(st, bi=bi, bp=bp, bo=bo, bop=bop):
+                api.launch_batch(bi, bp, sh * bp, sw, sh, nb, taps, a.prefetch, bo, bop,
+                                 (sh - 4) * bop, stream=st)
+            batch(s_ptr)
+            torch.cuda.synchronize()
+            gb = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gb, stream=vs):
+                for i in range(4):
+                    batch(vs.cuda_stream)
+            gb.replay()
+            torch.cuda.synchronize()
+            v0.record(stream)
+            gb.replay()
+            v1.record(stream)
+            torch.cuda.synchronize()
+            us_batch = v0.elapsed_time(v1) / (4 * nb) * 1e3
+            del gb, bi, bo
             sb = sw * sh + (sw - 4) * (sh - 4) * OUT_BYTES[a.contract]
             sizes[f"{sw}x{sh}"] = {
                 "stream_us_per_image": us_stream, "gpx_s": sw * sh / us_stream / 1e3,
                 "frac": sb / us_stream / 1e3 / hbm_peak,
+                "batch16_us_per_image": us_batch, "batch16_frac": sb / us_batch / 1e3 / hbm_peak,
                 "latency_us_wall_api": float(np.median(wall_api)),
                 "latency_us_wall_graph": float(np.median(wall_graph)),
                 "latency_us_device": float(np.median(dev_us)), "alg_bytes": sb}
