@@ -94,3 +94,46 @@ def test_metrics_harness_matches_reference(tmp_path):
                         "-o", str(ref)], check=True)
         assert got == subprocess.run([str(ref)], capture_output=True, text=True,
                                      check=True).stdout
+
+
+EC_SRC = os.path.join(ROOT, "tests", "cpp", "errors_check.cpp")
+EC_GOLD = os.path.join(ROOT, "tests", "golden", "errors_check.txt")
+
+
+@pytest.fixture(scope="module")
+def ec_exe(tmp_path_factory):
+    from paper_2305_00515_b200 import _abi
+    _abi.load()
+    lib = os.path.join(ROOT, "paper_2305_00515_b200", "lib")
+    out = str(tmp_path_factory.mktemp("ec") / "errors_check")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-Werror",
+                    "-I" + os.path.join(ROOT, "include"), EC_SRC, "-L" + lib, "-lsobel5_b200",
+                    "-Wl,-rpath," + lib, "-o", out], check=True)
+    return out
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INC), reason="reference headers absent")
+def test_errors_golden_is_the_reference_output(tmp_path):
+    """tests/golden/errors_check.txt is exactly what the reference build of
+    tests/cpp/errors_check.cpp prints (regenerated live here)."""
+    ref = tmp_path / "ec_ref"
+    subprocess.run(["g++", "-std=c++20", "-O2", "-include", "algorithm", f"-I{REF_INC}",
+                    "-I" + os.path.join(ROOT, "oracle", "png_stub"), EC_SRC, "-o", str(ref)],
+                   check=True)
+    got = subprocess.run([str(ref)], capture_output=True, text=True, check=True).stdout
+    with open(EC_GOLD) as f:
+        assert got == f.read()
+
+
+@pytest.mark.gpu
+def test_errors_same_as_reference_on_gpu(ec_exe, cuda):
+    """The unmodified caller program built against the drop-in prints the
+    reference's exceptions and messages line for line: the ParityViolation
+    pair of fault-injected taps for every runtime-taps kernel family and
+    strip widths 1..4092 (workers = 1), run_stream's validation order, the
+    host-side parameter / plan / padding / quantize errors, and the
+    results of even faults."""
+    got = subprocess.run([ec_exe], capture_output=True, text=True, timeout=300).stdout
+    with open(EC_GOLD) as f:
+        want = f.read()
+    assert got.splitlines() == want.splitlines()
