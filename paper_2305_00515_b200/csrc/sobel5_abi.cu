@@ -419,10 +419,16 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     // replicate-padded): the issue-bound contract has its own kernel
     // (sobel5_u8.cuh: packed pairs, ring vertical pass, TMA band rows).  SOBEL5_U8_FAST=0 keeps
     // the general packed kernel (ablation).
-    if (prefetch && !top && !bot && out->u8 && !wide && !ex.minmax && !ex.norm && !ex.u8_norm &&
-        !ex.s32 && taps_are_default(*taps) && out->pitch % 8 == 0 && aligned(out->u8, 8) &&
-        (frames == 1 || out_frame_stride % 8 == 0) && env_int("SOBEL5_U8_FAST", 1) != 0 &&
-        env_int("SOBEL5_GENERIC", 0) == 0 && env_int("SOBEL5_DENSE", 0) == 0) {
+    // The normalize export's pass 1 (the exact S plane + the frame's min / max,
+    // nothing else) runs on the same kernel in its S mode.
+    const bool u8_only = out->u8 && !ex.minmax && !ex.norm && !ex.u8_norm && !ex.s32 &&
+                         aligned(out->u8, 8);
+    const bool s_pass = !out->u8 && ex.minmax && ex.s32 && !ex.norm && !ex.u8_norm &&
+                        aligned(ex.s32, 32);
+    if (prefetch && !top && !bot && !wide && (u8_only || s_pass) && taps_are_default(*taps) &&
+        out->pitch % 8 == 0 && (frames == 1 || out_frame_stride % 8 == 0) &&
+        env_int("SOBEL5_U8_FAST", 1) != 0 && env_int("SOBEL5_GENERIC", 0) == 0 &&
+        env_int("SOBEL5_DENSE", 0) == 0) {
         const U8Plan u8p = u8_fast_plan(out_w, out_h, frames);
         kp.band = u8p.band;
         const int gy = (out_h + kp.band - 1) / kp.band;

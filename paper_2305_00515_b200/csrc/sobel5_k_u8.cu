@@ -20,6 +20,11 @@ cudaError_t go(const KernelParams& kp, int frames, cudaStream_t s) {
     const dim3 grid(static_cast<unsigned>((kp.out_w + G::kCtaCols - 1) / G::kCtaCols),
                     static_cast<unsigned>((kp.out_h + kp.band - 1) / kp.band),
                     static_cast<unsigned>(frames));
+    if (kp.s32) {  // normalize pass 1: exact S plane + min / max (MODE 1)
+        if (kp.pad)
+            return launch_kp(sobel5_u8_kernel<NP, true, W, 1>, grid, G::kThreads, 0, s, kp);
+        return launch_kp(sobel5_u8_kernel<NP, false, W, 1>, grid, G::kThreads, 0, s, kp);
+    }
     if (kp.pad)
         return launch_kp(sobel5_u8_kernel<NP, true, W>, grid, G::kThreads, 0, s, kp);
     return launch_kp(sobel5_u8_kernel<NP, false, W>, grid, G::kThreads, 0, s, kp);

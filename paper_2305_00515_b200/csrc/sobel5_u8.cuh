@@ -253,7 +253,20 @@ __device__ __forceinline__ void u8_prime(const U8Row (&h)[NP], uint32_t (&F)[5][
 
 // One input row i >= 4 (ring slot S = i mod 5, static): the Q accumulators
 // and output row i - 4 as 2NP u8 pixels (byte 0 of each u[k]).
-template <int S, int NP>
+// Exact S of a packed pair whose halves carry the bias 0x8000: XOR turns the
+// halves into two's complement, then sign extension / arithmetic shift.
+__device__ __forceinline__ void pair_ints(uint32_t vb, int32_t& lo, int32_t& hi) {
+    const uint32_t v = vb ^ 0x80008000u;
+    lo = static_cast<int32_t>(static_cast<int16_t>(v & 0xffffu));
+    hi = static_cast<int32_t>(v) >> 16;
+}
+
+// One input row i >= 4 (ring slot S = i mod 5, static): the Q accumulators
+// and output row i - 4.  MODE 0: 2NP clamp_abs u8 pixels (byte 0 of each
+// u[k]); MODE 1: the exact integer S = gx^2 + gy^2 + gd^2 + gdt^2 of each
+// pixel in u[k] (normalize pass 1, image_io.hpp:242-255: the S plane and the
+// frame's min / max).
+template <int S, int NP, int MODE = 0>
 __device__ __forceinline__ void u8_step(const U8Row (&h)[NP], uint32_t (&F)[5][NP],
                                         uint32_t (&D)[5][NP], uint32_t (&H)[5][NP],
                                         uint32_t (&aq)[5][NP], uint32_t (&u)[2 * NP]) {
@@ -276,28 +289,32 @@ __device__ __forceinline__ void u8_step(const U8Row (&h)[NP], uint32_t (&F)[5][N
         const uint32_t n = 3u * (t + w) + F[s2][j] - 5u * (D[s0][j] + D[s][j]) +
                            6u * D[s2][j];                   // bias 0x68006800
         const uint32_t gy = (H[s][j] - H[s0][j] + kB) + 2u * (H[s3][j] - H[s1][j]);
-        const float2 fx = u8_pair_float<0x8000u>(gx);
-        const float2 fy = u8_pair_float<0x8000u>(gy);
-#if SOBEL5_U8_GD
-        // gd = N - Q (bias 0x6800 per half: n's 0x6800 - q's 0x8000 + kB)
-        // and gdt = -N - Q (bias 0x8000 per half: + 0x16800 (1 + 2^16) mod 2^32)
-        const uint32_t gd = n - q + kB, gdt = 0x68016800u - n - q;
-        const float2 fd = u8_pair_float<0x6800u>(gd);
-        const float2 ft = u8_pair_float<0x8000u>(gdt);
-        const float2 Sq = __ffma2_rn(ft, ft, __ffma2_rn(fd, fd, __ffma2_rn(fy, fy, __fmul2_rn(fx, fx))));
-#else
-        const float2 fn = u8_pair_float<0x6800u>(n);
-        const float2 fq = u8_pair_float<0x8000u>(q);
-        // S = gx^2 + gy^2 + 2 (N^2 + Q^2): every partial sum is an exact
-        // integer while the true sum is <= 65280; above it the rounded
-        // partial sums are monotone, so the result is >= 65281 -- all
-        // clamp_abs needs (saturation at 255)
-        const float2 a = __ffma2_rn(fy, fy, __fmul2_rn(fx, fx));
-        const float2 b = __ffma2_rn(fq, fq, __fmul2_rn(fn, fn));
-        const float2 Sq = __ffma2_rn(b, make_float2(2.0f, 2.0f), a);
-#endif
         const int c = j < 2 ? j : j + 2;  // pair j = pixels (c, c + 2)
-        u8_round_sqrt2(Sq, u[c], u[c + 2]);
+        if constexpr (MODE == 1) {
+            // gd = N - Q and gdt = -N - Q with the bias 0x8000 per half:
+            // n - q carries 0x6800 - 0x8000 per half, -n - q carries -0xE800
+            const uint32_t gd = n - q + 0x98009800u, gdt = 0x68016800u - n - q;
+            int32_t a0, a1, b0, b1, c0, c1, d0, d1;
+            pair_ints(gx, a0, a1);
+            pair_ints(gy, b0, b1);
+            pair_ints(gd, c0, c1);
+            pair_ints(gdt, d0, d1);
+            u[c] = static_cast<uint32_t>(a0 * a0 + b0 * b0 + c0 * c0 + d0 * d0);
+            u[c + 2] = static_cast<uint32_t>(a1 * a1 + b1 * b1 + c1 * c1 + d1 * d1);
+        } else {
+            const float2 fx = u8_pair_float<0x8000u>(gx);
+            const float2 fy = u8_pair_float<0x8000u>(gy);
+            const float2 fn = u8_pair_float<0x6800u>(n);
+            const float2 fq = u8_pair_float<0x8000u>(q);
+            // S = gx^2 + gy^2 + 2 (N^2 + Q^2): every partial sum is an exact
+            // integer while the true sum is <= 65280; above it the rounded
+            // partial sums are monotone, so the result is >= 65281 -- all
+            // clamp_abs needs (saturation at 255)
+            const float2 a = __ffma2_rn(fy, fy, __fmul2_rn(fx, fx));
+            const float2 b = __ffma2_rn(fq, fq, __fmul2_rn(fn, fn));
+            const float2 Sq = __ffma2_rn(b, make_float2(2.0f, 2.0f), a);
+            u8_round_sqrt2(Sq, u[c], u[c + 2]);
+        }
     }
 }
 
@@ -328,9 +345,26 @@ struct U8Bounds {  // resident CTAs per SM the register budget is set for
     static constexpr int kMinBlocks = (NP == 4 ? 16 : 24) / W;
 };
 
+// 2NP exact S values (u[k] = pixel x0 + k) to the S plane row (MODE 1).
+template <int NP>
+__device__ __forceinline__ void s32_store(uint32_t* out, const uint32_t (&u)[2 * NP], bool full,
+                                          int x0, int out_w) {
+    if (full) {
+#pragma unroll
+        for (int i = 0; i < 2 * NP; i += 4)
+            *reinterpret_cast<uint4*>(out + i) = make_uint4(u[i], u[i + 1], u[i + 2], u[i + 3]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 2 * NP; ++i)
+            if (x0 + i < out_w) out[i] = u[i];
+    }
+}
+
 // One band of one CTA from shared memory: rows 0..4 wait on bar[0], row 5 on
 // bar[1] (phase `par`), outputs rows oy0 .. oy0 + n_out - 1 of column tile tx.
-template <int NP, bool PAD, int W>
+// MODE 0: the clamp_abs u8 plane; MODE 1: the exact S plane (p.s32) and the
+// frame's min / max of g (p.minmax; normalize pass 1).
+template <int NP, bool PAD, int W, int MODE = 0>
 __device__ __forceinline__ void u8_band_compute(const KernelParams& p, const uint8_t* s_band,
                                                 uint64_t* s_bar, uint32_t par, int tx, int oy0,
                                                 int frame, int n_out) {
@@ -341,8 +375,11 @@ __device__ __forceinline__ void u8_band_compute(const KernelParams& p, const uin
     if ((x0 & ~(kLaneCols * 32 - 1)) >= p.out_w) return;  // whole warp right of the image
     const bool full = x0 + kLaneCols <= p.out_w;
     const uint8_t* srow = s_band + T::kLead + threadIdx.x * kLaneCols;
-    uint8_t* out = p.u8 + static_cast<int64_t>(frame) * p.out_frame_stride +
-                   static_cast<int64_t>(oy0) * p.pitch + x0;
+    const int64_t o0 = static_cast<int64_t>(frame) * p.out_frame_stride +
+                       static_cast<int64_t>(oy0) * p.pitch + x0;
+    uint8_t* out = MODE == 0 ? p.u8 + o0 : nullptr;
+    uint32_t* outs = MODE == 1 ? p.s32 + o0 : nullptr;
+    uint32_t s_min = 0xffffffffu, s_max = 0u;
 
     // ring [slot = input row mod 5][pair]; Q accumulators [slot = output row mod 5]
     uint32_t F[5][NP], D[5][NP], H[5][NP], aq[5][NP];
@@ -369,20 +406,41 @@ __device__ __forceinline__ void u8_band_compute(const KernelParams& p, const uin
             u8_row<NP, PAD>(srow + r * T::kRowBytes, x0, p.width, h);
             uint32_t u[2 * NP];
             switch (k) {
-                case 0: u8_step<4>(h, F, D, H, aq, u); break;
-                case 1: u8_step<0>(h, F, D, H, aq, u); break;
-                case 2: u8_step<1>(h, F, D, H, aq, u); break;
-                case 3: u8_step<2>(h, F, D, H, aq, u); break;
-                default: u8_step<3>(h, F, D, H, aq, u); break;
+                case 0: u8_step<4, NP, MODE>(h, F, D, H, aq, u); break;
+                case 1: u8_step<0, NP, MODE>(h, F, D, H, aq, u); break;
+                case 2: u8_step<1, NP, MODE>(h, F, D, H, aq, u); break;
+                case 3: u8_step<2, NP, MODE>(h, F, D, H, aq, u); break;
+                default: u8_step<3, NP, MODE>(h, F, D, H, aq, u); break;
             }
-            u8_store<NP>(out, u, full, x0, p.out_w);
-            out += p.pitch;
+            if constexpr (MODE == 1) {
+                s32_store<NP>(outs, u, full, x0, p.out_w);
+                outs += p.pitch;
+#pragma unroll
+                for (int i = 0; i < 2 * NP; ++i) {
+                    if (full || x0 + i < p.out_w) {
+                        s_min = min(s_min, u[i]);
+                        s_max = max(s_max, u[i]);
+                    }
+                }
+            } else {
+                u8_store<NP>(out, u, full, x0, p.out_w);
+                out += p.pitch;
+            }
+        }
+    }
+    if constexpr (MODE == 1) {  // the frame's min / max of g = sqrt(S), monotone in S
+        s_min = __reduce_min_sync(0xffffffffu, s_min);
+        s_max = __reduce_max_sync(0xffffffffu, s_max);
+        if ((threadIdx.x & 31) == 0 && s_min <= s_max) {
+            sobel5_minmax* mm = p.minmax + frame;
+            atomicMin(reinterpret_cast<unsigned long long*>(&mm->lo_key), dkey(sqrt_u30(s_min)));
+            atomicMax(reinterpret_cast<unsigned long long*>(&mm->hi_key), dkey(sqrt_u30(s_max)));
         }
     }
 }
 
 // The kernel: grid = (column tiles of W * 32 * 2NP, bands, frames).
-template <int NP, bool PAD, int W>
+template <int NP, bool PAD, int W, int MODE = 0>
 __global__ void __launch_bounds__(U8Geom<NP, W>::kThreads, U8Bounds<NP, W>::kMinBlocks)
     sobel5_u8_kernel(const __grid_constant__ KernelParams p) {
     pdl_enter();
@@ -391,7 +449,7 @@ __global__ void __launch_bounds__(U8Geom<NP, W>::kThreads, U8Bounds<NP, W>::kMin
     const int oy0 = blockIdx.y * p.band;
     const int n_out = min(p.band, p.out_h - oy0);
     u8_band_issue<NP, PAD, W>(p, s_band, s_bar, n_out + 4);
-    u8_band_compute<NP, PAD, W>(p, s_band, s_bar, 0u, blockIdx.x, oy0, blockIdx.z, n_out);
+    u8_band_compute<NP, PAD, W, MODE>(p, s_band, s_bar, 0u, blockIdx.x, oy0, blockIdx.z, n_out);
 }
 
 }  // namespace sobel5_b200
