@@ -335,9 +335,16 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     // profiles/r1/tma_load.txt).  SOBEL5_TMA_LOAD=0 disables it.
     // Stacked bands (C5, halos possibly in a peer GPU's memory): only the CTAs
     // whose rows are all in `mid` bulk-copy them (kGeomSegTma).
+    // (opt-in SOBEL5_F32_TMA=1: kernel F, the packed-FP32 kernel of larger
+    // taps, with TMA band rows on plain images -- measured slower at every
+    // band, 8K (2,3,5,7) SR 182.8 us at 16 rows vs 168.5 on the register
+    // ring: it is bound by its FFMA2 chains, not by the row loads;
+    // profiles/r2/f32_tma.txt)
+    const bool f32_tma = !taps_are_default(*taps) && !taps_fit_packed(*taps) && taps_fit_f32(*taps) &&
+                         !ex.pad && !top && !bot && env_int("SOBEL5_F32_TMA", 0) != 0;
     kp.tma_load = (prefetch && (!ex.pad || env_int("SOBEL5_TMA_PAD", 1) != 0) &&
                    ((!top && !bot) || env_int("SOBEL5_TMA_SEG", 1) != 0) &&
-                   (out->g || out->g32) && taps_are_default(*taps) &&
+                   (out->g || out->g32) && (taps_are_default(*taps) || f32_tma) &&
                    env_int("SOBEL5_TMA_LOAD", 1) != 0 && env_int("SOBEL5_GENERIC", 0) == 0 &&
                    env_int("SOBEL5_DENSE", 0) == 0 && !(ex.u8_norm || ex.norm))
                       ? 1

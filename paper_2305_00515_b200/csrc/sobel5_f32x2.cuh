@@ -62,6 +62,13 @@ __global__ void __launch_bounds__(kCtaThreads, SOBEL5_F32_MIN_CTAS)
     if (p.diag) odd_init(s_odd);
     constexpr bool SEG = GEOM == kGeomSeg;
     constexpr bool PAD = GEOM == kGeomPad;
+    // TMAL: the CTA's band rows bulk-copied into shared memory at CTA start
+    // (tma_band_issue, as kernel A's kGeomPlainTma), read when consumed
+    // (instantiated with PF = 0): no global-load latency in the row loop
+    constexpr bool TMAL = GEOM == kGeomPlainTma;
+    __shared__ __align__(128) uint8_t s_band[TMAL ? TmaBand<false>::kBytes : 16];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    if constexpr (TMAL) tma_band_issue<false>(p, s_band, s_bar);
     constexpr bool RT = OUTS == kOutRuntime;
     const bool w_gx = RT ? p.gx != nullptr : (OUTS & kOutGx) != 0;
     const bool w_gy = RT ? p.gy != nullptr : (OUTS & kOutGy) != 0;
@@ -96,6 +103,12 @@ __global__ void __launch_bounds__(kCtaThreads, SOBEL5_F32_MIN_CTAS)
 
     const uint8_t* plain = p.mid + in_frame + static_cast<int64_t>(oy0) * p.in_pitch + x0;
     auto load_row = [&](int r, uint32_t& a, uint32_t& b) {
+        if constexpr (TMAL) {
+            const uint8_t* sr = tma_band_row<false>(s_band, s_bar, r, x0);
+            a = load_a ? *reinterpret_cast<const uint32_t*>(sr) : 0u;
+            b = load_b ? *reinterpret_cast<const uint32_t*>(sr + xoff) : 0u;
+            return;
+        }
         const uint8_t* rp;
         if (SEG) {
             rp = stacked_row(p, in_frame, oy0 + r) + x0;

@@ -25,6 +25,8 @@ template <int PF>
 cudaError_t geom(const KernelParams& kp, dim3 grid, MagMode mag, cudaStream_t s) {
     if (kp.pad) return go<PF, kGeomPad>(kp, grid, mag, s);
     if (kp.top_rows > 0 || kp.bot != nullptr) return go<PF, kGeomSeg>(kp, grid, mag, s);
+    // band rows by TMA (launch_common decides), read from shared memory when consumed
+    if (PF > 0 && kp.tma_load) return go<0, kGeomPlainTma>(kp, grid, mag, s);
     return go<PF, kGeomPlain>(kp, grid, mag, s);
 }
 }  // namespace
