@@ -139,6 +139,13 @@ struct sobel5_ctx {
     void* h_wire[4] = {};
     size_t h_wire_bytes[4] = {};
     bool wire = false;
+    // sobel5_run_host's wire layout is chunk-major: chunk k's four int16
+    // planes are one contiguous block (device and staging), moved by ONE
+    // copy per chunk instead of four; wire_pitch = their row pitch (elements)
+    bool wire_cm = false;
+    int64_t wire_pitch = 0;
+    void* d_wire = nullptr;
+    size_t d_wire_bytes = 0;
     std::vector<cudaEvent_t> ev_in, ev_comp, ev_out;
     HostPool pool;
     // state between sobel5_run_host_begin and _finish
@@ -328,9 +335,11 @@ void finish_staged(sobel5_ctx* ctx, void* const staged[7], int out_w, int rows) 
 sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
                              const sobel5_taps* taps, int prefetch, unsigned mask,
                              void* const dst[7], int* chunk_out, int* n_chunks_out,
-                             StageBudget& budget, int op = 5, bool wire = false) {
+                             StageBudget& budget, int op = 5, bool wire = false,
+                             bool chunk_major = false) {
     const int R = op == 3 ? 1 : 2;  // operator radius
     ctx->wire = wire;
+    ctx->wire_cm = wire && chunk_major;
     const int out_w = width - 2 * R, out_h = height - 2 * R;
     const int64_t in_pitch = round_up(width, 128);
     const int64_t dpitch = round_up(out_w, 32);  // elements; 128 B-aligned int rows
@@ -351,6 +360,16 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
     for (int i = 0; i < 7; ++i) {
         if (!((mask >> i) & 1u)) continue;
         const size_t plane_bytes = static_cast<size_t>(out_w) * out_h * wire_elem(ctx, i);
+        if (ctx->wire_cm && i < 4) {
+            // block of the four int16 planes, padded rows (dpitch); the
+            // per-chunk plane pointers are set at the launches
+            const size_t wb = 4 * static_cast<size_t>(dpitch) * out_h * 2;
+            CK(ensure(&ctx->d_wire, &ctx->d_wire_bytes, wb));
+            CK(ensure_host(&ctx->h_wire[0], &ctx->h_wire_bytes[0], wb));
+            *dslots[i] = ctx->d_wire;
+            hdst[i] = ctx->h_wire[0];
+            continue;
+        }
         CK(ensure(&ctx->d_plane[i], &ctx->d_plane_bytes[i],
                   static_cast<size_t>(dpitch) * out_h * kElem[i]));
         *dslots[i] = ctx->d_plane[i];
@@ -373,6 +392,7 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
     int chunk = std::max(256, (out_h + n_want - 1) / n_want);
     chunk = std::min(chunk, out_h);
     const int n_chunks = (out_h + chunk - 1) / chunk;
+    ctx->wire_pitch = dpitch;
     CK(ensure_events(ctx->ev_in, static_cast<size_t>(n_chunks)));
     CK(ensure_events(ctx->ev_comp, static_cast<size_t>(n_chunks)));
     CK(ensure_events(ctx->ev_out, static_cast<size_t>(n_chunks)));
@@ -394,10 +414,20 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
         // int16 wire planes: the kernel addresses them as int16 at the int32
         // pointer (dpitch is even, so the chunk starts on an int32 boundary)
         const int64_t off_g = wire ? off / 2 : off;
-        if (sub.gx) sub.gx += off_g;
-        if (sub.gy) sub.gy += off_g;
-        if (sub.gd) sub.gd += off_g;
-        if (sub.gdt) sub.gdt += off_g;
+        if (ctx->wire_cm) {
+            // chunk k's block: plane p at (4 k chunk + p (y1 - y0)) rows
+            int16_t* blk = static_cast<int16_t*>(ctx->d_wire) + 4 * static_cast<int64_t>(y0) * dpitch;
+            const int64_t ps = static_cast<int64_t>(y1 - y0) * dpitch;
+            sub.gx = reinterpret_cast<int32_t*>(blk);
+            sub.gy = reinterpret_cast<int32_t*>(blk + ps);
+            sub.gd = reinterpret_cast<int32_t*>(blk + 2 * ps);
+            sub.gdt = reinterpret_cast<int32_t*>(blk + 3 * ps);
+        } else {
+            if (sub.gx) sub.gx += off_g;
+            if (sub.gy) sub.gy += off_g;
+            if (sub.gd) sub.gd += off_g;
+            if (sub.gdt) sub.gdt += off_g;
+        }
         if (sub.g) sub.g += off;
         if (sub.g32) sub.g32 += off;
         if (sub.u8) sub.u8 += off;
@@ -416,8 +446,16 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
         }
         CK(cudaEventRecord(ctx->ev_comp[k], ctx->s_comp));
         CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_comp[k], 0));
+        if (ctx->wire_cm) {  // the four int16 planes of the chunk: one copy
+            const size_t off = 4 * static_cast<size_t>(y0) * dpitch * 2;
+            const size_t n = 4 * static_cast<size_t>(y1 - y0) * dpitch * 2;
+            ctx->last_d2h += n;
+            CK(cudaMemcpyAsync(static_cast<char*>(ctx->h_wire[0]) + off,
+                               static_cast<const char*>(ctx->d_wire) + off, n,
+                               cudaMemcpyDeviceToHost, ctx->s_d2h));
+        }
         for (int i = 0; i < 7; ++i) {
-            if (!hdst[i]) continue;
+            if (!hdst[i] || (ctx->wire_cm && i < 4)) continue;
             const size_t es = wire_elem(ctx, i);
             ctx->last_d2h += static_cast<uint64_t>(out_w) * es * static_cast<uint64_t>(y1 - y0);
             CK(cudaMemcpy2DAsync(static_cast<char*>(hdst[i]) + static_cast<size_t>(y0) * out_w * es,
@@ -447,26 +485,46 @@ sobel5_status drain_stream(sobel5_ctx* ctx, int out_w, int out_h, int chunk, int
     struct Piece {
         char* dst;
         const char* src;
-        size_t n;     // bytes of src
+        size_t n;     // bytes of src (rows: row count)
         bool widen;   // int16 wire -> int32 destination
+        bool rows = false;  // chunk-major wire: n rows of out_w, source pitch wire_pitch
     };
     std::vector<Piece> pieces;
     for (int k = 0; k < n_chunks; ++k) {
         CK(cudaEventSynchronize(ctx->ev_out[k]));
         const int y0 = k * chunk, y1 = std::min(out_h, y0 + chunk);
         pieces.clear();
+        if (ctx->wire_cm) {
+            // rows of the chunk's four int16 planes, ~1 MiB of output per piece
+            const int64_t dp = ctx->wire_pitch, rows = y1 - y0;
+            const int per = std::max<int64_t>(1, (int64_t{1} << 18) / std::max(out_w, 1));
+            const int16_t* blk = static_cast<const int16_t*>(ctx->h_wire[0]) + 4 * static_cast<int64_t>(y0) * dp;
+            for (int i = 0; i < 4; ++i) {
+                if (!stage_dst[i]) continue;
+                for (int64_t r = 0; r < rows; r += per)
+                    pieces.push_back({static_cast<char*>(stage_dst[i]) +
+                                          (static_cast<size_t>(y0 + r) * out_w) * 4,
+                                      reinterpret_cast<const char*>(blk + (i * rows + r) * dp),
+                                      static_cast<size_t>(std::min<int64_t>(per, rows - r)), true, true});
+            }
+        }
         for (int i = 0; i < 7; ++i) {
-            if (!stage_dst[i]) continue;
+            if (!stage_dst[i] || (ctx->wire_cm && i < 4)) continue;
             const bool widen = ctx->wire && i < 4;
             const size_t es = wire_elem(ctx, i), row = static_cast<size_t>(out_w) * es;
             const size_t off = static_cast<size_t>(y0) * row, n = static_cast<size_t>(y1 - y0) * row;
             const char* src = static_cast<const char*>(widen ? ctx->h_wire[i] : ctx->h_stage[i]);
             for (size_t o = 0; o < n; o += kPiece)
                 pieces.push_back({static_cast<char*>(stage_dst[i]) + (widen ? 2 : 1) * (off + o),
-                                  src + off + o, std::min(kPiece, n - o), widen});
+                                  src + off + o, std::min(kPiece, n - o), widen, false});
         }
         auto move = [&](const Piece& q) {
-            if (q.widen)
+            if (q.rows) {
+                for (size_t r = 0; r < q.n; ++r)
+                    sobel5_b200::widen_i16(reinterpret_cast<int32_t*>(q.dst) + r * out_w,
+                                           reinterpret_cast<const int16_t*>(q.src) + r * ctx->wire_pitch,
+                                           static_cast<size_t>(out_w));
+            } else if (q.widen)
                 sobel5_b200::widen_i16(reinterpret_cast<int32_t*>(q.dst),
                                        reinterpret_cast<const int16_t*>(q.src), q.n / 2);
             else
@@ -523,6 +581,7 @@ void sobel5_ctx_destroy(sobel5_ctx* ctx) {
     for (auto ev : ctx->ev_comp) cudaEventDestroy(ev);
     for (auto ev : ctx->ev_out) cudaEventDestroy(ev);
     if (ctx->d_in) cudaFree(ctx->d_in);
+    if (ctx->d_wire) cudaFree(ctx->d_wire);
     for (void* p : ctx->d_plane)
         if (p) cudaFree(p);
     for (void* p : ctx->h_stage)
@@ -570,7 +629,8 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     void* staged[7] = {};  // pageable ones: through pinned staging (and the int16 wire planes)
     StageBudget budget;    // the planes first, then the input if it still fits
     const size_t n_px = static_cast<size_t>(out_w) * out_h;
-    const bool wire = want_wire(mask, taps, 5, false) && budget.take(4 * n_px * 2);
+    const bool wire = want_wire(mask, taps, 5, false) &&
+                      budget.take(4 * static_cast<size_t>(round_up(out_w, 32)) * out_h * 2);
     for (int i = 0; i < 7; ++i) {
         if (!hp[i]) continue;
         if (wire && i < 4) {
@@ -584,7 +644,7 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     }
     int chunk = 0, n_chunks = 0;
     const sobel5_status st = enqueue_stream(ctx, h_in, width, height, taps, prefetch, mask, direct,
-                                            &chunk, &n_chunks, budget, 5, wire);
+                                            &chunk, &n_chunks, budget, 5, wire, true);
     if (st != SOBEL5_OK) return st;
     return drain_stream(ctx, out_w, out_h, chunk, n_chunks, staged, diag_out);
 }
@@ -609,6 +669,9 @@ void sobel5_ctx_trim(sobel5_ctx* ctx) {
     if (ctx->h_in_stage) cudaFreeHost(ctx->h_in_stage);
     ctx->h_in_stage = nullptr;
     ctx->h_in_stage_bytes = 0;
+    if (ctx->d_wire) cudaFree(ctx->d_wire);
+    ctx->d_wire = nullptr;
+    ctx->d_wire_bytes = 0;
     if (ctx->d_in) cudaFree(ctx->d_in);
     ctx->d_in = nullptr;
     ctx->d_in_bytes = 0;

@@ -68,8 +68,11 @@ def test_run_host_sr_wire(ctx, oracle, monkeypatch, wire, h, w, kind):
                              C.byref(planes_struct(res, ow)), C.byref(d)) == 0
     for k in PLANES:
         np.testing.assert_array_equal(res[k], ref[k], err_msg=f"pageable {k} wire={wire}")
-    # bytes over PCIe: 4 x int16 + f64 with the wire, 4 x int32 + f64 without
-    assert L.sobel5_ctx_last_d2h_bytes(ctx.handle) == ow * oh * (16 if wire == "1" else 24)
+    # bytes over PCIe: the four int16 planes as one block per row chunk (rows
+    # padded to 32 elements) + f64 with the wire, 4 x int32 + f64 without
+    dp = (ow + 31) // 32 * 32
+    want = 4 * dp * oh * 2 + ow * oh * 8 if wire == "1" else ow * oh * 24
+    assert L.sobel5_ctx_last_d2h_bytes(ctx.handle) == want
     # page-locked planes (the bench's e2e path)
     pin = {k: torch.full((oh, ow), 7, dtype=getattr(torch, np.dtype(DT[k]).name)).pin_memory()
            for k in PLANES}

@@ -171,6 +171,43 @@ int main() {
             for (auto& e : ev) cudaEventDestroy(e);
         }
     }
+    // (4) k of the 4 gradient planes narrow (int16 + host widening), the
+    // other 4-k int32 straight into the destination: 8 host threads, 16 chunks
+    for (int k = 0; k <= 4; ++k) {
+        const int chunks = 16, T = 8;
+        std::vector<cudaEvent_t> ev(chunks);
+        for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        double best = 1e9;
+        for (int rep = 0; rep < 3; ++rep) {
+            const double t0 = now();
+            const size_t rows = (H + chunks - 1) / chunks;
+            for (int c = 0; c < chunks; ++c) {
+                const size_t o = std::min<size_t>(H, c * rows) * W, e = std::min<size_t>(H, (c + 1) * rows) * W;
+                for (int i = 0; i < 4; ++i) {
+                    if (i < k) CK(cudaMemcpyAsync(s16[i] + o, d16[i] + o, (e - o) * 2, cudaMemcpyDeviceToHost, s));
+                    else CK(cudaMemcpyAsync(h32[i] + o, d32[i] + o, (e - o) * 4, cudaMemcpyDeviceToHost, s));
+                }
+                CK(cudaMemcpyAsync(hg + o, dg + o, (e - o) * 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaEventRecord(ev[c], s));
+            }
+            for (int c = 0; c < chunks; ++c) {
+                CK(cudaEventSynchronize(ev[c]));
+                if (k == 0) continue;
+                const size_t o = std::min<size_t>(H, c * rows) * W, e = std::min<size_t>(H, (c + 1) * rows) * W;
+                const size_t n = e - o;
+                par(T, static_cast<size_t>(k) * n, [&](size_t a, size_t b) {
+                    for (int i = 0; i < k; ++i) {
+                        const size_t lo = std::max(a, i * n), hi = std::min(b, (i + 1) * n);
+                        if (lo < hi) widen(h32[i] + o + (lo - i * n), s16[i] + o + (lo - i * n), hi - lo, true);
+                    }
+                });
+            }
+            best = std::min(best, now() - t0);
+        }
+        std::printf("(4) %d of 4 gradient planes on the int16 wire: %.2f ms (%.2f Gpx/s)\n", k, best * 1e3,
+                    N / best / 1e9);
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
     std::printf("check %d %d\n", h32[0][12345], h32[3][N - 1]);
     return 0;
 }
