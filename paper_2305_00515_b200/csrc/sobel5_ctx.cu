@@ -388,7 +388,8 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
     // each kernel still fills the GPU.
     // (16 with the int16 wire: the host widening of chunk k overlaps the
     // download of chunk k+1, so shorter chunks expose less of it)
-    const int n_want = wire ? 16 : 8;
+    const char* cv = std::getenv("SOBEL5_CHUNKS");
+    const int n_want = cv && *cv && std::atoi(cv) > 0 ? std::atoi(cv) : (wire ? 16 : 8);
     int chunk = std::max(256, (out_h + n_want - 1) / n_want);
     chunk = std::min(chunk, out_h);
     const int n_chunks = (out_h + chunk - 1) / chunk;
