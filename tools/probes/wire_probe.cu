@@ -208,6 +208,54 @@ int main() {
                     N / best / 1e9);
         for (auto& e : ev) cudaEventDestroy(e);
     }
+    // (5) chunk-major int16 blocks through a SMALL staging ring (slots
+    // reused every `slots` chunks, so DMA writes may land in the host LLC
+    // (DDIO) and the widening reads them from there): the D2H of chunk k is
+    // enqueued once chunk k - slots has been widened
+    for (int chunks : {16, 32, 64}) {
+        for (int slots : {2, 3, 4, 8}) {
+            const int T = 8;
+            const size_t rows = (H + chunks - 1) / chunks;
+            const size_t blk = 4 * rows * W;  // int16 elements per chunk block
+            int16_t* ring = nullptr;
+            CK(cudaMallocHost(&ring, blk * 2 * slots));
+            int16_t* dblk = nullptr;
+            CK(cudaMalloc(&dblk, blk * 2 * chunks));
+            std::vector<cudaEvent_t> ev(chunks);
+            for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            double best = 1e9;
+            for (int rep = 0; rep < 3; ++rep) {
+                const double t0 = now();
+                auto enqueue = [&](int c) {
+                    const size_t y0 = std::min<size_t>(H, c * rows), y1 = std::min<size_t>(H, (c + 1) * rows);
+                    const size_t n = 4 * (y1 - y0) * W;
+                    CK(cudaMemcpyAsync(ring + (c % slots) * blk, dblk + c * blk, n * 2, cudaMemcpyDeviceToHost, s));
+                    CK(cudaMemcpyAsync(hg + y0 * W, dg + y0 * W, (y1 - y0) * W * 8, cudaMemcpyDeviceToHost, s));
+                    CK(cudaEventRecord(ev[c], s));
+                };
+                for (int c = 0; c < std::min(slots, chunks); ++c) enqueue(c);
+                for (int c = 0; c < chunks; ++c) {
+                    CK(cudaEventSynchronize(ev[c]));
+                    const size_t y0 = std::min<size_t>(H, c * rows), y1 = std::min<size_t>(H, (c + 1) * rows);
+                    const size_t n = (y1 - y0) * W;
+                    const int16_t* src = ring + (c % slots) * blk;
+                    par(T, 4 * n, [&](size_t a, size_t b) {
+                        for (int i = 0; i < 4; ++i) {
+                            const size_t lo = std::max(a, i * n), hi = std::min(b, (i + 1) * n);
+                            if (lo < hi) widen(h32[i] + y0 * W + (lo - i * n), src + i * n + (lo - i * n), hi - lo, true);
+                        }
+                    });
+                    if (c + slots < chunks) enqueue(c + slots);
+                }
+                best = std::min(best, now() - t0);
+            }
+            std::printf("(5) ring: %2d chunks, %d slots (%.1f MB staging): %.2f ms (%.2f Gpx/s)\n", chunks, slots,
+                        blk * 2.0 * slots / 1e6, best * 1e3, N / best / 1e9);
+            for (auto& e : ev) cudaEventDestroy(e);
+            cudaFreeHost(ring);
+            cudaFree(dblk);
+        }
+    }
     std::printf("check %d %d\n", h32[0][12345], h32[3][N - 1]);
     return 0;
 }
