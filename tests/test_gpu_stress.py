@@ -35,6 +35,12 @@ def test_random_launch_space(cuda, oracle, monkeypatch, seed):
             monkeypatch.setenv("SOBEL5_BAND", band)
         else:
             monkeypatch.delenv("SOBEL5_BAND", raising=False)
+        # the u8-only kernels' CTA width (sobel5_u8.cuh): default rule or forced
+        warps = str(rng.choice(["", "1", "2", "4"]))
+        if warps:
+            monkeypatch.setenv("SOBEL5_U8_WARPS", warps)
+        else:
+            monkeypatch.delenv("SOBEL5_U8_WARPS", raising=False)
         img = (rng.integers(0, 256, (h, w), dtype=np.uint8) & mask).astype(np.uint8)
         st_t = oracle.make_stream_taps(*prm)
         taps = api.Taps.from_dict(st_t.as_dict())
@@ -122,3 +128,80 @@ def test_random_stacked_bands(cuda, oracle, monkeypatch, seed):
                 assert ulps.max() <= 1, what
             else:
                 np.testing.assert_array_equal(got, want, err_msg=f"{k} {what}")
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SOBEL5_STRESS_SEEDS", "6"))))
+def test_random_3x3_and_detect(cuda, oracle, monkeypatch, seed):
+    """The 3x3 operator (every output subset incl. the u8-only kernel
+    sobel3_u8.cuh) and the detect export in both SaveModes (normalize pass 1
+    on kernel U's S mode for the default taps), random sizes, padding,
+    prefetch, forced bands and u8 CTA widths."""
+    import torch
+    from paper_2305_00515_b200 import api
+    rng = np.random.default_rng(9000 + seed)
+    for case in range(8):
+        w = int(rng.choice([3, 9, 127, 131, 509, 1029, 2055]))
+        h = int(rng.integers(3, 80))
+        pad = bool(rng.integers(0, 2))
+        pf = int(rng.integers(0, 2))
+        band = BANDS[int(rng.integers(0, len(BANDS)))]
+        warps = str(rng.choice(["", "1", "2", "4"]))
+        for name, val in (("SOBEL5_BAND", band), ("SOBEL5_U8_WARPS", warps)):
+            if val:
+                monkeypatch.setenv(name, val)
+            else:
+                monkeypatch.delenv(name, raising=False)
+        mask = int(rng.choice([0xFF, 0x0F, 0x03]))
+        img = (rng.integers(0, 256, (h, w), dtype=np.uint8) & mask).astype(np.uint8)
+        d, pitch = api.alloc_input(w, h)
+        d.fill_(0xA5)
+        d[:, :w].copy_(torch.from_numpy(img))
+        what = f"{w}x{h} pad={pad} pf={pf} band={band or 'auto'} warps={warps or 'auto'}"
+        if case % 2 == 0:  # 3x3 operator
+            if not pad and (w < 3 or h < 3):
+                continue
+            planes = [("gx", "gy", "g"), ("u8",), ("gy", "u8"), ("g32",)][int(rng.integers(0, 4))]
+            ow, oh = (w, h) if pad else (w - 2, h - 2)
+            src = img
+            if pad:
+                st, src = oracle.pad_replicate(img, 1)
+                assert st == 0
+            st, ref = oracle.sobel3_2d(src)
+            assert st == 0
+            out, op = api.alloc_planes(ow, oh, planes)
+            for v in out.values():
+                v.fill_(0x5A if v.dtype == torch.uint8 else 7)
+            api.launch3(d, pitch, w, h, pf, pad, out, op)
+            torch.cuda.synchronize()
+            for k in planes:
+                got = out[k][:, :ow].cpu().numpy()
+                if k == "u8":
+                    np.testing.assert_array_equal(got, oracle.quantize(ref["g"], "clamp_abs"),
+                                                  err_msg=f"3x3 u8 {what}")
+                elif k == "g32":
+                    exact = ref["g"].astype(np.float32)
+                    ulps = np.abs(got.view(np.int32).astype(np.int64) - exact.view(np.int32))
+                    assert ulps.max() <= 1, what
+                else:
+                    np.testing.assert_array_equal(got, ref[k], err_msg=f"3x3 {k} {what}")
+        else:  # detect: pad_replicate(img, 2) (optional) -> run_stream -> quantize(g)
+            if not pad and (w < 5 or h < 5):
+                continue
+            mode = api.SaveMode.normalize if rng.integers(0, 2) else api.SaveMode.clamp_abs
+            ow, oh = (w, h) if pad else (w - 4, h - 4)
+            src = img
+            if pad:
+                st, src = oracle.pad_replicate(img, 2)
+                assert st == 0
+            st, ref, _ = oracle.run_stream(src)
+            assert st == 0
+            out, op = api.alloc_planes(ow, oh, ("u8",))
+            out["u8"].fill_(0x5A)
+            scratch = api.alloc_scratch(1, "cuda", out_h=oh, pitch=op)
+            api.detect_device(d, pitch, w, h, api.make_stream_taps(), pf, pad, mode, out, op,
+                              scratch)
+            torch.cuda.synchronize()
+            want = oracle.quantize(ref["g"], "normalize" if mode == api.SaveMode.normalize
+                                   else "clamp_abs")
+            np.testing.assert_array_equal(out["u8"][:, :ow].cpu().numpy(), want,
+                                          err_msg=f"detect {mode} {what}")
