@@ -4,7 +4,7 @@
 # C ABI), plus the round-1 subset.  memcheck / racecheck / synccheck.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
 T1="tests/test_gpu_parity.py::test_random_sweep_vs_oracle tests/test_gpu_parity.py::test_tma_band_loads_any_band tests/test_gpu_detect.py::test_pad_tma_band_loads tests/test_gpu_sobel3.py::test_sobel3_launch"
-T2="tests/test_gpu_u8_only.py tests/test_gpu_parity.py::test_parity_violation_pair_matches_reference tests/test_gpu_tma_store.py tests/test_gpu_mgpu.py"
+T2="tests/test_gpu_u8_only.py tests/test_gpu_parity.py::test_parity_violation_pair_matches_reference tests/test_gpu_tma_store.py tests/test_gpu_mgpu.py tests/test_gpu_detect.py tests/test_gpu_sobel3.py"
 T3="tests/test_gpu_wire16.py"
 for tool in memcheck racecheck synccheck; do
   echo "== $tool"
