@@ -340,9 +340,12 @@ __device__ __forceinline__ void u8_store(uint8_t* out, const uint32_t (&u)[2 * N
     }
 }
 
+#ifndef SOBEL5_U8_WARPS_PER_SM
+#define SOBEL5_U8_WARPS_PER_SM 16  // NP = 4: 128 registers; 20 / 24 spill (88 / 152 B) and were slower
+#endif
 template <int NP, int W>
 struct U8Bounds {  // resident CTAs per SM the register budget is set for
-    static constexpr int kMinBlocks = (NP == 4 ? 16 : 24) / W;
+    static constexpr int kMinBlocks = (NP == 4 ? SOBEL5_U8_WARPS_PER_SM : 24) / W;
 };
 
 // 2NP exact S values (u[k] = pixel x0 + k) to the S plane row (MODE 1).
