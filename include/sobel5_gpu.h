@@ -343,11 +343,10 @@ sobel5_status sobel3_run_host_begin(sobel5_ctx* ctx, const uint8_t* h_in, int wi
 const void* sobel5_run_host_staging(const sobel5_ctx* ctx, int plane);
 /* Bytes per element of staged plane i of the pending call (0 if not in the
  * mask).  With default taps and exactly the StreamResult planes (mask 0x1f)
- * sobel5_run_host ships gx, gy, gd, gdt over PCIe as int16 (every value lies
- * in [-2^15, 2^15)) and widens them into the caller's int32 planes (env
- * SOBEL5_WIRE16=0 disables it).  The split _begin form does so only with
- * SOBEL5_WIRE16=2: the staging of those planes then holds int16 (2) and the
- * consumer sign-extends (_finish with h_out widens itself). */
+ * gx, gy, gd, gdt cross PCIe as int16 (every value lies in [-2^15, 2^15);
+ * env SOBEL5_WIRE16=0 disables it): sobel5_run_host widens them into the
+ * caller's int32 planes itself; in the split _begin form their staging holds
+ * int16 (2) and the consumer sign-extends (_finish with h_out widens). */
 int sobel5_run_host_staging_elem(const sobel5_ctx* ctx, int plane);
 
 /* ---- the classic 3x3 two-direction operator ---------

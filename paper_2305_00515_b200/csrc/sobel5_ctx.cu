@@ -178,15 +178,11 @@ size_t wire_elem(const sobel5_ctx* ctx, int i) { return ctx->wire && i < 4 ? 2 :
 
 // The int16 wire applies to a 5x5 call with exactly the StreamResult planes
 // and default taps (sobel5_b200::n16_wire_ok), if its int16 staging fits.
-// The split begin/_chunk form (the C++ drop-in, which fills freshly
-// allocated planes and is bound by page faults, not PCIe) uses it only when
-// SOBEL5_WIRE16=2: its consumers' int16 -> int32 appends measured slower
-// (8K run_stream 64 vs 55 ms).
-bool want_wire(unsigned mask, const sobel5_taps* taps, int op, bool split) {
-    if (split) {
-        const char* v = std::getenv("SOBEL5_WIRE16");
-        if (!v || std::atoi(v) < 2) return false;
-    }
+// The split begin/_chunk form (the C++ drop-in, which appends each row
+// chunk into freshly allocated planes) uses it too, with 8 row chunks
+// (8K run_stream 48.2-50.6 vs 53.4-54.5 ms without the wire; 16 chunks
+// cost it ~10 ms of per-chunk synchronisation: profiles/r2/cpp_wire.txt).
+bool want_wire(unsigned mask, const sobel5_taps* taps, int op, bool /*split*/) {
     return op == 5 && mask == 0x1fu && sobel5_b200::n16_wire_ok(taps);
 }
 
@@ -386,10 +382,11 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
 
     // Row chunks: enough to overlap copies with compute, few enough that
     // each kernel still fills the GPU.
-    // (16 with the int16 wire: the host widening of chunk k overlaps the
-    // download of chunk k+1, so shorter chunks expose less of it)
+    // (16 for sobel5_run_host's int16 wire: the host widening of chunk k
+    // overlaps the download of chunk k+1, so shorter chunks expose less of
+    // it; the split form's consumers synchronise per chunk and prefer 8)
     const char* cv = std::getenv("SOBEL5_CHUNKS");
-    const int n_want = cv && *cv && std::atoi(cv) > 0 ? std::atoi(cv) : (wire ? 16 : 8);
+    const int n_want = cv && *cv && std::atoi(cv) > 0 ? std::atoi(cv) : (ctx->wire_cm ? 16 : 8);
     int chunk = std::max(256, (out_h + n_want - 1) / n_want);
     chunk = std::min(chunk, out_h);
     const int n_chunks = (out_h + chunk - 1) / chunk;

@@ -45,11 +45,10 @@ def test_cpp_api_gpu_staging_cap(exe, cuda):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("wire", ["2", "0"])
+@pytest.mark.parametrize("wire", ["1", "0"])
 def test_cpp_api_gpu_wire(exe, cuda, wire):
-    """The same checks with the split form's int16 wire forced on (the C++
-    run_stream then sign-extends gx..gdt from the int16 staging) and with
-    every wire off."""
+    """The same checks with the int16 wire on (the default: the C++
+    run_stream sign-extends gx..gdt from the int16 staging) and off."""
     env = dict(os.environ, SOBEL5_WIRE16=wire)
     r = subprocess.run([exe, "--gpu"], capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stdout + r.stderr

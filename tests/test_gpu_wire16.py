@@ -85,9 +85,8 @@ def test_run_host_sr_wire(ctx, oracle, monkeypatch, wire, h, w, kind):
 
 @pytest.mark.parametrize("wire", ["2", "1", "0"])
 def test_staging_elem_and_consumer(ctx, oracle, monkeypatch, wire):
-    """begin(0x1f) -> _staging_elem / _staging (int16 when the split form's
-    wire is on, SOBEL5_WIRE16=2) -> the consumer widens the rows itself ->
-    finish(NULL)."""
+    """begin(0x1f) -> _staging_elem / _staging (int16 unless SOBEL5_WIRE16=0)
+    -> the consumer widens the rows itself -> finish(NULL)."""
     from paper_2305_00515_b200 import _abi, api
     monkeypatch.setenv("SOBEL5_WIRE16", wire)
     L = _abi.load()
@@ -98,7 +97,7 @@ def test_staging_elem_and_consumer(ctx, oracle, monkeypatch, wire):
     taps = api.make_stream_taps()
     assert L.sobel5_run_host_staging_elem(ctx.handle, 0) == 0  # nothing pending
     assert L.sobel5_run_host_begin(ctx.handle, img.ctypes.data, w, h, C.byref(taps), 1, 0x1F) == 0
-    want = 2 if wire == "2" else 4
+    want = 2 if wire in ("1", "2") else 4
     assert [L.sobel5_run_host_staging_elem(ctx.handle, i) for i in range(7)] == \
         [want] * 4 + [8, 0, 0]
     y0, y1, k = C.c_int(), C.c_int(), 0
@@ -138,8 +137,8 @@ def test_wire_not_for_custom_taps_or_other_masks(ctx, oracle):
 
 
 def test_split_form_finish_widens(ctx, oracle, monkeypatch):
-    """SOBEL5_WIRE16=2: begin(0x1f) -> finish(h_out) widens the int16
-    staging into the caller's int32 planes (several row chunks)."""
+    """begin(0x1f) -> finish(h_out) widens the int16 staging into the
+    caller's int32 planes (several row chunks)."""
     from paper_2305_00515_b200 import _abi, api
     monkeypatch.setenv("SOBEL5_WIRE16", "2")
     L = _abi.load()
