@@ -28,6 +28,7 @@ template <int PF, bool PAD>
 cudaError_t outs(const KernelParams& kp, dim3 grid, cudaStream_t s) {
     switch (packed_out_set(kp)) {
         case kOut3: return go<PF, PAD, kOut3>(kp, grid, s);
+        case kOut3 | kOutN16: return go<PF, PAD, kOut3 | kOutN16>(kp, grid, s);
         case kOutU8: return go<PF, PAD, kOutU8>(kp, grid, s);
         case kOutMinMax: return go<PF, PAD, kOutMinMax>(kp, grid, s);
         case kOutMinMax | kOutS32: return go<PF, PAD, kOutMinMax | kOutS32>(kp, grid, s);
@@ -57,6 +58,9 @@ sobel5_status sobel3_common(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
     const int out_h = ex.pad ? height : height - 2;
     if (sobel5_status st = check_planes(out, out_w); st != SOBEL5_OK) return st;
     if (out->gd || out->gdt) return SOBEL5_INVALID_ARG;  // the 3x3 operator has no diagonals
+    if (ex.n16 && (ex.pad || !out->gx || !out->gy || !out->g || out->g32 || out->u8 || ex.minmax ||
+                   ex.norm || ex.u8_norm || ex.s32))
+        return SOBEL5_INVALID_ARG;  // the int16 wire: exactly the Stream3Result, valid mode
     if (ex.u8_norm && (!ex.norm || !out->u8)) return SOBEL5_INVALID_ARG;
 
     KernelParams kp{};
@@ -80,6 +84,7 @@ sobel5_status sobel3_common(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
     kp.norm = ex.norm;
     kp.u8_norm = ex.u8_norm;
     kp.s32 = ex.s32;
+    kp.n16 = ex.n16;
     // the write-bound Stream3Result contract reads its band rows by TMA, as the
     // 5x5 kernel does, with 4-row bands (8K: 89.6 vs 91.3 us at 8; 2r = 2 halo
     // rows per band), SOBEL5_TMA_LOAD=0 disables it

@@ -67,6 +67,9 @@ __global__ void __launch_bounds__(kCtaThreads, OUTS == kOutU8 ? SOBEL5_U8_MIN_CT
     constexpr bool RT = OUTS == kOutRuntime;
     const bool w_gx = RT ? p.gx != nullptr : (OUTS & kOutGx) != 0;
     const bool w_gy = RT ? p.gy != nullptr : (OUTS & kOutGy) != 0;
+    // gx, gy as int16 at the int32 pointers (the host path's narrow D2H
+    // wire, |gx|, |gy| <= 1020)
+    constexpr bool N16 = !RT && (OUTS & kOutN16) != 0;
     const bool w_g = RT ? p.g != nullptr : (OUTS & kOutG) != 0;
     const bool w_g32 = RT ? p.g32 != nullptr : (OUTS & kOutG32) != 0;
     const bool w_u8 = RT ? p.u8 != nullptr : (OUTS & kOutU8) != 0;
@@ -240,7 +243,27 @@ __global__ void __launch_bounds__(kCtaThreads, OUTS == kOutU8 ? SOBEL5_U8_MIN_CT
                     for (int j = 0; j < 4; ++j)
                         u[j] = u8_norm ? u8_normalize_s(S[j], s_thr, n_lo, n_scale) : u8_from_s(S[j]);
                 }
-                if (full) {
+                if constexpr (N16) {
+                    auto st16 = [&](int32_t* plane, const int32_t (&v)[4]) {
+                        int16_t* q = reinterpret_cast<int16_t*>(plane) + row_off;
+                        if (full) {
+                            st_wb_v2u(q, __byte_perm(v[0], v[1], 0x5410), __byte_perm(v[2], v[3], 0x5410));
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                if (x0 + j < p.out_w) q[j] = static_cast<int16_t>(v[j]);
+                        }
+                    };
+                    st16(p.gx, gx);
+                    st16(p.gy, gy);
+                    if (full) {
+                        st_cs_v4d(p.g + row_off, g[0], g[1], g[2], g[3]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (x0 + j < p.out_w) p.g[row_off + j] = g[j];
+                    }
+                } else if (full) {
                     if (w_gx) st_cs_v4(p.gx + row_off, gx[0], gx[1], gx[2], gx[3]);
                     if (w_gy) st_cs_v4(p.gy + row_off, gy[0], gy[1], gy[2], gy[3]);
                     if (w_g) st_cs_v4d(p.g + row_off, g[0], g[1], g[2], g[3]);

@@ -143,6 +143,7 @@ struct sobel5_ctx {
     // planes are one contiguous block (device and staging), moved by ONE
     // copy per chunk instead of four; wire_pitch = their row pitch (elements)
     bool wire_cm = false;
+    int wire_np = 4;  // int16 planes on the wire: slots 0..wire_np-1 (4: 5x5, 2: 3x3 gx gy)
     int64_t wire_pitch = 0;
     void* d_wire = nullptr;
     size_t d_wire_bytes = 0;
@@ -174,7 +175,7 @@ cudaError_t reset_diag(sobel5_ctx* ctx) {
 }
 
 // bytes per element of plane slot i as it crosses PCIe in the current call
-size_t wire_elem(const sobel5_ctx* ctx, int i) { return ctx->wire && i < 4 ? 2 : kElem[i]; }
+size_t wire_elem(const sobel5_ctx* ctx, int i) { return ctx->wire && i < ctx->wire_np ? 2 : kElem[i]; }
 
 // The int16 wire applies to a 5x5 call with exactly the StreamResult planes
 // and default taps (sobel5_b200::n16_wire_ok), if its int16 staging fits.
@@ -182,7 +183,13 @@ size_t wire_elem(const sobel5_ctx* ctx, int i) { return ctx->wire && i < 4 ? 2 :
 // chunk into freshly allocated planes) uses it too, with 8 row chunks
 // (8K run_stream 48.2-50.6 vs 53.4-54.5 ms without the wire; 16 chunks
 // cost it ~10 ms of per-chunk synchronisation: profiles/r2/cpp_wire.txt).
+// The 3x3 operator's Stream3Result (gx, gy, g; |gx|, |gy| <= 1020) rides it
+// the same way with two int16 planes.
 bool want_wire(unsigned mask, const sobel5_taps* taps, int op, bool /*split*/) {
+    if (op == 3) {
+        const char* v = std::getenv("SOBEL5_WIRE16");
+        return mask == 0x13u && !(v && *v && std::atoi(v) == 0);
+    }
     return op == 5 && mask == 0x1fu && sobel5_b200::n16_wire_ok(taps);
 }
 
@@ -336,6 +343,8 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
     const int R = op == 3 ? 1 : 2;  // operator radius
     ctx->wire = wire;
     ctx->wire_cm = wire && chunk_major;
+    ctx->wire_np = op == 3 ? 2 : 4;
+    const int np = ctx->wire_np;
     const int out_w = width - 2 * R, out_h = height - 2 * R;
     const int64_t in_pitch = round_up(width, 128);
     const int64_t dpitch = round_up(out_w, 32);  // elements; 128 B-aligned int rows
@@ -356,10 +365,10 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
     for (int i = 0; i < 7; ++i) {
         if (!((mask >> i) & 1u)) continue;
         const size_t plane_bytes = static_cast<size_t>(out_w) * out_h * wire_elem(ctx, i);
-        if (ctx->wire_cm && i < 4) {
-            // block of the four int16 planes, padded rows (dpitch); the
+        if (ctx->wire_cm && i < np) {
+            // block of the np int16 planes, padded rows (dpitch); the
             // per-chunk plane pointers are set at the launches
-            const size_t wb = 4 * static_cast<size_t>(dpitch) * out_h * 2;
+            const size_t wb = np * static_cast<size_t>(dpitch) * out_h * 2;
             CK(ensure(&ctx->d_wire, &ctx->d_wire_bytes, wb));
             CK(ensure_host(&ctx->h_wire[0], &ctx->h_wire_bytes[0], wb));
             *dslots[i] = ctx->d_wire;
@@ -369,7 +378,7 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
         CK(ensure(&ctx->d_plane[i], &ctx->d_plane_bytes[i],
                   static_cast<size_t>(dpitch) * out_h * kElem[i]));
         *dslots[i] = ctx->d_plane[i];
-        if (wire && i < 4) {
+        if (wire && i < np) {
             CK(ensure_host(&ctx->h_wire[i], &ctx->h_wire_bytes[i], plane_bytes));
             hdst[i] = ctx->h_wire[i];
         } else if (dst[i]) {
@@ -414,12 +423,14 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
         const int64_t off_g = wire ? off / 2 : off;
         if (ctx->wire_cm) {
             // chunk k's block: plane p at (4 k chunk + p (y1 - y0)) rows
-            int16_t* blk = static_cast<int16_t*>(ctx->d_wire) + 4 * static_cast<int64_t>(y0) * dpitch;
+            int16_t* blk = static_cast<int16_t*>(ctx->d_wire) + np * static_cast<int64_t>(y0) * dpitch;
             const int64_t ps = static_cast<int64_t>(y1 - y0) * dpitch;
             sub.gx = reinterpret_cast<int32_t*>(blk);
             sub.gy = reinterpret_cast<int32_t*>(blk + ps);
-            sub.gd = reinterpret_cast<int32_t*>(blk + 2 * ps);
-            sub.gdt = reinterpret_cast<int32_t*>(blk + 3 * ps);
+            if (np == 4) {
+                sub.gd = reinterpret_cast<int32_t*>(blk + 2 * ps);
+                sub.gdt = reinterpret_cast<int32_t*>(blk + 3 * ps);
+            }
         } else {
             if (sub.gx) sub.gx += off_g;
             if (sub.gy) sub.gy += off_g;
@@ -433,8 +444,8 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
         sobel5_b200::LaunchExtra ex;
         ex.n16 = wire ? 1 : 0;
         const sobel5_status st =
-            op == 3 ? sobel3_launch(d_rows, in_pitch, 0, width, y1 - y0 + 2, 1, prefetch, 0, &sub, 0,
-                                    ctx->s_comp)
+            op == 3 ? sobel5_b200::sobel3_common(d_rows, in_pitch, 0, width, y1 - y0 + 2, 1, prefetch,
+                                                 &sub, 0, ctx->s_comp, ex)
                     : sobel5_b200::launch_common(nullptr, d_rows, nullptr, in_pitch, 0, width,
                                                  y1 - y0 + 4, 1, taps, prefetch, &sub, 0,
                                                  ctx->d_diag, ctx->s_comp, ex);
@@ -445,15 +456,15 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
         CK(cudaEventRecord(ctx->ev_comp[k], ctx->s_comp));
         CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_comp[k], 0));
         if (ctx->wire_cm) {  // the four int16 planes of the chunk: one copy
-            const size_t off = 4 * static_cast<size_t>(y0) * dpitch * 2;
-            const size_t n = 4 * static_cast<size_t>(y1 - y0) * dpitch * 2;
+            const size_t off = np * static_cast<size_t>(y0) * dpitch * 2;
+            const size_t n = np * static_cast<size_t>(y1 - y0) * dpitch * 2;
             ctx->last_d2h += n;
             CK(cudaMemcpyAsync(static_cast<char*>(ctx->h_wire[0]) + off,
                                static_cast<const char*>(ctx->d_wire) + off, n,
                                cudaMemcpyDeviceToHost, ctx->s_d2h));
         }
         for (int i = 0; i < 7; ++i) {
-            if (!hdst[i] || (ctx->wire_cm && i < 4)) continue;
+            if (!hdst[i] || (ctx->wire_cm && i < np)) continue;
             const size_t es = wire_elem(ctx, i);
             ctx->last_d2h += static_cast<uint64_t>(out_w) * es * static_cast<uint64_t>(y1 - y0);
             CK(cudaMemcpy2DAsync(static_cast<char*>(hdst[i]) + static_cast<size_t>(y0) * out_w * es,
@@ -496,8 +507,9 @@ sobel5_status drain_stream(sobel5_ctx* ctx, int out_w, int out_h, int chunk, int
             // rows of the chunk's four int16 planes, ~1 MiB of output per piece
             const int64_t dp = ctx->wire_pitch, rows = y1 - y0;
             const int per = std::max<int64_t>(1, (int64_t{1} << 18) / std::max(out_w, 1));
-            const int16_t* blk = static_cast<const int16_t*>(ctx->h_wire[0]) + 4 * static_cast<int64_t>(y0) * dp;
-            for (int i = 0; i < 4; ++i) {
+            const int np = ctx->wire_np;
+            const int16_t* blk = static_cast<const int16_t*>(ctx->h_wire[0]) + np * static_cast<int64_t>(y0) * dp;
+            for (int i = 0; i < np; ++i) {
                 if (!stage_dst[i]) continue;
                 for (int64_t r = 0; r < rows; r += per)
                     pieces.push_back({static_cast<char*>(stage_dst[i]) +
@@ -507,8 +519,8 @@ sobel5_status drain_stream(sobel5_ctx* ctx, int out_w, int out_h, int chunk, int
             }
         }
         for (int i = 0; i < 7; ++i) {
-            if (!stage_dst[i] || (ctx->wire_cm && i < 4)) continue;
-            const bool widen = ctx->wire && i < 4;
+            if (!stage_dst[i] || (ctx->wire_cm && i < ctx->wire_np)) continue;
+            const bool widen = ctx->wire && i < ctx->wire_np;
             const size_t es = wire_elem(ctx, i), row = static_cast<size_t>(out_w) * es;
             const size_t off = static_cast<size_t>(y0) * row, n = static_cast<size_t>(y1 - y0) * row;
             const char* src = static_cast<const char*>(widen ? ctx->h_wire[i] : ctx->h_stage[i]);
@@ -689,7 +701,7 @@ sobel5_status begin_common(sobel5_ctx* ctx, const uint8_t* h_in, int width, int 
     for (int i = 0; i < 7; ++i)
         if ((plane_mask >> i) & 1u)
             stage_bytes += static_cast<size_t>(width - 2 * R) * (height - 2 * R) *
-                           (wire && i < 4 ? 2 : kElem[i]);
+                           (wire && i < (op == 3 ? 2 : 4) ? 2 : kElem[i]);
     StageBudget budget;  // the planes must fit; the input is staged if it still does
     if (!budget.take(stage_bytes)) return SOBEL5_OUT_OF_MEMORY;  // callers use run_host
     CK(cudaSetDevice(ctx->device));
@@ -864,12 +876,20 @@ sobel5_status sobel3_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     void* hp[7];
     planes_array(h_out, hp);
     unsigned mask = 0;
+    for (int i = 0; i < 7; ++i)
+        if (hp[i]) mask |= 1u << i;
     void* direct[7] = {};
     void* staged[7] = {};
     StageBudget budget;
+    // gx, gy over the int16 wire (chunk-major), widened into the caller's planes
+    const bool wire = want_wire(mask, nullptr, 3, false) &&
+                      budget.take(2 * static_cast<size_t>(round_up(out_w, 32)) * out_h * 2);
     for (int i = 0; i < 7; ++i) {
         if (!hp[i]) continue;
-        mask |= 1u << i;
+        if (wire && i < 2) {
+            staged[i] = hp[i];
+            continue;
+        }
         if (!is_pinned(hp[i]) && budget.take(static_cast<size_t>(out_w) * out_h * kElem[i]))
             staged[i] = hp[i];
         else
@@ -878,7 +898,7 @@ sobel5_status sobel3_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     if (!mask) return SOBEL5_OK;
     int chunk = 0, n_chunks = 0;
     const sobel5_status st = enqueue_stream(ctx, h_in, width, height, nullptr, prefetch, mask,
-                                            direct, &chunk, &n_chunks, budget, 3);
+                                            direct, &chunk, &n_chunks, budget, 3, wire, true);
     if (st != SOBEL5_OK) return st;
     return drain_stream(ctx, out_w, out_h, chunk, n_chunks, staged, nullptr);
 }

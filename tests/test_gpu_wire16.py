@@ -153,3 +153,32 @@ def test_split_form_finish_widens(ctx, oracle, monkeypatch):
     assert L.sobel5_run_host_finish(ctx.handle, C.byref(planes_struct(res, w - 4)), C.byref(d)) == 0
     for k in PLANES:
         np.testing.assert_array_equal(res[k], ref[k], err_msg=k)
+
+
+@pytest.mark.parametrize("wire", ["1", "0"])
+@pytest.mark.parametrize("h,w", [(3, 3), (61, 97), (2300, 1027), (700, 4099)])
+def test_sobel3_run_host_wire(ctx, oracle, monkeypatch, wire, h, w):
+    """run_stream_3x3's host path: gx, gy over the int16 wire (|gx|, |gy| <=
+    1020), widened into the caller's int32 planes; g as f64."""
+    import torch
+    from paper_2305_00515_b200 import _abi
+    monkeypatch.setenv("SOBEL5_WIRE16", wire)
+    L = _abi.load()
+    img = np.random.default_rng(h + 7 * w).integers(0, 256, (h, w), dtype=np.uint8)
+    if h > 100:
+        img[: h // 2] = extreme_image(h // 2, w)[:, :w]
+    st, ref = oracle.sobel3_2d(img)
+    assert st == 0
+    ow, oh = w - 2, h - 2
+    for pinned in (False, True):
+        res = {k: np.full((oh, ow), 7, DT[k]) for k in ("gx", "gy", "g")}
+        if pinned:
+            res = {k: torch.from_numpy(v).pin_memory() for k, v in res.items()}
+        assert L.sobel3_run_host(ctx.handle, img.ctypes.data, w, h, 1,
+                                 C.byref(planes_struct(res, ow))) == 0
+        for k in ("gx", "gy", "g"):
+            got = res[k].numpy() if pinned else res[k]
+            np.testing.assert_array_equal(got, ref[k], err_msg=f"{k} pinned={pinned} wire={wire}")
+        dp = (ow + 31) // 32 * 32
+        want = 2 * dp * oh * 2 + ow * oh * 8 if wire == "1" else ow * oh * 16
+        assert L.sobel5_ctx_last_d2h_bytes(ctx.handle) == want
