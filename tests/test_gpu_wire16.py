@@ -45,7 +45,8 @@ def extreme_image(h, w):
 
 
 @pytest.mark.parametrize("wire", ["1", "0"])
-@pytest.mark.parametrize("h,w,kind", [(61, 97, "rand"), (300, 1031, "extreme"),
+@pytest.mark.parametrize("h,w,kind", [(5, 5, "rand"), (6, 9, "rand"), (300, 5, "rand"),
+                                      (61, 97, "rand"), (300, 1031, "extreme"),
                                       (4400, 1027, "rand"), (2100, 4099, "extreme")])
 def test_run_host_sr_wire(ctx, oracle, monkeypatch, wire, h, w, kind):
     import torch
