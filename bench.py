@@ -88,7 +88,13 @@ def base_config(a, world: int) -> dict:
             "contract": a.contract + " (" + "+".join(CONTRACT_PLANES[a.contract]) + ")",
             "prefetch": bool(a.prefetch),
             "parallelism": (f"row-bands x{world} ({a.transport} halos)"
-                            if a.workload == "32k-bands" else f"batch-split x{world}")}
+                            if a.workload == "32k-bands" else f"batch-split x{world}"),
+            # L2 policy of the GPU timing (126 MB L2): no L2 flush; every step
+            # reads an input larger than L2 or rotates inputs over > 2x L2, and
+            # writes outputs far larger than L2
+            "l2": ("inputs larger than L2: each rank's 32768-wide band (>= 128 MB) read "
+                   "once per step, outputs >= 3.2 GB per step" if a.workload == "32k-bands"
+                   else "inputs rotated over >= 2 x L2 of frames (no L2 flush)")}
 
 
 def dist_env():
