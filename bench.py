@@ -734,6 +734,61 @@ def main():
                        "; every rank one image, max time over ranks"}
         ctx.close()
 
+    elif not a.no_e2e and frames > 1:
+        # C4 end to end: the rank's frames from pinned host memory through
+        # sobel5_run_host_frames (the frame-stream call: run_stream per frame,
+        # pipelined across frames), 32 frames per call into one pinned
+        # 32-frame output set; wall clock, max over ranks, whole-job frames
+        import ctypes as C
+        ctx = api.Context(local)
+        h_in = torch.empty((frames, h, w), dtype=torch.uint8, pin_memory=True)
+        d0 = ins[0]
+        for f_ in range(frames):
+            h_in[f_].copy_(d0[f_][:, :w].cpu())
+        group = min(32, frames)
+        dt = {"gx": torch.int32, "gy": torch.int32, "gd": torch.int32, "gdt": torch.int32,
+              "g": torch.float64, "g32": torch.float32, "u8": torch.uint8}
+        ho = {k: torch.empty((group, oh, ow), dtype=dt[k], pin_memory=True) for k in planes_names}
+        pl = _abi.Planes(pitch=ow)
+        for k, v in ho.items():
+            setattr(pl, k, v.data_ptr())
+        diag = _abi.Diag()
+        L = _abi.load()
+
+        def e2e_frames():
+            d2h = 0
+            for f0 in range(0, frames, group):
+                n = min(group, frames - f0)
+                st = L.sobel5_run_host_frames(ctx.handle, h_in[f0].data_ptr(), w, h, n, w * h,
+                                              C.byref(taps), a.prefetch, C.byref(pl), ow * oh,
+                                              C.byref(diag))
+                api.check(st, "sobel5_run_host_frames")
+                d2h += int(L.sobel5_ctx_last_d2h_bytes(ctx.handle))
+            return d2h
+
+        e2e_frames()
+        n_e2e = 2
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            d2h = e2e_frames()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device="cpu" if a.share_gpu else dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        s_e2e = el / n_e2e
+        result = sum(v[0].numel() * v.element_size() for v in ho.values()) * frames
+        e2e = {"value": world * frames * w * h / s_e2e / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": world * frames * w * h,
+               "d2h_bytes_per_step": world * d2h, "result_bytes_per_step": world * result,
+               "ms_per_step": s_e2e * 1e3, "steps": n_e2e, "ranks": world,
+               "path": f"sobel5_run_host_frames (C ABI) over the rank's {frames} frames, "
+                       f"{group} frames per call, pinned input frames and output set, "
+                       "int16 wire for gx..gdt; max time over ranks"}
+        ctx.close()
+
     elif not a.no_e2e and a.workload == "32k-bands":
         # C5 end to end, every rank at once over its own PCIe link: its band's
         # input rows from pinned host memory, the band step (halo exchange

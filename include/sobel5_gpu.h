@@ -323,6 +323,17 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
  * per context (env SOBEL5_STAGING_MAX_MB, default 4096): beyond it
  * sobel5_run_host downloads straight into pageable memory and _begin
  * returns SOBEL5_OUT_OF_MEMORY (use sobel5_run_host). */
+/* A stream of n_frames W x H frames end to end (run_stream per frame,
+ * pipelined across frames: frame f+1's upload and kernel overlap frame f's
+ * download and host-side widening; 4 units in flight).  h_in: frame f at
+ * h_in + f * in_frame_stride bytes (>= W*H, tightly packed rows); h_out:
+ * planes with pitch W-4, frame f at + f * out_frame_stride elements
+ * (>= (W-4)*(H-4)).  Same plane rules, wire and errors as sobel5_run_host;
+ * diag_out covers every frame. */
+sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
+                                     int n_frames, int64_t in_frame_stride, const sobel5_taps* taps,
+                                     int prefetch, const sobel5_planes* h_out,
+                                     int64_t out_frame_stride, sobel5_diag* diag_out);
 sobel5_status sobel5_run_host_begin(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
                                     const sobel5_taps* taps, int prefetch, unsigned plane_mask);
 sobel5_status sobel5_run_host_finish(sobel5_ctx* ctx, const sobel5_planes* h_out,

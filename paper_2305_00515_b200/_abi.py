@@ -99,7 +99,7 @@ EXPORTS = (
     "sobel5_run_host_chunk", "sobel5_run_host_staging", "sobel5_run_host_staging_elem",
     "sobel5_kernel_for_taps",
     "sobel3_run_host_begin", "sobel5_ctx_trim", "sobel5_last_launch",
-    "sobel5_ctx_set_strip_width", "sobel5_ctx_last_d2h_bytes",
+    "sobel5_ctx_set_strip_width", "sobel5_ctx_last_d2h_bytes", "sobel5_run_host_frames",
     "sobel5_conv2d_valid", "sobel5_conv2d_valid_host", "sobel5_dense_4d", "sobel5_dense_4d_host",
     "sobel5_mgpu_create", "sobel5_mgpu_destroy", "sobel5_mgpu_band", "sobel5_mgpu_upload",
     "sobel5_mgpu_synth", "sobel5_mgpu_run_bands", "sobel5_mgpu_sync", "sobel5_mgpu_run_host", "sobel5_mgpu_last_diag",
@@ -201,6 +201,9 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.sobel5_ctx_set_strip_width.restype = i32
     L.sobel5_ctx_last_d2h_bytes.argtypes = [vp]
     L.sobel5_ctx_last_d2h_bytes.restype = C.c_uint64
+    L.sobel5_run_host_frames.argtypes = [vp, vp, i32, i32, i32, C.c_int64, C.POINTER(Taps), i32,
+                                         C.POINTER(Planes), C.c_int64, vp]
+    L.sobel5_run_host_frames.restype = i32
     L.sobel3_run_host_begin.argtypes = [vp, vp, i32, i32, i32, C.c_uint32]
     L.sobel3_run_host_begin.restype = i32
     L.sobel5_kernel_for_taps.argtypes = [C.POINTER(Taps)]

@@ -147,6 +147,15 @@ struct sobel5_ctx {
     int64_t wire_pitch = 0;
     void* d_wire = nullptr;
     size_t d_wire_bytes = 0;
+    // sobel5_run_host_frames: a ring of kFrameSlots units (frame row chunks)
+    // in flight -- device input / output slots, pinned staging slots, events
+    void* f_d_in = nullptr;
+    size_t f_d_in_bytes = 0;
+    void* f_d_out = nullptr;
+    size_t f_d_out_bytes = 0;
+    void* f_h_stage = nullptr;
+    size_t f_h_stage_bytes = 0;
+    std::vector<cudaEvent_t> f_ev;
     std::vector<cudaEvent_t> ev_in, ev_comp, ev_out;
     HostPool pool;
     // state between sobel5_run_host_begin and _finish
@@ -592,6 +601,10 @@ void sobel5_ctx_destroy(sobel5_ctx* ctx) {
     for (auto ev : ctx->ev_out) cudaEventDestroy(ev);
     if (ctx->d_in) cudaFree(ctx->d_in);
     if (ctx->d_wire) cudaFree(ctx->d_wire);
+    if (ctx->f_d_in) cudaFree(ctx->f_d_in);
+    if (ctx->f_d_out) cudaFree(ctx->f_d_out);
+    if (ctx->f_h_stage) cudaFreeHost(ctx->f_h_stage);
+    for (auto ev : ctx->f_ev) cudaEventDestroy(ev);
     for (void* p : ctx->d_plane)
         if (p) cudaFree(p);
     for (void* p : ctx->h_stage)
@@ -659,6 +672,195 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     return drain_stream(ctx, out_w, out_h, chunk, n_chunks, staged, diag_out);
 }
 
+// Frames end to end (sobel5_run_host_frames): the units are row chunks of
+// the frames (one per frame up to ~4 M output px, else the row chunks of
+// sobel5_run_host), kept kFrameSlots in flight on the three streams through
+// rings of device input / output slots and pinned staging slots.  The host
+// enqueues unit u + kFrameSlots only after unit u's download has landed and
+// been widened / copied out, which is also what frees every slot it reuses,
+// so no device-side slot waits are needed.  With default taps and the five
+// StreamResult planes gx..gdt ride the int16 wire (chunk-major block per
+// unit); other pinned destinations are DMA'd straight into, pageable ones go
+// through the unit's staging slot.
+sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int width, int height,
+                                     int n_frames, int64_t in_frame_stride, const sobel5_taps* taps,
+                                     int prefetch, const sobel5_planes* h_out,
+                                     int64_t out_frame_stride, sobel5_diag* diag_out) {
+    if (!ctx) return SOBEL5_INVALID_ARG;
+    if (width < 5 || height < 5) return SOBEL5_IMAGE_TOO_SMALL;  // pipeline.hpp:454-456
+    if (!h_in || !taps || !h_out || n_frames < 1) return SOBEL5_INVALID_ARG;
+    if (ctx->pend.active) return SOBEL5_INVALID_ARG;
+    const int out_w = width - 4, out_h = height - 4;
+    const int64_t out_px = static_cast<int64_t>(out_w) * out_h;
+    if (h_out->pitch != out_w || in_frame_stride < static_cast<int64_t>(width) * height ||
+        out_frame_stride < out_px)
+        return SOBEL5_INVALID_ARG;
+    CK(cudaSetDevice(ctx->device));
+    constexpr int kFrameSlots = 4;
+    void* hp[7];
+    planes_array(h_out, hp);
+    unsigned mask = 0;
+    for (int i = 0; i < 7; ++i)
+        if (hp[i]) mask |= 1u << i;
+    if (!mask) return SOBEL5_OK;
+    const bool wire = want_wire(mask, taps, 5, false);
+    ctx->wire = false;  // (the single-call wire state is not used here)
+    const int64_t in_pitch = round_up(width, 128);
+    const int64_t dpitch = round_up(out_w, 32);
+    const int chunk = out_px <= (int64_t{4} << 20) ? out_h : std::min(out_h, std::max(256, (out_h + 15) / 16));
+    const int n_chunks = (out_h + chunk - 1) / chunk;
+    const int64_t n_units = static_cast<int64_t>(n_frames) * n_chunks;
+    // slot layouts (bytes): device [input rows][wire block | planes], host
+    // staging [wire block | pageable planes]
+    const size_t in_slot = static_cast<size_t>(in_pitch) * (chunk + 4);
+    size_t dev_off[7] = {}, host_off[7] = {}, dev_slot = 0, host_slot = 0;
+    bool pinned[7] = {};
+    const size_t wire_bytes = wire ? 4 * static_cast<size_t>(chunk) * dpitch * 2 : 0;
+    dev_slot = host_slot = wire_bytes;
+    for (int i = 0; i < 7; ++i) {
+        if (!hp[i] || (wire && i < 4)) continue;
+        dev_off[i] = dev_slot;
+        dev_slot += round_up(static_cast<int64_t>(chunk) * dpitch * kElem[i], 256);
+        pinned[i] = is_pinned(hp[i]);
+        if (!pinned[i]) {
+            host_off[i] = host_slot;
+            host_slot += round_up(static_cast<int64_t>(chunk) * out_w * kElem[i], 256);
+        }
+    }
+    dev_slot = round_up(static_cast<int64_t>(dev_slot), 256);
+    host_slot = round_up(static_cast<int64_t>(std::max<size_t>(host_slot, 256)), 256);
+    CK(ensure(&ctx->f_d_in, &ctx->f_d_in_bytes, kFrameSlots * in_slot));
+    CK(ensure(&ctx->f_d_out, &ctx->f_d_out_bytes, kFrameSlots * dev_slot));
+    CK(ensure_host(&ctx->f_h_stage, &ctx->f_h_stage_bytes, kFrameSlots * host_slot));
+    CK(ensure_events(ctx->f_ev, 3 * kFrameSlots));
+    CK(reset_diag(ctx));
+    const uint8_t* src_in = h_in;  // pageable input: the driver stages the (small) uploads
+    ctx->last_d2h = 0;
+
+    auto unit_rows = [&](int64_t u, int& f, int& y0, int& y1) {
+        f = static_cast<int>(u / n_chunks);
+        y0 = static_cast<int>(u % n_chunks) * chunk;
+        y1 = std::min(out_h, y0 + chunk);
+    };
+    auto enqueue_unit = [&](int64_t u) -> sobel5_status {
+        int f, y0, y1;
+        unit_rows(u, f, y0, y1);
+        const int slot = static_cast<int>(u % kFrameSlots), rows = y1 - y0;
+        cudaEvent_t ev_in = ctx->f_ev[3 * slot], ev_comp = ctx->f_ev[3 * slot + 1],
+                    ev_out = ctx->f_ev[3 * slot + 2];
+        uint8_t* d_in = static_cast<uint8_t*>(ctx->f_d_in) + slot * in_slot;
+        char* d_out = static_cast<char*>(ctx->f_d_out) + slot * dev_slot;
+        char* h_st = static_cast<char*>(ctx->f_h_stage) + slot * host_slot;
+        // input rows [y0, y1 + 4) of frame f
+        CK(cudaMemcpy2DAsync(d_in, in_pitch,
+                             src_in + static_cast<int64_t>(f) * in_frame_stride +
+                                 static_cast<int64_t>(y0) * width,
+                             width, width, rows + 4, cudaMemcpyHostToDevice, ctx->s_h2d));
+        CK(cudaEventRecord(ev_in, ctx->s_h2d));
+        CK(cudaStreamWaitEvent(ctx->s_comp, ev_in, 0));
+        sobel5_planes sub{};
+        sub.pitch = dpitch;
+        int32_t** islots[4] = {&sub.gx, &sub.gy, &sub.gd, &sub.gdt};
+        for (int i = 0; i < 4; ++i) {
+            if (!hp[i]) continue;
+            *islots[i] = reinterpret_cast<int32_t*>(
+                wire ? d_out + static_cast<size_t>(i) * rows * dpitch * 2 : d_out + dev_off[i]);
+        }
+        if (hp[4]) sub.g = reinterpret_cast<double*>(d_out + dev_off[4]);
+        if (hp[5]) sub.g32 = reinterpret_cast<float*>(d_out + dev_off[5]);
+        if (hp[6]) sub.u8 = reinterpret_cast<uint8_t*>(d_out + dev_off[6]);
+        sobel5_b200::LaunchExtra ex;
+        ex.n16 = wire ? 1 : 0;
+        const sobel5_status st = sobel5_b200::launch_common(nullptr, d_in, nullptr, in_pitch, 0, width,
+                                                            rows + 4, 1, taps, prefetch, &sub, 0,
+                                                            ctx->d_diag, ctx->s_comp, ex);
+        if (st != SOBEL5_OK) {
+            ctx->last_error = cudaGetErrorString(cudaGetLastError());
+            return st;
+        }
+        CK(cudaEventRecord(ev_comp, ctx->s_comp));
+        CK(cudaStreamWaitEvent(ctx->s_d2h, ev_comp, 0));
+        if (wire) {
+            const size_t n = 4 * static_cast<size_t>(rows) * dpitch * 2;
+            CK(cudaMemcpyAsync(h_st, d_out, n, cudaMemcpyDeviceToHost, ctx->s_d2h));
+            ctx->last_d2h += n;
+        }
+        for (int i = 0; i < 7; ++i) {
+            if (!hp[i] || (wire && i < 4)) continue;
+            const size_t es = kElem[i];
+            void* dst = pinned[i] ? static_cast<char*>(hp[i]) +
+                                        (static_cast<size_t>(f) * out_frame_stride +
+                                         static_cast<size_t>(y0) * out_w) * es
+                                  : h_st + host_off[i];
+            CK(cudaMemcpy2DAsync(dst, static_cast<size_t>(out_w) * es, d_out + dev_off[i],
+                                 static_cast<size_t>(dpitch) * es, static_cast<size_t>(out_w) * es,
+                                 rows, cudaMemcpyDeviceToHost, ctx->s_d2h));
+            ctx->last_d2h += static_cast<uint64_t>(rows) * out_w * es;
+        }
+        CK(cudaEventRecord(ev_out, ctx->s_d2h));
+        return SOBEL5_OK;
+    };
+    // host side of unit u: wire planes widened, staged planes copied out
+    struct Piece {
+        int plane;
+        const char* src;
+        char* dst;
+        int rows;
+    };
+    std::vector<Piece> pieces;
+    auto finish_unit = [&](int64_t u) {
+        int f, y0, y1;
+        unit_rows(u, f, y0, y1);
+        const int slot = static_cast<int>(u % kFrameSlots), rows = y1 - y0;
+        const char* h_st = static_cast<const char*>(ctx->f_h_stage) + slot * host_slot;
+        const int per = std::max(1, (1 << 18) / std::max(out_w, 1));
+        pieces.clear();
+        for (int i = 0; i < 7; ++i) {
+            if (!hp[i]) continue;
+            const bool w16 = wire && i < 4;
+            if (!w16 && pinned[i]) continue;
+            const size_t es = kElem[i];
+            char* dst = static_cast<char*>(hp[i]) +
+                        (static_cast<size_t>(f) * out_frame_stride + static_cast<size_t>(y0) * out_w) * es;
+            const char* src = w16 ? h_st + static_cast<size_t>(i) * rows * dpitch * 2 : h_st + host_off[i];
+            const size_t src_row = w16 ? static_cast<size_t>(dpitch) * 2 : static_cast<size_t>(out_w) * es;
+            for (int r = 0; r < rows; r += per)
+                pieces.push_back({i, src + r * src_row, dst + static_cast<size_t>(r) * out_w * es,
+                                  std::min(per, rows - r)});
+        }
+        auto move = [&](const Piece& q) {
+            const bool w16 = wire && q.plane < 4;
+            if (w16) {
+                for (int r = 0; r < q.rows; ++r)
+                    sobel5_b200::widen_i16(reinterpret_cast<int32_t*>(q.dst) + static_cast<size_t>(r) * out_w,
+                                           reinterpret_cast<const int16_t*>(q.src) + static_cast<size_t>(r) * dpitch,
+                                           static_cast<size_t>(out_w));
+            } else {
+                std::memcpy(q.dst, q.src, static_cast<size_t>(q.rows) * out_w * kElem[q.plane]);
+            }
+        };
+        if (pieces.size() == 1) move(pieces[0]);
+        else if (!pieces.empty())
+            ctx->pool.run(static_cast<int>(pieces.size()), [&](int t) { move(pieces[t]); });
+    };
+    sobel5_status st = SOBEL5_OK;
+    for (int64_t u = 0; u < std::min<int64_t>(kFrameSlots, n_units) && st == SOBEL5_OK; ++u)
+        st = enqueue_unit(u);
+    for (int64_t u = 0; u < n_units && st == SOBEL5_OK; ++u) {
+        const cudaError_t e = cudaEventSynchronize(ctx->f_ev[3 * (u % kFrameSlots) + 2]);
+        if (e != cudaSuccess) return fail(ctx, e);
+        finish_unit(u);
+        if (u + kFrameSlots < n_units) st = enqueue_unit(u + kFrameSlots);
+    }
+    CK(cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(sobel5_diag), cudaMemcpyDeviceToHost,
+                       ctx->s_d2h));
+    CK(cudaStreamSynchronize(ctx->s_d2h));
+    CK(cudaStreamSynchronize(ctx->s_comp));
+    if (st != SOBEL5_OK) return st;
+    if (diag_out) *diag_out = *ctx->h_diag;
+    return ctx->h_diag->violations ? SOBEL5_PARITY_VIOLATION : SOBEL5_OK;
+}
+
 void sobel5_ctx_trim(sobel5_ctx* ctx) {
     if (!ctx || ctx->pend.active) return;
     cudaSetDevice(ctx->device);
@@ -682,6 +884,11 @@ void sobel5_ctx_trim(sobel5_ctx* ctx) {
     if (ctx->d_wire) cudaFree(ctx->d_wire);
     ctx->d_wire = nullptr;
     ctx->d_wire_bytes = 0;
+    if (ctx->f_d_in) cudaFree(ctx->f_d_in);
+    if (ctx->f_d_out) cudaFree(ctx->f_d_out);
+    if (ctx->f_h_stage) cudaFreeHost(ctx->f_h_stage);
+    ctx->f_d_in = ctx->f_d_out = ctx->f_h_stage = nullptr;
+    ctx->f_d_in_bytes = ctx->f_d_out_bytes = ctx->f_h_stage_bytes = 0;
     if (ctx->d_in) cudaFree(ctx->d_in);
     ctx->d_in = nullptr;
     ctx->d_in_bytes = 0;
