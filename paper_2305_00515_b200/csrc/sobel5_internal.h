@@ -48,6 +48,7 @@ cudaError_t launch_packed_rt_pad(const KernelParams& kp, dim3 grid, int pf, cuda
 // TMA band rows; its own grid (W warps x 32 x 2NP columns per CTA) and band.
 struct U8Plan {
     int np = 4, warps = 4, band = 16, cta_cols = 1024;
+    bool fp = false;  // packed-FP32 arithmetic (sobel5_u8f.cuh), np 4 geometry
 };
 U8Plan u8_fast_plan(int out_w, int out_h, int frames);
 cudaError_t launch_u8_fast(const KernelParams& kp, int frames, const U8Plan& plan, cudaStream_t s);
