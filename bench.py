@@ -730,7 +730,9 @@ def main():
                "path": "sobel5_run_host (C ABI), pinned host buffers, chunked H2D/kernel/D2H "
                        "overlap on 3 streams" +
                        (f"; {'/'.join(narrow)} cross PCIe as int16 and are sign-extended into "
-                        "the int32 result planes by the host pool" if narrow else "") +
+                        "the int32 result planes by the host pool" +
+                        (", which rebuilds g from them (exact; g does not cross PCIe)"
+                         if d2h < result // 2 else "") if narrow else "") +
                        "; every rank one image, max time over ranks"}
         ctx.close()
 

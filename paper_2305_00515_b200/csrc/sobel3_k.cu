@@ -29,6 +29,7 @@ cudaError_t outs(const KernelParams& kp, dim3 grid, cudaStream_t s) {
     switch (packed_out_set(kp)) {
         case kOut3: return go<PF, PAD, kOut3>(kp, grid, s);
         case kOut3 | kOutN16: return go<PF, PAD, kOut3 | kOutN16>(kp, grid, s);
+        case kOutGx | kOutGy | kOutN16: return go<PF, PAD, kOutGx | kOutGy | kOutN16>(kp, grid, s);
         case kOutU8: return go<PF, PAD, kOutU8>(kp, grid, s);
         case kOutMinMax: return go<PF, PAD, kOutMinMax>(kp, grid, s);
         case kOutMinMax | kOutS32: return go<PF, PAD, kOutMinMax | kOutS32>(kp, grid, s);
@@ -58,9 +59,9 @@ sobel5_status sobel3_common(const uint8_t* d_in, int64_t in_pitch, int64_t in_fr
     const int out_h = ex.pad ? height : height - 2;
     if (sobel5_status st = check_planes(out, out_w); st != SOBEL5_OK) return st;
     if (out->gd || out->gdt) return SOBEL5_INVALID_ARG;  // the 3x3 operator has no diagonals
-    if (ex.n16 && (ex.pad || !out->gx || !out->gy || !out->g || out->g32 || out->u8 || ex.minmax ||
+    if (ex.n16 && (ex.pad || !out->gx || !out->gy || out->g32 || out->u8 || ex.minmax ||
                    ex.norm || ex.u8_norm || ex.s32))
-        return SOBEL5_INVALID_ARG;  // the int16 wire: exactly the Stream3Result, valid mode
+        return SOBEL5_INVALID_ARG;  // the int16 wire: gx, gy (+ g), valid mode
     if (ex.u8_norm && (!ex.norm || !out->u8)) return SOBEL5_INVALID_ARG;
 
     KernelParams kp{};

@@ -256,12 +256,14 @@ __global__ void __launch_bounds__(kCtaThreads, OUTS == kOutU8 ? SOBEL5_U8_MIN_CT
                     };
                     st16(p.gx, gx);
                     st16(p.gy, gy);
-                    if (full) {
-                        st_cs_v4d(p.g + row_off, g[0], g[1], g[2], g[3]);
-                    } else {
+                    if (w_g) {  // (without g: the host rebuilds it from the wire)
+                        if (full) {
+                            st_cs_v4d(p.g + row_off, g[0], g[1], g[2], g[3]);
+                        } else {
 #pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            if (x0 + j < p.out_w) p.g[row_off + j] = g[j];
+                            for (int j = 0; j < 4; ++j)
+                                if (x0 + j < p.out_w) p.g[row_off + j] = g[j];
+                        }
                     }
                 } else if (full) {
                     if (w_gx) st_cs_v4(p.gx + row_off, gx[0], gx[1], gx[2], gx[3]);

@@ -307,7 +307,7 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     if (ex.s32 && !taps_packed(taps)) return SOBEL5_INVALID_ARG;
     if (rows > (int64_t{1} << 30) || frames > 65535) return SOBEL5_INVALID_ARG;
     if (ex.n16 && (top || bot || ex.pad || !n16_wire_ok(taps) || !out->gx || !out->gy ||
-                   !out->gd || !out->gdt || !out->g || out->g32 || out->u8 || ex.minmax ||
+                   !out->gd || !out->gdt || out->g32 || out->u8 || ex.minmax ||
                    ex.norm || ex.u8_norm || ex.s32))
         return SOBEL5_INVALID_ARG;
 

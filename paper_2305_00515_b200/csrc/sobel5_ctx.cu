@@ -144,6 +144,9 @@ struct sobel5_ctx {
     // copy per chunk instead of four; wire_pitch = their row pitch (elements)
     bool wire_cm = false;
     int wire_np = 4;  // int16 planes on the wire: slots 0..wire_np-1 (4: 5x5, 2: 3x3 gx gy)
+    // g is not on the chunk-major wire: the host rebuilds it from the int16
+    // rows while widening them (sobel5_wire.cpp; SOBEL5_WIRE_G=0 ships it)
+    bool wire_g = false;
     int64_t wire_pitch = 0;
     void* d_wire = nullptr;
     size_t d_wire_bytes = 0;
@@ -194,6 +197,35 @@ size_t wire_elem(const sobel5_ctx* ctx, int i) { return ctx->wire && i < ctx->wi
 // cost it ~10 ms of per-chunk synchronisation: profiles/r2/cpp_wire.txt).
 // The 3x3 operator's Stream3Result (gx, gy, g; |gx|, |gy| <= 1020) rides it
 // the same way with two int16 planes.
+bool want_wire(unsigned mask, const sobel5_taps* taps, int op, bool /*split*/);
+
+// With the chunk-major wire, g (a function of the int16 gradients alone) is
+// rebuilt on the host unless SOBEL5_WIRE_G=0: 8 instead of 16 B/px over PCIe
+// for the 5x5 StreamResult, 4 instead of 12 for the 3x3 one.
+bool want_host_g() {
+    const char* v = std::getenv("SOBEL5_WIRE_G");
+    return !(v && *v && std::atoi(v) == 0);
+}
+
+// Rows [r0, r0 + rows) of one chunk-major wire block (plane p's row r at
+// src + (p * plane_rows + r) * spitch): widened into the int32 planes dst[p]
+// (rows of out_w, nullptr = not wanted) and, with g, the magnitude rebuilt.
+void decode_wire_rows(void* const dst[7], const int16_t* src, int np, int64_t plane_rows,
+                      int64_t spitch, int out_w, int64_t r0, int64_t rows, bool with_g) {
+    for (int64_t r = r0; r < r0 + rows; ++r) {
+        const int16_t* row[4] = {};
+        for (int p = 0; p < np; ++p) {
+            row[p] = src + (p * plane_rows + r) * spitch;
+            if (dst[p])
+                sobel5_b200::widen_i16(static_cast<int32_t*>(dst[p]) + r * out_w, row[p],
+                                       static_cast<size_t>(out_w));
+        }
+        if (with_g)
+            sobel5_b200::magnitude_i16(static_cast<double*>(dst[4]) + r * out_w, row, np,
+                                       static_cast<size_t>(out_w));
+    }
+}
+
 bool want_wire(unsigned mask, const sobel5_taps* taps, int op, bool /*split*/) {
     if (op == 3) {
         const char* v = std::getenv("SOBEL5_WIRE16");
@@ -348,10 +380,11 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
                              const sobel5_taps* taps, int prefetch, unsigned mask,
                              void* const dst[7], int* chunk_out, int* n_chunks_out,
                              StageBudget& budget, int op = 5, bool wire = false,
-                             bool chunk_major = false) {
+                             bool chunk_major = false, bool host_g = false) {
     const int R = op == 3 ? 1 : 2;  // operator radius
     ctx->wire = wire;
     ctx->wire_cm = wire && chunk_major;
+    ctx->wire_g = ctx->wire_cm && host_g && ((mask >> 4) & 1u);
     ctx->wire_np = op == 3 ? 2 : 4;
     const int np = ctx->wire_np;
     const int out_w = width - 2 * R, out_h = height - 2 * R;
@@ -372,7 +405,7 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
                         reinterpret_cast<void**>(&dp.u8)};
     void* hdst[7] = {};
     for (int i = 0; i < 7; ++i) {
-        if (!((mask >> i) & 1u)) continue;
+        if (!((mask >> i) & 1u) || (i == 4 && ctx->wire_g)) continue;
         const size_t plane_bytes = static_cast<size_t>(out_w) * out_h * wire_elem(ctx, i);
         if (ctx->wire_cm && i < np) {
             // block of the np int16 planes, padded rows (dpitch); the
@@ -512,7 +545,28 @@ sobel5_status drain_stream(sobel5_ctx* ctx, int out_w, int out_h, int chunk, int
         CK(cudaEventSynchronize(ctx->ev_out[k]));
         const int y0 = k * chunk, y1 = std::min(out_h, y0 + chunk);
         pieces.clear();
-        if (ctx->wire_cm) {
+        if (ctx->wire_g) {
+            // rows of the chunk's int16 planes widened + g rebuilt, ~1 MiB of
+            // output per piece
+            const int64_t dp = ctx->wire_pitch, rows = y1 - y0;
+            const int np = ctx->wire_np;
+            const int per = std::max<int64_t>(
+                1, (int64_t{1} << 20) / (std::max(out_w, 1) * int64_t{4 * np + 8}));
+            const int n_pieces = static_cast<int>((rows + per - 1) / per);
+            const int16_t* blk = static_cast<const int16_t*>(ctx->h_wire[0]) + np * static_cast<int64_t>(y0) * dp;
+            void* dst[7] = {};
+            for (int i = 0; i < 7; ++i)
+                if (stage_dst[i] && (i < np || i == 4))
+                    dst[i] = static_cast<char*>(stage_dst[i]) +
+                             static_cast<size_t>(y0) * out_w * kElem[i];
+            auto dec = [&](int t) {
+                const int64_t r0 = static_cast<int64_t>(t) * per;
+                decode_wire_rows(dst, blk, np, rows, dp, out_w, r0, std::min<int64_t>(per, rows - r0),
+                                 dst[4] != nullptr);
+            };
+            if (n_pieces == 1) dec(0);
+            else ctx->pool.run(n_pieces, dec);
+        } else if (ctx->wire_cm) {
             // rows of the chunk's four int16 planes, ~1 MiB of output per piece
             const int64_t dp = ctx->wire_pitch, rows = y1 - y0;
             const int per = std::max<int64_t>(1, (int64_t{1} << 18) / std::max(out_w, 1));
@@ -528,7 +582,8 @@ sobel5_status drain_stream(sobel5_ctx* ctx, int out_w, int out_h, int chunk, int
             }
         }
         for (int i = 0; i < 7; ++i) {
-            if (!stage_dst[i] || (ctx->wire_cm && i < ctx->wire_np)) continue;
+            if (!stage_dst[i] || (ctx->wire_cm && i < ctx->wire_np) || (i == 4 && ctx->wire_g))
+                continue;
             const bool widen = ctx->wire && i < ctx->wire_np;
             const size_t es = wire_elem(ctx, i), row = static_cast<size_t>(out_w) * es;
             const size_t off = static_cast<size_t>(y0) * row, n = static_cast<size_t>(y1 - y0) * row;
@@ -654,10 +709,11 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     const size_t n_px = static_cast<size_t>(out_w) * out_h;
     const bool wire = want_wire(mask, taps, 5, false) &&
                       budget.take(4 * static_cast<size_t>(round_up(out_w, 32)) * out_h * 2);
+    const bool host_g = wire && want_host_g();
     for (int i = 0; i < 7; ++i) {
         if (!hp[i]) continue;
-        if (wire && i < 4) {
-            staged[i] = hp[i];  // widened from the int16 staging into the caller's plane
+        if (wire && (i < 4 || (i == 4 && host_g))) {
+            staged[i] = hp[i];  // widened (g: rebuilt) from the int16 staging
             continue;
         }
         if (!is_pinned(hp[i]) && budget.take(n_px * kElem[i]))
@@ -667,7 +723,7 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     }
     int chunk = 0, n_chunks = 0;
     const sobel5_status st = enqueue_stream(ctx, h_in, width, height, taps, prefetch, mask, direct,
-                                            &chunk, &n_chunks, budget, 5, wire, true);
+                                            &chunk, &n_chunks, budget, 5, wire, true, host_g);
     if (st != SOBEL5_OK) return st;
     return drain_stream(ctx, out_w, out_h, chunk, n_chunks, staged, diag_out);
 }
@@ -704,6 +760,7 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
         if (hp[i]) mask |= 1u << i;
     if (!mask) return SOBEL5_OK;
     const bool wire = want_wire(mask, taps, 5, false);
+    const bool host_g = wire && want_host_g();  // g rebuilt on the host from the wire
     ctx->wire = false;  // (the single-call wire state is not used here)
     const int64_t in_pitch = round_up(width, 128);
     const int64_t dpitch = round_up(out_w, 32);
@@ -718,7 +775,7 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
     const size_t wire_bytes = wire ? 4 * static_cast<size_t>(chunk) * dpitch * 2 : 0;
     dev_slot = host_slot = wire_bytes;
     for (int i = 0; i < 7; ++i) {
-        if (!hp[i] || (wire && i < 4)) continue;
+        if (!hp[i] || (wire && i < 4) || (host_g && i == 4)) continue;
         dev_off[i] = dev_slot;
         dev_slot += round_up(static_cast<int64_t>(chunk) * dpitch * kElem[i], 256);
         pinned[i] = is_pinned(hp[i]);
@@ -766,7 +823,7 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
             *islots[i] = reinterpret_cast<int32_t*>(
                 wire ? d_out + static_cast<size_t>(i) * rows * dpitch * 2 : d_out + dev_off[i]);
         }
-        if (hp[4]) sub.g = reinterpret_cast<double*>(d_out + dev_off[4]);
+        if (hp[4] && !host_g) sub.g = reinterpret_cast<double*>(d_out + dev_off[4]);
         if (hp[5]) sub.g32 = reinterpret_cast<float*>(d_out + dev_off[5]);
         if (hp[6]) sub.u8 = reinterpret_cast<uint8_t*>(d_out + dev_off[6]);
         sobel5_b200::LaunchExtra ex;
@@ -786,7 +843,7 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
             ctx->last_d2h += n;
         }
         for (int i = 0; i < 7; ++i) {
-            if (!hp[i] || (wire && i < 4)) continue;
+            if (!hp[i] || (wire && i < 4) || (host_g && i == 4)) continue;
             const size_t es = kElem[i];
             void* dst = pinned[i] ? static_cast<char*>(hp[i]) +
                                         (static_cast<size_t>(f) * out_frame_stride +
@@ -802,7 +859,7 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
     };
     // host side of unit u: wire planes widened, staged planes copied out
     struct Piece {
-        int plane;
+        int plane;  // -1: the wire planes + g rebuilt, from row `rows` on
         const char* src;
         char* dst;
         int rows;
@@ -815,8 +872,12 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
         const char* h_st = static_cast<const char*>(ctx->f_h_stage) + slot * host_slot;
         const int per = std::max(1, (1 << 18) / std::max(out_w, 1));
         pieces.clear();
+        if (host_g) {  // gx..gdt widened and g rebuilt together, ~1 MiB of output per piece
+            const int per_g = std::max(1, (1 << 20) / (std::max(out_w, 1) * 24));
+            for (int r = 0; r < rows; r += per_g) pieces.push_back({-1, nullptr, nullptr, r});
+        }
         for (int i = 0; i < 7; ++i) {
-            if (!hp[i]) continue;
+            if (!hp[i] || (host_g && i <= 4)) continue;
             const bool w16 = wire && i < 4;
             if (!w16 && pinned[i]) continue;
             const size_t es = kElem[i];
@@ -830,7 +891,16 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
         }
         auto move = [&](const Piece& q) {
             const bool w16 = wire && q.plane < 4;
-            if (w16) {
+            if (q.plane < 0) {
+                void* dst[7] = {};
+                for (int i = 0; i < 5; ++i)
+                    dst[i] = static_cast<char*>(hp[i]) +
+                             (static_cast<size_t>(f) * out_frame_stride + static_cast<size_t>(y0) * out_w) *
+                                 kElem[i];
+                const int per_g = std::max(1, (1 << 20) / (std::max(out_w, 1) * 24));
+                decode_wire_rows(dst, reinterpret_cast<const int16_t*>(h_st), 4, rows, dpitch, out_w,
+                                 q.rows, std::min(per_g, rows - q.rows), true);
+            } else if (w16) {
                 for (int r = 0; r < q.rows; ++r)
                     sobel5_b200::widen_i16(reinterpret_cast<int32_t*>(q.dst) + static_cast<size_t>(r) * out_w,
                                            reinterpret_cast<const int16_t*>(q.src) + static_cast<size_t>(r) * dpitch,
@@ -1091,9 +1161,10 @@ sobel5_status sobel3_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     // gx, gy over the int16 wire (chunk-major), widened into the caller's planes
     const bool wire = want_wire(mask, nullptr, 3, false) &&
                       budget.take(2 * static_cast<size_t>(round_up(out_w, 32)) * out_h * 2);
+    const bool host_g = wire && want_host_g();
     for (int i = 0; i < 7; ++i) {
         if (!hp[i]) continue;
-        if (wire && i < 2) {
+        if (wire && (i < 2 || (i == 4 && host_g))) {
             staged[i] = hp[i];
             continue;
         }
@@ -1105,7 +1176,7 @@ sobel5_status sobel3_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     if (!mask) return SOBEL5_OK;
     int chunk = 0, n_chunks = 0;
     const sobel5_status st = enqueue_stream(ctx, h_in, width, height, nullptr, prefetch, mask,
-                                            direct, &chunk, &n_chunks, budget, 3, wire, true);
+                                            direct, &chunk, &n_chunks, budget, 3, wire, true, host_g);
     if (st != SOBEL5_OK) return st;
     return drain_stream(ctx, out_w, out_h, chunk, n_chunks, staged, nullptr);
 }

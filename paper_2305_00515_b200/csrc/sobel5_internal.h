@@ -48,7 +48,6 @@ cudaError_t launch_packed_rt_pad(const KernelParams& kp, dim3 grid, int pf, cuda
 // TMA band rows; its own grid (W warps x 32 x 2NP columns per CTA) and band.
 struct U8Plan {
     int np = 4, warps = 4, band = 16, cta_cols = 1024;
-    bool fp = false;  // packed-FP32 arithmetic (sobel5_u8f.cuh), np 4 geometry
 };
 U8Plan u8_fast_plan(int out_w, int out_h, int frames);
 cudaError_t launch_u8_fast(const KernelParams& kp, int frames, const U8Plan& plan, cudaStream_t s);
@@ -87,6 +86,8 @@ struct LaunchExtra {
 bool n16_wire_ok(const sobel5_taps* taps);
 // Sign-extends n int16 into int32 (sobel5_wire.cpp: AVX2 streaming stores).
 void widen_i16(int32_t* dst, const int16_t* src, size_t n);
+// g = sqrt(sum of the np int16 rows' squares), n pixels (the wire without g)
+void magnitude_i16(double* g, const int16_t* const* src, int np, size_t n);
 
 // Common launch path (validation in the reference's order, geometry, kernel
 // selection) for plain, batched, band and detect launches.

@@ -40,6 +40,7 @@ cudaError_t outs(const KernelParams& kp, dim3 grid, cudaStream_t s) {
     switch (packed_out_set(kp)) {
         case kOutSR: return go<PF, kOutSR>(kp, grid, s);
         case kOutSR | kOutN16: return go<PF, kOutSR | kOutN16>(kp, grid, s);
+        case 15 | kOutN16: return go<PF, 15 | kOutN16>(kp, grid, s);
         case kOutSR | kOutU8: return go<PF, kOutSR | kOutU8>(kp, grid, s);
         case kOutU8: return go<PF, kOutU8>(kp, grid, s);
         case 15 | kOutG32: return go<PF, 15 | kOutG32>(kp, grid, s);

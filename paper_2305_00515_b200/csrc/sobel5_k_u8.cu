@@ -6,7 +6,6 @@
 
 #include "sobel5_internal.h"
 #include "sobel5_u8.cuh"
-#include "sobel5_u8f.cuh"
 
 namespace sobel5_b200 {
 
@@ -29,16 +28,6 @@ cudaError_t go(const KernelParams& kp, int frames, cudaStream_t s) {
     if (kp.pad)
         return launch_kp(sobel5_u8_kernel<NP, true, W>, grid, G::kThreads, 0, s, kp);
     return launch_kp(sobel5_u8_kernel<NP, false, W>, grid, G::kThreads, 0, s, kp);
-}
-
-template <int W>
-cudaError_t go_f(const KernelParams& kp, int frames, cudaStream_t s) {
-    using G = U8Geom<4, W>;
-    const dim3 grid(static_cast<unsigned>((kp.out_w + G::kCtaCols - 1) / G::kCtaCols),
-                    static_cast<unsigned>((kp.out_h + kp.band - 1) / kp.band),
-                    static_cast<unsigned>(frames));
-    if (kp.pad) return launch_kp(sobel5_u8f_kernel<true, W>, grid, G::kThreads, 0, s, kp);
-    return launch_kp(sobel5_u8f_kernel<false, W>, grid, G::kThreads, 0, s, kp);
 }
 
 template <int NP>
@@ -66,7 +55,6 @@ cudaError_t go_w(const KernelParams& kp, int frames, int warps, cudaStream_t s) 
 U8Plan u8_fast_plan(int out_w, int out_h, int frames) {
     U8Plan pl;
     pl.np = env_or("SOBEL5_U8_NP", 4) == 2 ? 2 : 4;
-    pl.fp = pl.np == 4 && env_or("SOBEL5_U8F", 0) != 0;
     const int64_t px = int64_t{out_w} * out_h * frames;
     const int forced_w = env_or("SOBEL5_U8_WARPS", 0);
     pl.warps = forced_w == 1 || forced_w == 2 || forced_w == 4
@@ -79,7 +67,7 @@ U8Plan u8_fast_plan(int out_w, int out_h, int frames) {
         return pl;
     }
     const int64_t cols = (out_w + pl.cta_cols - 1) / pl.cta_cols;
-    const int64_t per_sm = (pl.fp ? 8 : pl.np == 4 ? 16 : 24) / pl.warps;  // resident CTAs per SM
+    const int64_t per_sm = (pl.np == 4 ? 16 : 24) / pl.warps;  // resident CTAs per SM
     int band = env_or("SOBEL5_U8_BAND", px >= (int64_t{96} << 20) ? 24 : 16);
     while (band > 4 && cols * frames * ((out_h + band - 1) / band) * 10 < 148 * per_sm * 9) band /= 2;
     pl.band = band;
@@ -87,13 +75,6 @@ U8Plan u8_fast_plan(int out_w, int out_h, int frames) {
 }
 
 cudaError_t launch_u8_fast(const KernelParams& kp, int frames, const U8Plan& pl, cudaStream_t s) {
-    if (pl.fp && !kp.s32) {
-        switch (pl.warps) {
-            case 1: return go_f<1>(kp, frames, s);
-            case 2: return go_f<2>(kp, frames, s);
-            default: return go_f<4>(kp, frames, s);
-        }
-    }
     return pl.np == 4 ? go_w<4>(kp, frames, pl.warps, s) : go_w<2>(kp, frames, pl.warps, s);
 }
 

@@ -8,8 +8,20 @@
 // destination planes are written once and not re-read here), scalar
 // elsewhere.  The values are copied, never computed: the result is the
 // int32 plane the device would have written.
+//
+// The magnitude plane g is a function of the four gradients alone
+// (pipeline.hpp:401-407: the left-to-right double sum of their squares, then
+// sqrt), so by default it does not cross PCIe at all (8 instead of 16 B/px):
+// the host rebuilds it from the int16 rows it is widening.  With default
+// taps every square is < 2^30 and the sum < 2^32, so each partial sum is an
+// exact double whatever the order and the IEEE square root (vsqrtpd, like
+// the device's __dsqrt_rn of the exact integer sum) gives the same bits the
+// reference computes.
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #if defined(__x86_64__) || defined(__i386__)
 #include <immintrin.h>
@@ -44,7 +56,103 @@ __attribute__((target("avx2"))) void widen_avx2(int32_t* dst, const int16_t* src
 }
 #endif
 
+void magnitude_scalar(double* g, const int16_t* const* src, int np, size_t n) {
+    for (size_t i = 0; i < n; ++i) {
+        double acc = 0.0;
+        for (int p = 0; p < np; ++p) {
+            const double v = src[p][i];
+            acc = acc + v * v;
+        }
+        g[i] = std::sqrt(acc);
+    }
+}
+
+#ifdef SOBEL5_WIRE_X86
+template <int NP>
+__attribute__((target("avx512f"))) void magnitude_avx512(double* g, const int16_t* const* src,
+                                                         size_t n) {
+    size_t i = 0;
+    // scalar head until g is 64-byte aligned (streaming stores need it)
+    for (; i < n && (reinterpret_cast<uintptr_t>(g + i) & 63u) != 0; ++i) {
+        double acc = 0.0;
+        for (int p = 0; p < NP; ++p) acc = acc + static_cast<double>(src[p][i]) * src[p][i];
+        g[i] = std::sqrt(acc);
+    }
+    for (; i + 16 <= n; i += 16) {
+        __m512d lo = _mm512_setzero_pd(), hi = _mm512_setzero_pd();
+#pragma GCC unroll 4
+        for (int p = 0; p < NP; ++p) {
+            const __m512i v = _mm512_cvtepi16_epi32(
+                _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src[p] + i)));
+            const __m512d a = _mm512_cvtepi32_pd(_mm512_castsi512_si256(v));
+            const __m512d b = _mm512_cvtepi32_pd(_mm512_extracti64x4_epi64(v, 1));
+            lo = _mm512_fmadd_pd(a, a, lo);  // exact: every partial sum < 2^53
+            hi = _mm512_fmadd_pd(b, b, hi);
+        }
+        _mm512_stream_pd(g + i, _mm512_sqrt_pd(lo));
+        _mm512_stream_pd(g + i + 8, _mm512_sqrt_pd(hi));
+    }
+    for (; i < n; ++i) {
+        double acc = 0.0;
+        for (int p = 0; p < NP; ++p) acc = acc + static_cast<double>(src[p][i]) * src[p][i];
+        g[i] = std::sqrt(acc);
+    }
+    _mm_sfence();
+}
+
+template <int NP>
+__attribute__((target("avx2,fma"))) void magnitude_avx2(double* g, const int16_t* const* src,
+                                                        size_t n) {
+    size_t i = 0;
+    for (; i < n && (reinterpret_cast<uintptr_t>(g + i) & 31u) != 0; ++i) {
+        double acc = 0.0;
+        for (int p = 0; p < NP; ++p) acc = acc + static_cast<double>(src[p][i]) * src[p][i];
+        g[i] = std::sqrt(acc);
+    }
+    for (; i + 8 <= n; i += 8) {
+        __m256d lo = _mm256_setzero_pd(), hi = _mm256_setzero_pd();
+        for (int p = 0; p < NP; ++p) {
+            const __m256i v = _mm256_cvtepi16_epi32(
+                _mm_loadu_si128(reinterpret_cast<const __m128i*>(src[p] + i)));
+            const __m256d a = _mm256_cvtepi32_pd(_mm256_castsi256_si128(v));
+            const __m256d b = _mm256_cvtepi32_pd(_mm256_extracti128_si256(v, 1));
+            lo = _mm256_fmadd_pd(a, a, lo);
+            hi = _mm256_fmadd_pd(b, b, hi);
+        }
+        _mm256_stream_pd(g + i, _mm256_sqrt_pd(lo));
+        _mm256_stream_pd(g + i + 4, _mm256_sqrt_pd(hi));
+    }
+    for (; i < n; ++i) {
+        double acc = 0.0;
+        for (int p = 0; p < NP; ++p) acc = acc + static_cast<double>(src[p][i]) * src[p][i];
+        g[i] = std::sqrt(acc);
+    }
+    _mm_sfence();
+}
+#endif
+
 }  // namespace
+
+void magnitude_i16(double* g, const int16_t* const* src, int np, size_t n) {
+#ifdef SOBEL5_WIRE_X86
+    // SOBEL5_WIRE_ISA=avx2 / scalar narrows the choice (tests)
+    static const char* isa = std::getenv("SOBEL5_WIRE_ISA");
+    static const bool narrow2 = isa && std::strcmp(isa, "avx2") == 0;
+    static const bool scalar = isa && std::strcmp(isa, "scalar") == 0;
+    static const bool avx512 = !scalar && !narrow2 && __builtin_cpu_supports("avx512f");
+    static const bool avx2 =
+        !scalar && __builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma");
+    if ((np == 2 || np == 4) && (avx512 || avx2)) {
+        if (avx512) {
+            np == 4 ? magnitude_avx512<4>(g, src, n) : magnitude_avx512<2>(g, src, n);
+        } else {
+            np == 4 ? magnitude_avx2<4>(g, src, n) : magnitude_avx2<2>(g, src, n);
+        }
+        return;
+    }
+#endif
+    magnitude_scalar(g, src, np, n);
+}
 
 void widen_i16(int32_t* dst, const int16_t* src, size_t n) {
 #ifdef SOBEL5_WIRE_X86

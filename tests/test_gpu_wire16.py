@@ -4,7 +4,9 @@ With default taps and exactly the StreamResult planes, sobel5_run_host ships
 gx, gy, gd, gdt over PCIe as int16 (every packed-kernel gradient lies in
 [-2^15, 2^15)) and widens them into the caller's int32 planes; the split
 begin/_staging form exposes the int16 staging (sobel5_run_host_staging_elem
-== 2).  Whatever the wire, the planes must equal the oracle's run_stream
+== 2).  The magnitude g does not cross PCIe on the chunk-major wire: the host
+rebuilds it from the int16 rows (wire "1"); SOBEL5_WIRE_G=0 ships it as f64
+(wire "g0").  Whatever the wire, the planes must equal the oracle's run_stream
 (pipeline.hpp:452-477) bit for bit, including the extreme gradients."""
 import ctypes as C
 
@@ -44,14 +46,15 @@ def extreme_image(h, w):
     return img
 
 
-@pytest.mark.parametrize("wire", ["1", "0"])
+@pytest.mark.parametrize("wire", ["1", "g0", "0"])
 @pytest.mark.parametrize("h,w,kind", [(5, 5, "rand"), (6, 9, "rand"), (300, 5, "rand"),
                                       (61, 97, "rand"), (300, 1031, "extreme"),
                                       (4400, 1027, "rand"), (2100, 4099, "extreme")])
 def test_run_host_sr_wire(ctx, oracle, monkeypatch, wire, h, w, kind):
     import torch
     from paper_2305_00515_b200 import _abi, api
-    monkeypatch.setenv("SOBEL5_WIRE16", wire)
+    monkeypatch.setenv("SOBEL5_WIRE16", "0" if wire == "0" else "1")
+    monkeypatch.setenv("SOBEL5_WIRE_G", "0" if wire == "g0" else "1")
     img = (np.random.default_rng(h * w).integers(0, 256, (h, w), dtype=np.uint8)
            if kind == "rand" else extreme_image(h, w))
     st, ref, _ = oracle.run_stream(img)
@@ -70,9 +73,10 @@ def test_run_host_sr_wire(ctx, oracle, monkeypatch, wire, h, w, kind):
     for k in PLANES:
         np.testing.assert_array_equal(res[k], ref[k], err_msg=f"pageable {k} wire={wire}")
     # bytes over PCIe: the four int16 planes as one block per row chunk (rows
-    # padded to 32 elements) + f64 with the wire, 4 x int32 + f64 without
+    # padded to 32 elements) (+ f64 g with SOBEL5_WIRE_G=0), 4 x int32 + f64
+    # without the wire
     dp = (ow + 31) // 32 * 32
-    want = 4 * dp * oh * 2 + ow * oh * 8 if wire == "1" else ow * oh * 24
+    want = {"1": 4 * dp * oh * 2, "g0": 4 * dp * oh * 2 + ow * oh * 8, "0": ow * oh * 24}[wire]
     assert L.sobel5_ctx_last_d2h_bytes(ctx.handle) == want
     # page-locked planes (the bench's e2e path)
     pin = {k: torch.full((oh, ow), 7, dtype=getattr(torch, np.dtype(DT[k]).name)).pin_memory()
@@ -156,14 +160,16 @@ def test_split_form_finish_widens(ctx, oracle, monkeypatch):
         np.testing.assert_array_equal(res[k], ref[k], err_msg=k)
 
 
-@pytest.mark.parametrize("wire", ["1", "0"])
+@pytest.mark.parametrize("wire", ["1", "g0", "0"])
 @pytest.mark.parametrize("h,w", [(3, 3), (61, 97), (2300, 1027), (700, 4099)])
 def test_sobel3_run_host_wire(ctx, oracle, monkeypatch, wire, h, w):
     """run_stream_3x3's host path: gx, gy over the int16 wire (|gx|, |gy| <=
-    1020), widened into the caller's int32 planes; g as f64."""
+    1020), widened into the caller's int32 planes; g rebuilt on the host (or
+    as f64 with SOBEL5_WIRE_G=0)."""
     import torch
     from paper_2305_00515_b200 import _abi
-    monkeypatch.setenv("SOBEL5_WIRE16", wire)
+    monkeypatch.setenv("SOBEL5_WIRE16", "0" if wire == "0" else "1")
+    monkeypatch.setenv("SOBEL5_WIRE_G", "0" if wire == "g0" else "1")
     L = _abi.load()
     img = np.random.default_rng(h + 7 * w).integers(0, 256, (h, w), dtype=np.uint8)
     if h > 100:
@@ -181,5 +187,5 @@ def test_sobel3_run_host_wire(ctx, oracle, monkeypatch, wire, h, w):
             got = res[k].numpy() if pinned else res[k]
             np.testing.assert_array_equal(got, ref[k], err_msg=f"{k} pinned={pinned} wire={wire}")
         dp = (ow + 31) // 32 * 32
-        want = 2 * dp * oh * 2 + ow * oh * 8 if wire == "1" else ow * oh * 16
+        want = {"1": 2 * dp * oh * 2, "g0": 2 * dp * oh * 2 + ow * oh * 8, "0": ow * oh * 16}[wire]
         assert L.sobel5_ctx_last_d2h_bytes(ctx.handle) == want
