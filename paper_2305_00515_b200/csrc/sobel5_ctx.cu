@@ -752,7 +752,12 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
         out_frame_stride < out_px)
         return SOBEL5_INVALID_ARG;
     CK(cudaSetDevice(ctx->device));
-    constexpr int kFrameSlots = 4;
+    // units in flight (SOBEL5_FRAME_SLOTS, 2..16) and row chunks per large
+    // frame (SOBEL5_FRAME_CHUNKS): experiment knobs
+    const char* sv = std::getenv("SOBEL5_FRAME_SLOTS");
+    const int kFrameSlots = sv && *sv ? std::min(16, std::max(2, std::atoi(sv))) : 4;
+    const char* cv = std::getenv("SOBEL5_FRAME_CHUNKS");
+    const int frame_chunks = cv && *cv && std::atoi(cv) > 0 ? std::atoi(cv) : 16;
     void* hp[7];
     planes_array(h_out, hp);
     unsigned mask = 0;
@@ -764,7 +769,9 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
     ctx->wire = false;  // (the single-call wire state is not used here)
     const int64_t in_pitch = round_up(width, 128);
     const int64_t dpitch = round_up(out_w, 32);
-    const int chunk = out_px <= (int64_t{4} << 20) ? out_h : std::min(out_h, std::max(256, (out_h + 15) / 16));
+    const int chunk = out_px <= (int64_t{4} << 20)
+                          ? out_h
+                          : std::min(out_h, std::max(64, (out_h + frame_chunks - 1) / frame_chunks));
     const int n_chunks = (out_h + chunk - 1) / chunk;
     const int64_t n_units = static_cast<int64_t>(n_frames) * n_chunks;
     // slot layouts (bytes): device [input rows][wire block | planes], host

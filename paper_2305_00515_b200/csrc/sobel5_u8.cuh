@@ -366,15 +366,15 @@ __device__ __forceinline__ void s32_store(uint32_t* out, const uint32_t (&u)[2 *
 // One band of one lane from shared memory: rows 0..4 wait on bar[0], row 5
 // on bar[1] (phase `par`), output rows oy0 .. oy0 + n_out - 1 at `o0`.
 // MODE 0: the clamp_abs u8 plane; MODE 1: the exact S plane (p.s32) and the
-// frame's min / max of g (p.minmax; normalize pass 1).  FULL: all 2NP
-// columns of the lane are inside the image -- the right edge's guarded
-// stores are a copy of the loop of their own, so the common loop carries no
-// per-row branch.
-template <int NP, bool PAD, int W, int MODE, bool FULL>
+// frame's min / max of g (p.minmax; normalize pass 1).  (Two copies of the
+// loop, whole lanes and right-edge lanes, drop the per-row branch but ran
+// 17-42% slower: profiles/r2/u8_split.txt.)
+template <int NP, bool PAD, int W, int MODE>
 __device__ __forceinline__ void u8_band_rows(const KernelParams& p, const uint8_t* srow,
                                              uint64_t* s_bar, uint32_t par, int x0, int64_t o0,
                                              int n_out, uint32_t& s_min, uint32_t& s_max) {
     using T = U8Band<NP, PAD, W>;
+    const bool full = x0 + U8Geom<NP, W>::kLaneCols <= p.out_w;  // all 2NP columns inside
     const int n_in = n_out + 4;
     uint8_t* out = MODE == 0 ? p.u8 + o0 : nullptr;
     uint32_t* outs = MODE == 1 ? p.s32 + o0 : nullptr;
@@ -411,17 +411,17 @@ __device__ __forceinline__ void u8_band_rows(const KernelParams& p, const uint8_
                 default: u8_step<3, NP, MODE>(h, F, D, H, aq, u); break;
             }
             if constexpr (MODE == 1) {
-                s32_store<NP>(outs, u, FULL, x0, p.out_w);
+                s32_store<NP>(outs, u, full, x0, p.out_w);
                 outs += p.pitch;
 #pragma unroll
                 for (int i = 0; i < 2 * NP; ++i) {
-                    if (FULL || x0 + i < p.out_w) {
+                    if (full || x0 + i < p.out_w) {
                         s_min = min(s_min, u[i]);
                         s_max = max(s_max, u[i]);
                     }
                 }
             } else {
-                u8_store<NP>(out, u, FULL, x0, p.out_w);
+                u8_store<NP>(out, u, full, x0, p.out_w);
                 out += p.pitch;
             }
         }
@@ -439,10 +439,7 @@ __device__ __forceinline__ void u8_band_compute(const KernelParams& p, const uin
     const int64_t o0 = static_cast<int64_t>(frame) * p.out_frame_stride +
                        static_cast<int64_t>(oy0) * p.pitch + x0;
     uint32_t s_min = 0xffffffffu, s_max = 0u;
-    if (x0 + kLaneCols <= p.out_w)
-        u8_band_rows<NP, PAD, W, MODE, true>(p, srow, s_bar, par, x0, o0, n_out, s_min, s_max);
-    else
-        u8_band_rows<NP, PAD, W, MODE, false>(p, srow, s_bar, par, x0, o0, n_out, s_min, s_max);
+    u8_band_rows<NP, PAD, W, MODE>(p, srow, s_bar, par, x0, o0, n_out, s_min, s_max);
     if constexpr (MODE == 1) {  // the frame's min / max of g = sqrt(S), monotone in S
         s_min = __reduce_min_sync(0xffffffffu, s_min);
         s_max = __reduce_max_sync(0xffffffffu, s_max);
