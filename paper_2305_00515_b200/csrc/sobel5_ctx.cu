@@ -31,9 +31,10 @@
 
 namespace {
 
-// Host worker pool for the copies between pinned staging and pageable caller
-// memory (one host thread moves ~14 GB/s, four or more ~50 GB/s on the B200
-// host: profiles/r1/alloc_probe.txt).  The calling thread takes part.
+// Host worker pool for the copies between pinned staging and caller memory
+// and the int16 wire decode (one host thread moves ~14 GB/s; the decode's
+// streaming stores reach ~112 GB/s with 16: profiles/r1/alloc_probe.txt,
+// profiles/r2/wire_probe.txt).  The calling thread takes part.
 class HostPool {
 public:
     ~HostPool() {
@@ -76,8 +77,18 @@ private:
         std::condition_variable done;
     };
     void start() {
+        // threads incl. the caller: the host's cores shared by the node's
+        // local ranks (LOCAL_WORLD_SIZE, set by torchrun), or
+        // SOBEL5_HOST_THREADS.  The host path is bound by host memory
+        // traffic, which scales with threads: 8K e2e 11.4-13.3 ms at 8, 9.1
+        // at 16 on the 16-core B200 host (profiles/r2/host_threads.txt).
         const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
-        const int n = static_cast<int>(std::min(8u, hw) - 1);
+        const char* lw = std::getenv("LOCAL_WORLD_SIZE");
+        const unsigned ranks = lw && *lw && std::atoi(lw) > 0 ? static_cast<unsigned>(std::atoi(lw)) : 1u;
+        const char* v = std::getenv("SOBEL5_HOST_THREADS");
+        const unsigned want = v && *v && std::atoi(v) > 0 ? static_cast<unsigned>(std::atoi(v))
+                                                          : std::max(2u, hw / ranks);
+        const int n = static_cast<int>(std::max(1u, std::min(want, hw)) - 1);
         for (int i = 0; i < n; ++i) th_.emplace_back([this] { loop(); });
     }
     static void work(Batch& b) {
