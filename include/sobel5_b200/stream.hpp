@@ -682,6 +682,8 @@ inline StreamResult run_stream_bands(const GrayPlane& img, const StreamTaps& tap
     pl.gdt = out.gdt.data().data();
     pl.g = out.g.data().data();
     const sobel5_taps t = gpu::to_abi(taps);
+    // the plan orders the reported ParityViolation pair (strip-major)
+    sobel5_mgpu_set_strip_width(part.get(), plan.lane_width - 2 * plan.radius);
     const sobel5_status st =
         sobel5_mgpu_run_host(part.get(), img.data().data(), &t, prefetch == Prefetch::on ? 1 : 0, &pl);
     sobel5_diag d{};

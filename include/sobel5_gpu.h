@@ -478,8 +478,14 @@ sobel5_status sobel5_mgpu_sync(sobel5_mgpu* m);
  * packed host planes (pitch == width-4). */
 sobel5_status sobel5_mgpu_run_host(sobel5_mgpu* m, const uint8_t* h_in, const sobel5_taps* taps,
                                    int prefetch, const sobel5_planes* h_out);
-/* After run_host returned SOBEL5_PARITY_VIOLATION: the offending pair. */
+/* After run_host returned SOBEL5_PARITY_VIOLATION: the offending pair -- the
+ * first odd pixel of the whole image in strip, row, column order (strips of
+ * strip_w output columns, see sobel5_mgpu_set_strip_width; 0 = one strip),
+ * as the reference's run_stream with workers = 1 reports it. */
 sobel5_status sobel5_mgpu_last_diag(const sobel5_mgpu* m, sobel5_diag* out);
+/* The strip width (plan lane width - 4) ordering run_host's ParityViolation
+ * pair, like sobel5_ctx_set_strip_width. */
+sobel5_status sobel5_mgpu_set_strip_width(sobel5_mgpu* m, int strip_w);
 
 /* ---- stream-ordered flags (cross-process band ordering, bands.py) --------
  * host_register maps host memory (e.g. a shared-memory segment several

@@ -103,6 +103,7 @@ EXPORTS = (
     "sobel5_conv2d_valid", "sobel5_conv2d_valid_host", "sobel5_dense_4d", "sobel5_dense_4d_host",
     "sobel5_mgpu_create", "sobel5_mgpu_destroy", "sobel5_mgpu_band", "sobel5_mgpu_upload",
     "sobel5_mgpu_synth", "sobel5_mgpu_run_bands", "sobel5_mgpu_sync", "sobel5_mgpu_run_host", "sobel5_mgpu_last_diag",
+    "sobel5_mgpu_set_strip_width",
     "sobel5_host_register", "sobel5_host_unregister", "sobel5_stream_write_u32",
     "sobel5_stream_wait_u32",
 )
@@ -159,6 +160,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     L.sobel5_mgpu_run_host.restype = i32
     L.sobel5_mgpu_last_diag.argtypes = [vp, C.POINTER(Diag)]
     L.sobel5_mgpu_last_diag.restype = i32
+    L.sobel5_mgpu_set_strip_width.argtypes = [vp, i32]
+    L.sobel5_mgpu_set_strip_width.restype = i32
     L.sobel5_host_register.argtypes = [vp, C.c_size_t, C.POINTER(vp)]
     L.sobel5_host_register.restype = i32
     L.sobel5_host_unregister.argtypes = [vp]

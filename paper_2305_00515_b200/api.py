@@ -263,6 +263,27 @@ class Context:
         return st, res, d
 
 
+    def run_host_frames(self, frames: np.ndarray, taps: Taps, prefetch: Prefetch = Prefetch.on,
+                        planes=("gx", "gy", "gd", "gdt", "g"), out: dict | None = None):
+        """sobel5_run_host_frames: a stream of frames (n, h, w) uint8 end to
+        end, run_stream per frame, pipelined across frames.  Returns
+        (status, dict of (n, h - 4, w - 4) planes, Diag)."""
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        n, h, w = frames.shape
+        ow, oh = max(w - 4, 0), max(h - 4, 0)
+        dt = {"gx": np.int32, "gy": np.int32, "gd": np.int32, "gdt": np.int32, "g": np.float64,
+              "g32": np.float32, "u8": np.uint8}
+        res = out if out is not None else {
+            k: np.empty((n, oh, ow), dt[k]) for k in planes} if (ow > 0 and oh > 0) else {}
+        pl = Planes(pitch=ow)
+        for k, v in res.items():
+            setattr(pl, k, v.ctypes.data)
+        d = Diag()
+        st = self._lib.sobel5_run_host_frames(self._h, frames.ctypes.data, w, h, n, w * h,
+                                              C.byref(taps), int(prefetch), C.byref(pl), ow * oh,
+                                              C.byref(d))
+        return st, res, d
+
     def detect_host(self, img: np.ndarray, taps: Taps, prefetch: Prefetch = Prefetch.on,
                     pad: bool = True, save_mode: "SaveMode" = None, planes=()):
         """sobel5_detect_host: returns (status, u8 edge map, dict of planes, Diag)."""
@@ -802,6 +823,9 @@ def run_stream_bands(img: np.ndarray, taps_or_params, plan: StripPlan, prefetch:
         taps_or_params)
     mg = MultiGpuBands(devices, w, h, transport)
     try:
+        # the plan orders the reported ParityViolation pair (strip-major)
+        check(_abi.load().sobel5_mgpu_set_strip_width(mg._h, plan.lane_width - 2 * plan.radius),
+              "sobel5_mgpu_set_strip_width")
         res = mg.run_host(img, taps, prefetch)
     finally:
         mg.close()

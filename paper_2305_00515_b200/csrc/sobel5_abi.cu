@@ -402,6 +402,8 @@ sobel5_status launch_common(const uint8_t* top, const uint8_t* mid, const uint8_
     kp.u8_norm = ex.u8_norm;
     kp.s32 = ex.s32;
     kp.n16 = ex.n16;
+    kp.diag_frame0 = ex.frame0;
+    kp.diag_row0 = ex.row0;
     fill_taps(kp, *taps);
     kp.tstore = 0;
     if (kp.tma_load && sr_only && !ex.pad && !top && !bot && env_int("SOBEL5_TS", 0) != 0) {
@@ -700,3 +702,14 @@ sobel5_status sobel5_synth_random_device(uint8_t* d_img, int64_t pitch, int widt
 }
 
 }  // extern "C"
+namespace sobel5_b200 {
+sobel5_status launch_band_at(const uint8_t* d_top, const uint8_t* d_in, const uint8_t* d_bot,
+                             int64_t in_pitch, int width, int band_rows, const sobel5_taps* taps,
+                             int prefetch, const sobel5_planes* d_out, sobel5_diag* d_diag,
+                             void* stream, int row0) {
+    LaunchExtra ex;
+    ex.row0 = row0;
+    return launch_common(d_top, d_in, d_bot, in_pitch, 0, width, band_rows, 1, taps, prefetch,
+                         d_out, 0, d_diag, stream, ex);
+}
+}  // namespace sobel5_b200

@@ -496,6 +496,7 @@ sobel5_status enqueue_stream(sobel5_ctx* ctx, const uint8_t* h_in, int width, in
         const uint8_t* d_rows = ctx->d_in + static_cast<int64_t>(y0) * in_pitch;
         sobel5_b200::LaunchExtra ex;
         ex.n16 = wire ? 1 : 0;
+        ex.row0 = y0;  // the chunk's rows in the image: a global ParityViolation key
         const sobel5_status st =
             op == 3 ? sobel5_b200::sobel3_common(d_rows, in_pitch, 0, width, y1 - y0 + 2, 1, prefetch,
                                                  &sub, 0, ctx->s_comp, ex)
@@ -846,6 +847,8 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
         if (hp[6]) sub.u8 = reinterpret_cast<uint8_t*>(d_out + dev_off[6]);
         sobel5_b200::LaunchExtra ex;
         ex.n16 = wire ? 1 : 0;
+        ex.frame0 = f;  // the ParityViolation key: frame, then strip, row, column
+        ex.row0 = y0;
         const sobel5_status st = sobel5_b200::launch_common(nullptr, d_in, nullptr, in_pitch, 0, width,
                                                             rows + 4, 1, taps, prefetch, &sub, 0,
                                                             ctx->d_diag, ctx->s_comp, ex);

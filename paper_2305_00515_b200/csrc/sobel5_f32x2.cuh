@@ -235,7 +235,9 @@ __global__ void __launch_bounds__(kCtaThreads, SOBEL5_F32_MIN_CTAS)
                 const unsigned odd_mask = __ballot_sync(0xffffffffu, odd_any);
                 if (odd_mask && p.diag) {
                     if (lane == __ffs(odd_mask) - 1) atomicAdd(&p.diag->violations, 1);
-                    if (odd_any) odd_note(s_odd, p.diag, blockIdx.z, oy0 + r - 4, odd_x, odd_p, odd_m);
+                    if (odd_any)
+                        odd_note(s_odd, p.diag, blockIdx.z + p.diag_frame0, p.diag_row0 + oy0 + r - 4,
+                                 odd_x, odd_p, odd_m);
                 }
                 const int64_t row_off = out_off;
                 out_off += p.pitch;

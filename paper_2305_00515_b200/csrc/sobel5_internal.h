@@ -77,6 +77,8 @@ struct LaunchExtra {
     int u8_norm = 0;
     uint32_t* s32 = nullptr;                   // exact g^2 plane (normalize pass 1)
     int n16 = 0;                               // gx..gdt as int16 (host-path wire)
+    int frame0 = 0, row0 = 0;                  // the launch's place in the caller's
+                                               // image (ParityViolation order key)
 };
 
 // The int16 D2H wire of the host path (sobel5_ctx.cu) applies: default taps
@@ -88,6 +90,13 @@ bool n16_wire_ok(const sobel5_taps* taps);
 void widen_i16(int32_t* dst, const int16_t* src, size_t n);
 // g = sqrt(sum of the np int16 rows' squares), n pixels (the wire without g)
 void magnitude_i16(double* g, const int16_t* const* src, int np, size_t n);
+
+// sobel5_launch_band whose first output row is row0 of the caller's image
+// (the multi-GPU bands: a global ParityViolation order key)
+sobel5_status launch_band_at(const uint8_t* d_top, const uint8_t* d_in, const uint8_t* d_bot,
+                             int64_t in_pitch, int width, int band_rows, const sobel5_taps* taps,
+                             int prefetch, const sobel5_planes* d_out, sobel5_diag* d_diag,
+                             void* stream, int row0);
 
 // Common launch path (validation in the reference's order, geometry, kernel
 // selection) for plain, batched, band and detect launches.

@@ -86,6 +86,8 @@ struct sobel5_mgpu {
     int64_t in_pitch = 0;
     std::vector<Band> bands;
     sobel5_diag last_diag{};  // run_host's first parity violation
+    int strip_w = 0;          // orders that pair (sobel5_mgpu_set_strip_width)
+    sobel5_diag diag_init{};  // what each band's record starts from
 };
 
 namespace {
@@ -130,15 +132,16 @@ sobel5_status run_band(sobel5_mgpu* m, int k, const sobel5_taps* taps, int prefe
             top = u.d_in + static_cast<int64_t>(u.rows() - 2) * P;
         }
         if (has_bot) bot = m->bands[static_cast<size_t>(k + 1)].d_in;
-        return sobel5_launch_band(top, b.d_in, bot, P, m->width, b.rows(), taps, prefetch, &out,
-                                  diag, b.stream);
+        return sobel5_b200::launch_band_at(top, b.d_in, bot, P, m->width, b.rows(), taps, prefetch,
+                                           &out, diag, b.stream, b.c0 - 2);
     }
     // copy transport: interior first (no halo needed), halos, then the seams
     const int top_rows = has_top ? 2 : 0;
     if (b.rows() > 4) {
         const sobel5_planes o = offset_planes(out, top_rows);
-        if (sobel5_status st = sobel5_launch_band(nullptr, b.d_in, nullptr, P, m->width, b.rows(),
-                                                  taps, prefetch, &o, diag, b.stream);
+        if (sobel5_status st = sobel5_b200::launch_band_at(nullptr, b.d_in, nullptr, P, m->width,
+                                                           b.rows(), taps, prefetch, &o, diag,
+                                                           b.stream, b.c0 - 2 + top_rows);
             st != SOBEL5_OK)
             return st;
     }
@@ -155,16 +158,17 @@ sobel5_status run_band(sobel5_mgpu* m, int k, const sobel5_taps* taps, int prefe
                                 b.stream));
     }
     if (has_top) {  // centres r0, r0 + 1 from [halo; body rows 0..3]
-        if (sobel5_status st = sobel5_launch_band(h_top, b.d_in, nullptr, P, m->width, 4, taps,
-                                                  prefetch, &out, diag, b.stream);
+        if (sobel5_status st = sobel5_b200::launch_band_at(h_top, b.d_in, nullptr, P, m->width, 4,
+                                                           taps, prefetch, &out, diag, b.stream,
+                                                           b.c0 - 2);
             st != SOBEL5_OK)
             return st;
     }
     if (has_bot) {  // centres r1 - 2, r1 - 1 from [body rows r1-4..r1-1; halo]
         const sobel5_planes o = offset_planes(out, b.c1 - b.c0 - 2);
-        if (sobel5_status st = sobel5_launch_band(nullptr, b.d_in + static_cast<int64_t>(b.rows() - 4) * P,
-                                                  h_bot, P, m->width, 4, taps, prefetch, &o,
-                                                  diag, b.stream);
+        if (sobel5_status st = sobel5_b200::launch_band_at(
+                nullptr, b.d_in + static_cast<int64_t>(b.rows() - 4) * P, h_bot, P, m->width, 4,
+                taps, prefetch, &o, diag, b.stream, b.c1 - 4);
             st != SOBEL5_OK)
             return st;
     }
@@ -383,7 +387,10 @@ sobel5_status sobel5_mgpu_run_host(sobel5_mgpu* m, const uint8_t* h_in, const so
     for (Band& b : m->bands) {
         CKS(cudaSetDevice(b.device));
         if (!b.d_diag) CKS(cudaMalloc(reinterpret_cast<void**>(&b.d_diag), sizeof(sobel5_diag)));
-        CKS(cudaMemsetAsync(b.d_diag, 0, sizeof(sobel5_diag), b.stream));
+        m->diag_init = sobel5_diag{};
+        m->diag_init.strip_w = m->strip_w;
+        CKS(cudaMemcpyAsync(b.d_diag, &m->diag_init, sizeof(sobel5_diag), cudaMemcpyHostToDevice,
+                            b.stream));
     }
     if (sobel5_status st = sobel5_mgpu_upload(m, h_in); st != SOBEL5_OK) return st;
     if (sobel5_status st = run_bands_impl(m, taps, prefetch, dp.data(), true); st != SOBEL5_OK)
@@ -401,15 +408,30 @@ sobel5_status sobel5_mgpu_run_host(sobel5_mgpu* m, const uint8_t* h_in, const so
         }
     }
     if (sobel5_status st = sobel5_mgpu_sync(m); st != SOBEL5_OK) return st;
-    for (Band& b : m->bands) {  // recover_diag (pipeline.hpp:268-273), first band in row order
+    // recover_diag (pipeline.hpp:268-273): the bands' keys are global (strip,
+    // row, column), so the reported pair is the band record with the earliest
+    // key (stored inverted: the largest), the count the sum over bands
+    bool odd = false;
+    sobel5_diag first{};
+    int64_t total = 0;
+    for (Band& b : m->bands) {
         sobel5_diag d{};
         CKS(cudaSetDevice(b.device));
         CKS(cudaMemcpy(&d, b.d_diag, sizeof d, cudaMemcpyDeviceToHost));
-        if (d.violations) {
-            m->last_diag = d;
-            return SOBEL5_PARITY_VIOLATION;
-        }
+        if (!d.violations) continue;
+        total += d.violations;
+        if (!odd || d.order > first.order) first = d;
+        odd = true;
     }
+    if (!odd) return SOBEL5_OK;
+    first.violations = static_cast<int32_t>(std::min<int64_t>(total, INT32_MAX));
+    m->last_diag = first;
+    return SOBEL5_PARITY_VIOLATION;
+}
+
+sobel5_status sobel5_mgpu_set_strip_width(sobel5_mgpu* m, int strip_w) {
+    if (!m || strip_w < 0) return SOBEL5_INVALID_ARG;
+    m->strip_w = strip_w;
     return SOBEL5_OK;
 }
 

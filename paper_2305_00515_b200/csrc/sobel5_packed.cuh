@@ -698,7 +698,8 @@ __global__ void __launch_bounds__(kCtaThreads,
                     if (odd_mask && p.diag) {
                         if (lane == __ffs(odd_mask) - 1) atomicAdd(&p.diag->violations, 1);
                         if (odd_any)
-                            odd_note(s_odd, p.diag, blockIdx.z, oy0 + r - 4, x0 + odd_j, odd_p, odd_m);
+                            odd_note(s_odd, p.diag, blockIdx.z + p.diag_frame0, p.diag_row0 + oy0 + r - 4,
+                                     x0 + odd_j, odd_p, odd_m);
                     }
                 } else {
 #pragma unroll

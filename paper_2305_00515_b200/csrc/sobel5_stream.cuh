@@ -76,6 +76,11 @@ struct KernelParams {
     int64_t pitch;
     int64_t out_frame_stride;
     sobel5_diag* diag;
+    // the launch's first frame / output row in the caller's image (a row
+    // chunk, a frame of a stream, a band of a partition): the ParityViolation
+    // order key is global, not launch-local
+    int diag_frame0;
+    int diag_row0;
     int need_mag;
     // detect path: replicate padding, normalize export
     int pad;                     // 1: pad_replicate(img, 2) fused (same-size output)
@@ -538,7 +543,9 @@ __global__ void __launch_bounds__(kCtaThreads, SOBEL5_GENERIC_MIN_CTAS)
                 const unsigned odd_mask = __ballot_sync(0xffffffffu, odd_any);
                 if (odd_mask && p.diag) {
                     if (lane == __ffs(odd_mask) - 1) atomicAdd(&p.diag->violations, 1);
-                    if (odd_any) odd_note(s_odd, p.diag, blockIdx.z, oy0 + v, x0 + odd_j, odd_p, odd_m);
+                    if (odd_any)
+                        odd_note(s_odd, p.diag, blockIdx.z + p.diag_frame0, p.diag_row0 + oy0 + v,
+                                 x0 + odd_j, odd_p, odd_m);
                 }
 
                 const int64_t row_off = out_frame + static_cast<int64_t>(oy0 + v) * p.pitch + x0;

@@ -135,3 +135,40 @@ def test_frames_errors(ctx):
                                     C.byref(pl), 36, C.byref(d)) == _abi.INVALID_ARG
     assert L.sobel5_run_host_frames(ctx.handle, img.ctypes.data, 10, 10, 1, 100, C.byref(taps), 1,
                                     C.byref(pl), 36, C.byref(d)) == 0
+
+
+def test_frames_python_api(ctx, oracle):
+    """Context.run_host_frames (the Python face of the C call), u8 included."""
+    from paper_2305_00515_b200 import api
+    rng = np.random.default_rng(11)
+    frames = rng.integers(0, 256, (5, 70, 133), dtype=np.uint8)
+    st, res, d = ctx.run_host_frames(frames, api.make_stream_taps(), planes=SR + ("u8",))
+    assert st == 0 and d.violations == 0
+    for f in range(5):
+        _, ref, _ = oracle.run_stream(frames[f])
+        for k in SR:
+            np.testing.assert_array_equal(res[k][f], ref[k], err_msg=f"frame {f} {k}")
+        np.testing.assert_array_equal(res["u8"][f], oracle.clamp_abs(ref["g"]))
+
+
+def test_frames_parity_pair_is_the_first_frames(ctx, reference):
+    """A stream of frames stops at the first frame with an odd pair, as a loop
+    of run_stream calls would: frame 1's first pair is reported although
+    frame 2 has one at an earlier strip and row."""
+    from paper_2305_00515_b200 import _abi, api
+    rng = np.random.default_rng(4)
+    h, w, lanes = 120, 301, 64
+    frames = [np.zeros((h, w), np.uint8) for _ in range(3)]
+    frames[1][60:70, 130:160] = rng.integers(0, 256, (10, 30), dtype=np.uint8)  # strip 2, rows ~56..
+    frames[2][3:9, 5:50] = rng.integers(0, 256, (6, 45), dtype=np.uint8)         # strip 0, rows ~0..
+    code, t, msg = reference.make_stream_taps(1, 1, 1, 1)
+    t.k1[2] += 1
+    L = _abi.load()
+    assert L.sobel5_ctx_set_strip_width(ctx.handle, lanes - 4) == 0
+    try:
+        _, d, _ = run_frames(ctx, frames, SR, api.Taps.from_dict(t.as_dict()), pinned=False,
+                             status=_abi.PARITY_VIOLATION)
+    finally:
+        L.sobel5_ctx_set_strip_width(ctx.handle, 0)
+    code, _, _, want = reference.run_stream(frames[1], t, lanes=lanes, prefetch=True, workers=1)
+    assert code == 17 and want == f"odd sum/difference pair ({d.sum}, {d.diff})"

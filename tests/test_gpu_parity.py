@@ -373,3 +373,60 @@ def test_parity_violation_pair_matches_reference(reference, lanes, kind):
     with pytest.raises(api.ParityViolation) as ei:
         api.run_stream(img, taps, plan, api.Prefetch.on)
     assert str(ei.value) == want
+
+
+def _fault_taps(reference):
+    from paper_2305_00515_b200 import api
+    code, t, msg = reference.make_stream_taps(1, 1, 1, 1)
+    assert code == 0, msg
+    t.k1[2] += 1  # odd P + M wherever the centre pixels of rows v+1, v+3 differ in parity
+    return t, api.Taps.from_dict(t.as_dict())
+
+
+def _noisy(img, rng, rows, cols):
+    """Random pixels in input rows [r0, r1) x columns [c0, c1) of a flat image
+    (a flat region has no odd pairs under the fault)."""
+    (r0, r1), (c0, c1) = rows, cols
+    img[r0:r1, c0:c1] = rng.integers(0, 256, (r1 - r0, c1 - c0), dtype=np.uint8)
+
+
+@pytest.mark.parametrize("layout", ["same_strip", "later_strip"])
+def test_parity_pair_across_row_chunks(reference, layout):
+    """sobel5_run_host cuts a tall image into row chunks (>= 256 output rows
+    each, one launch per chunk); the order key of a pair is global, so the
+    reported pair is the reference's first in (strip, row, column) order even
+    when a later chunk holds odd pixels at smaller chunk-local rows."""
+    from paper_2305_00515_b200 import api
+    rng = np.random.default_rng(5)
+    h, w, lanes = 900, 301, 64  # strips of 60 output columns; chunks 0..255, 256..511, ...
+    img = np.zeros((h, w), np.uint8)
+    a_cols = (10, 40) if layout == "same_strip" else (130, 160)  # strip 0 or strip 2
+    _noisy(img, rng, (200, 216), a_cols)   # chunk 0, rows ~196..215
+    _noisy(img, rng, (300, 311), (5, 50))  # chunk 1 (local rows ~40..54), strip 0
+    t, taps = _fault_taps(reference)
+    code, _, _, want = reference.run_stream(img, t, lanes=lanes, prefetch=True, workers=1)
+    assert code == 17, want
+    with pytest.raises(api.ParityViolation) as ei:
+        api.run_stream(img, taps, api.plan_strips(w, lanes, 2), api.Prefetch.on)
+    assert str(ei.value) == want
+
+
+@pytest.mark.parametrize("transport", ["peer", "copy"])
+def test_parity_pair_across_bands(reference, transport):
+    """The multi-GPU row bands (device list {0, 0, 0}): band keys are global
+    rows and the merge keeps the earliest, so the pair is the reference's even
+    when a later band has an odd pixel at a smaller band-local row."""
+    from paper_2305_00515_b200 import api
+    rng = np.random.default_rng(9)
+    h, w, lanes = 300, 301, 64
+    img = np.zeros((h, w), np.uint8)
+    _noisy(img, rng, (20, 31), (130, 160))   # band 0, strip 2
+    _noisy(img, rng, (150, 161), (5, 50))    # band 1, strip 0, band-local rows ~46..
+    _noisy(img, rng, (205, 211), (5, 50))    # band 2, strip 0, band-local rows ~1..
+    t, taps = _fault_taps(reference)
+    code, _, _, want = reference.run_stream(img, t, lanes=lanes, prefetch=True, workers=1)
+    assert code == 17, want
+    with pytest.raises(api.ParityViolation) as ei:
+        api.run_stream_bands(img, taps, api.plan_strips(w, lanes, 2), api.Prefetch.on, [0, 0, 0],
+                             transport)
+    assert str(ei.value) == want
