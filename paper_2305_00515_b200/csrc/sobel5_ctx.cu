@@ -225,15 +225,13 @@ void decode_wire_rows(void* const dst[7], const int16_t* src, int np, int64_t pl
                       int64_t spitch, int out_w, int64_t r0, int64_t rows, bool with_g) {
     for (int64_t r = r0; r < r0 + rows; ++r) {
         const int16_t* row[4] = {};
+        int32_t* out[4] = {};
         for (int p = 0; p < np; ++p) {
             row[p] = src + (p * plane_rows + r) * spitch;
-            if (dst[p])
-                sobel5_b200::widen_i16(static_cast<int32_t*>(dst[p]) + r * out_w, row[p],
-                                       static_cast<size_t>(out_w));
+            if (dst[p]) out[p] = static_cast<int32_t*>(dst[p]) + r * out_w;
         }
-        if (with_g)
-            sobel5_b200::magnitude_i16(static_cast<double*>(dst[4]) + r * out_w, row, np,
-                                       static_cast<size_t>(out_w));
+        sobel5_b200::decode_row_i16(out, with_g ? static_cast<double*>(dst[4]) + r * out_w : nullptr,
+                                    row, np, static_cast<size_t>(out_w));
     }
 }
 

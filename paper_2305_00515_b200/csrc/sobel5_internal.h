@@ -90,6 +90,10 @@ bool n16_wire_ok(const sobel5_taps* taps);
 void widen_i16(int32_t* dst, const int16_t* src, size_t n);
 // g = sqrt(sum of the np int16 rows' squares), n pixels (the wire without g)
 void magnitude_i16(double* g, const int16_t* const* src, int np, size_t n);
+// One wire row decoded: the np int16 rows widened into dst[p] (nullptr =
+// skip) and, with g, the magnitude -- in one AVX-512 pass when every
+// destination can be 64-byte aligned at one column, else widen + magnitude.
+void decode_row_i16(int32_t* const* dst, double* g, const int16_t* const* src, int np, size_t n);
 
 // sobel5_launch_band whose first output row is row0 of the caller's image
 // (the multi-GPU bands: a global ParityViolation order key)

@@ -15,6 +15,7 @@
 namespace sobel5_b200 {
 void widen_i16(int32_t* dst, const int16_t* src, size_t n);
 void magnitude_i16(double* g, const int16_t* const* src, int np, size_t n);
+void decode_row_i16(int32_t* const* dst, double* g, const int16_t* const* src, int np, size_t n);
 }  // namespace sobel5_b200
 
 int main() {
@@ -64,6 +65,58 @@ int main() {
                 if (w[mis + n] != 7) {
                     std::printf("widen wrote outside its row\n");
                     return 1;
+                }
+                ++cases;
+            }
+        }
+    }
+    // decode_row_i16: one pass when every destination can be 64-byte aligned
+    // at one column (same offset mod 16 for the int32 planes, g matching),
+    // two passes otherwise; either way the reference's values
+    for (int np : {2, 4}) {
+        for (size_t n : {size_t{1}, size_t{63}, size_t{64}, size_t{100}, size_t{1000}, size_t{7676}}) {
+            for (int layout = 0; layout < 6; ++layout) {
+                // layout 0..2: aligned-compatible offsets; 3: int32 planes
+                // disagree; 4: g misaligned; 5: some planes skipped, no g
+                std::vector<int16_t> src[4];
+                const int16_t* rows[4] = {};
+                for (int p = 0; p < np; ++p) {
+                    src[p].resize(n);
+                    for (auto& v : src[p])
+                        v = (rng() & 7) == 0 ? extremes[rng() % 9] : static_cast<int16_t>(rng() & 0xffff);
+                    rows[p] = src[p].data();
+                }
+                const int off = layout < 3 ? layout * 4 : 3;
+                std::vector<std::vector<int32_t>> w32(np, std::vector<int32_t>(n + 64, 7));
+                std::vector<double> g(n + 64, -1.0);
+                int32_t* dst[4] = {};
+                auto aligned = [](void* p) {
+                    return reinterpret_cast<uintptr_t>(p) & ~uintptr_t{63};
+                };
+                for (int p = 0; p < np; ++p) {
+                    char* base = reinterpret_cast<char*>(aligned(w32[p].data() + 16));
+                    dst[p] = reinterpret_cast<int32_t*>(base) + off + (layout == 3 && p == 1 ? 1 : 0);
+                    if (layout == 5 && p == 1) dst[p] = nullptr;
+                }
+                double* gb = reinterpret_cast<double*>(aligned(g.data() + 8)) + off % 8;  // matches the int32 planes
+                if (layout == 4) gb += 1;
+                if (layout == 5) gb = nullptr;
+                sobel5_b200::decode_row_i16(dst, gb, rows, np, n);
+                for (size_t i = 0; i < n; ++i) {
+                    double acc = 0.0;
+                    for (int p = 0; p < np; ++p) {
+                        if (dst[p] && dst[p][i] != rows[p][i]) {
+                            std::printf("decode int mismatch np %d n %zu layout %d p %d i %zu\n", np, n,
+                                        layout, p, i);
+                            return 1;
+                        }
+                        acc = acc + static_cast<double>(rows[p][i]) * rows[p][i];
+                    }
+                    const double want = std::sqrt(acc);
+                    if (gb && std::memcmp(&want, &gb[i], 8) != 0) {
+                        std::printf("decode g mismatch np %d n %zu layout %d i %zu\n", np, n, layout, i);
+                        return 1;
+                    }
                 }
                 ++cases;
             }
