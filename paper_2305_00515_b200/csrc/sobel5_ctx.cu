@@ -713,6 +713,17 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
     unsigned mask = 0;
     for (int i = 0; i < 7; ++i)
         if (hp[i]) mask |= 1u << i;
+    // The StreamResult over the int16 wire with g rebuilt on the host runs
+    // as a one-frame stream: row chunks through a small ring of device and
+    // pinned staging slots, the decode of chunk k overlapping the downloads
+    // of the next ones (8K: 8.1-8.3 vs 8.9-9.1 ms for the whole-image
+    // staging, profiles/r2/frames_ring2.txt).  SOBEL5_RUN_HOST_RING=0 keeps
+    // the whole-image form.
+    if (want_wire(mask, taps, 5, false) && want_host_g() &&
+        !(std::getenv("SOBEL5_RUN_HOST_RING") && std::atoi(std::getenv("SOBEL5_RUN_HOST_RING")) == 0))
+        return sobel5_run_host_frames(ctx, h_in, width, height, 1, static_cast<int64_t>(width) * height,
+                                      taps, prefetch, h_out, static_cast<int64_t>(out_w) * out_h,
+                                      diag_out);
     void* direct[7] = {};  // pinned destinations: DMA straight into them
     void* staged[7] = {};  // pageable ones: through pinned staging (and the int16 wire planes)
     StageBudget budget;    // the planes first, then the input if it still fits
@@ -767,7 +778,7 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
     const char* sv = std::getenv("SOBEL5_FRAME_SLOTS");
     const int kFrameSlots = sv && *sv ? std::min(16, std::max(2, std::atoi(sv))) : 4;
     const char* cv = std::getenv("SOBEL5_FRAME_CHUNKS");
-    const int frame_chunks = cv && *cv && std::atoi(cv) > 0 ? std::atoi(cv) : 16;
+    const int frame_chunks = cv && *cv && std::atoi(cv) > 0 ? std::atoi(cv) : 32;
     void* hp[7];
     planes_array(h_out, hp);
     unsigned mask = 0;

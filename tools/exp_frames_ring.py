@@ -20,7 +20,7 @@ if len(sys.argv) > 1:
     for k, v in h_out.items():
         setattr(pl, k, v.data_ptr())
     d = _abi.Diag()
-    if sys.argv[1] == "run_host":
+    if sys.argv[1].startswith("run_host"):
         fn = lambda: L.sobel5_run_host(ctx.handle, h_in.data_ptr(), w, h, C.byref(taps), 1, C.byref(pl), C.byref(d))
     else:
         fn = lambda: L.sobel5_run_host_frames(ctx.handle, h_in.data_ptr(), w, h, 1, w * h, C.byref(taps), 1,
@@ -33,8 +33,10 @@ if len(sys.argv) > 1:
     print(f"{sys.argv[1]:28s} median {np.median(ts):6.2f} ms  min {np.min(ts):6.2f}", flush=True)
     sys.exit(0)
 for rep in range(2):
-    subprocess.run([sys.executable, __file__, "run_host"])
-    for chunks in (16, 32, 64, 128):
-        for slots in (2, 3, 4, 6, 8):
+    for c in (8, 16, 32):
+        subprocess.run([sys.executable, __file__, f"run_host chunks {c}"],
+                       env=dict(os.environ, SOBEL5_CHUNKS=str(c)))
+    for chunks in (8, 16, 32, 64):
+        for slots in (2, 4, 8):
             env = dict(os.environ, SOBEL5_FRAME_SLOTS=str(slots), SOBEL5_FRAME_CHUNKS=str(chunks))
             subprocess.run([sys.executable, __file__, f"frames chunks {chunks} slots {slots}"], env=env)
