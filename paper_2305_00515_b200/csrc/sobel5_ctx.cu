@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
@@ -57,6 +58,7 @@ public:
             std::lock_guard<std::mutex> g(m_);
             batch_ = b;
             ++gen_;
+            gen_seen_.store(gen_, std::memory_order_release);
         }
         cv_.notify_all();
         work(*b);
@@ -106,6 +108,13 @@ private:
     void loop() {
         uint64_t seen = 0;
         for (;;) {
+            // spin briefly before blocking: the host path hands out a batch
+            // per row chunk every ~0.2 ms, and a futex wake-up of the whole
+            // pool costs tens of microseconds per batch (SOBEL5_POOL_SPIN_US)
+            const auto t0 = std::chrono::steady_clock::now();
+            while (gen_seen_.load(std::memory_order_acquire) == seen &&
+                   std::chrono::steady_clock::now() - t0 < spin_)
+                spin_pause();
             std::shared_ptr<Batch> b;
             {
                 std::unique_lock<std::mutex> g(m_);
@@ -122,7 +131,17 @@ private:
     std::condition_variable cv_;
     std::shared_ptr<Batch> batch_;
     uint64_t gen_ = 0;
+    std::atomic<uint64_t> gen_seen_{0};
+    std::chrono::microseconds spin_{[] {
+        const char* v = std::getenv("SOBEL5_POOL_SPIN_US");
+        return v && *v ? std::atoi(v) : 300;
+    }()};
     bool stop_ = false;
+    static void spin_pause() {
+#if defined(__x86_64__) || defined(__i386__)
+        __builtin_ia32_pause();
+#endif
+    }
 };
 
 }  // namespace
@@ -752,10 +771,11 @@ sobel5_status sobel5_run_host(sobel5_ctx* ctx, const uint8_t* h_in, int width, i
 // Frames end to end (sobel5_run_host_frames): the units are row chunks of
 // the frames (one per frame up to ~4 M output px, else the row chunks of
 // sobel5_run_host), kept kFrameSlots in flight on the three streams through
-// rings of device input / output slots and pinned staging slots.  The host
-// enqueues unit u + kFrameSlots only after unit u's download has landed and
-// been widened / copied out, which is also what frees every slot it reuses,
-// so no device-side slot waits are needed.  With default taps and the five
+// rings of kFrameSlots + 1 device input / output slots and pinned staging
+// slots.  Once unit u's download has landed the host enqueues unit
+// u + kFrameSlots -- into the slot of unit u - 1, already widened / copied
+// out, so no device-side slot waits are needed -- and then decodes unit u
+// while the device works on the next ones.  With default taps and the five
 // StreamResult planes gx..gdt ride the int16 wire (chunk-major block per
 // unit); other pinned destinations are DMA'd straight into, pageable ones go
 // through the unit's staging slot.
@@ -777,6 +797,7 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
     // frame (SOBEL5_FRAME_CHUNKS): experiment knobs
     const char* sv = std::getenv("SOBEL5_FRAME_SLOTS");
     const int kFrameSlots = sv && *sv ? std::min(16, std::max(2, std::atoi(sv))) : 4;
+    const int n_slots = kFrameSlots + 1;
     const char* cv = std::getenv("SOBEL5_FRAME_CHUNKS");
     const int frame_chunks = cv && *cv && std::atoi(cv) > 0 ? std::atoi(cv) : 32;
     void* hp[7];
@@ -814,10 +835,10 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
     }
     dev_slot = round_up(static_cast<int64_t>(dev_slot), 256);
     host_slot = round_up(static_cast<int64_t>(std::max<size_t>(host_slot, 256)), 256);
-    CK(ensure(&ctx->f_d_in, &ctx->f_d_in_bytes, kFrameSlots * in_slot));
-    CK(ensure(&ctx->f_d_out, &ctx->f_d_out_bytes, kFrameSlots * dev_slot));
-    CK(ensure_host(&ctx->f_h_stage, &ctx->f_h_stage_bytes, kFrameSlots * host_slot));
-    CK(ensure_events(ctx->f_ev, 3 * kFrameSlots));
+    CK(ensure(&ctx->f_d_in, &ctx->f_d_in_bytes, n_slots * in_slot));
+    CK(ensure(&ctx->f_d_out, &ctx->f_d_out_bytes, n_slots * dev_slot));
+    CK(ensure_host(&ctx->f_h_stage, &ctx->f_h_stage_bytes, n_slots * host_slot));
+    CK(ensure_events(ctx->f_ev, 3 * n_slots));
     CK(reset_diag(ctx));
     const uint8_t* src_in = h_in;  // pageable input: the driver stages the (small) uploads
     ctx->last_d2h = 0;
@@ -830,7 +851,7 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
     auto enqueue_unit = [&](int64_t u) -> sobel5_status {
         int f, y0, y1;
         unit_rows(u, f, y0, y1);
-        const int slot = static_cast<int>(u % kFrameSlots), rows = y1 - y0;
+        const int slot = static_cast<int>(u % n_slots), rows = y1 - y0;
         cudaEvent_t ev_in = ctx->f_ev[3 * slot], ev_comp = ctx->f_ev[3 * slot + 1],
                     ev_out = ctx->f_ev[3 * slot + 2];
         uint8_t* d_in = static_cast<uint8_t*>(ctx->f_d_in) + slot * in_slot;
@@ -898,7 +919,7 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
     auto finish_unit = [&](int64_t u) {
         int f, y0, y1;
         unit_rows(u, f, y0, y1);
-        const int slot = static_cast<int>(u % kFrameSlots), rows = y1 - y0;
+        const int slot = static_cast<int>(u % n_slots), rows = y1 - y0;
         const char* h_st = static_cast<const char*>(ctx->f_h_stage) + slot * host_slot;
         const int per = std::max(1, (1 << 18) / std::max(out_w, 1));
         pieces.clear();
@@ -947,10 +968,10 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
     for (int64_t u = 0; u < std::min<int64_t>(kFrameSlots, n_units) && st == SOBEL5_OK; ++u)
         st = enqueue_unit(u);
     for (int64_t u = 0; u < n_units && st == SOBEL5_OK; ++u) {
-        const cudaError_t e = cudaEventSynchronize(ctx->f_ev[3 * (u % kFrameSlots) + 2]);
+        const cudaError_t e = cudaEventSynchronize(ctx->f_ev[3 * (u % n_slots) + 2]);
         if (e != cudaSuccess) return fail(ctx, e);
+        if (u + kFrameSlots < n_units) st = enqueue_unit(u + kFrameSlots);  // slot of unit u - 1
         finish_unit(u);
-        if (u + kFrameSlots < n_units) st = enqueue_unit(u + kFrameSlots);
     }
     CK(cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(sobel5_diag), cudaMemcpyDeviceToHost,
                        ctx->s_d2h));
