@@ -66,6 +66,11 @@ public:
         b->done.wait(g, [&] { return b->left == 0; });
     }
     int size() const { return static_cast<int>(th_.size()) + 1; }
+    // threads including the caller, starting the pool if needed
+    int threads() {
+        if (th_.empty()) start();
+        return size();
+    }
 
 private:
     // One run(): a worker that wakes late only sees next >= n and leaves
@@ -252,6 +257,21 @@ void decode_wire_rows(void* const dst[7], const int16_t* src, int np, int64_t pl
         sobel5_b200::decode_row_i16(out, with_g ? static_cast<double*>(dst[4]) + r * out_w : nullptr,
                                     row, np, static_cast<size_t>(out_w));
     }
+}
+
+// Rows per decode piece of a wire chunk: ~1 MiB of output per piece
+// (SOBEL5_DECODE_SPLIT=mib, default) or the rows split evenly over the pool
+// (=pool).
+int decode_rows_per_piece(sobel5_ctx* ctx, int rows, int out_w) {
+    static const bool even = [] {
+        const char* v = std::getenv("SOBEL5_DECODE_SPLIT");
+        return v && std::strcmp(v, "pool") == 0;
+    }();
+    if (even) {
+        const int nt = ctx->pool.threads();
+        return std::max(1, (rows + nt - 1) / nt);
+    }
+    return std::max(1, (1 << 20) / (std::max(out_w, 1) * 24));
 }
 
 bool want_wire(unsigned mask, const sobel5_taps* taps, int op, bool /*split*/) {
@@ -579,8 +599,7 @@ sobel5_status drain_stream(sobel5_ctx* ctx, int out_w, int out_h, int chunk, int
             // output per piece
             const int64_t dp = ctx->wire_pitch, rows = y1 - y0;
             const int np = ctx->wire_np;
-            const int per = std::max<int64_t>(
-                1, (int64_t{1} << 20) / (std::max(out_w, 1) * int64_t{4 * np + 8}));
+            const int per = decode_rows_per_piece(ctx, static_cast<int>(rows), out_w);
             const int n_pieces = static_cast<int>((rows + per - 1) / per);
             const int16_t* blk = static_cast<const int16_t*>(ctx->h_wire[0]) + np * static_cast<int64_t>(y0) * dp;
             void* dst[7] = {};
@@ -923,10 +942,12 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
         const char* h_st = static_cast<const char*>(ctx->f_h_stage) + slot * host_slot;
         const int per = std::max(1, (1 << 18) / std::max(out_w, 1));
         pieces.clear();
-        if (host_g) {  // gx..gdt widened and g rebuilt together, ~1 MiB of output per piece
-            const int per_g = std::max(1, (1 << 20) / (std::max(out_w, 1) * 24));
+        // gx..gdt widened and g rebuilt together: the unit's rows split evenly
+        // over the pool (one wave; 1 MiB pieces left up to 40% of the threads
+        // idle in the second wave of a 1/32 8K chunk)
+        const int per_g = decode_rows_per_piece(ctx, rows, out_w);
+        if (host_g)
             for (int r = 0; r < rows; r += per_g) pieces.push_back({-1, nullptr, nullptr, r});
-        }
         for (int i = 0; i < 7; ++i) {
             if (!hp[i] || (host_g && i <= 4)) continue;
             const bool w16 = wire && i < 4;
@@ -948,7 +969,6 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
                     dst[i] = static_cast<char*>(hp[i]) +
                              (static_cast<size_t>(f) * out_frame_stride + static_cast<size_t>(y0) * out_w) *
                                  kElem[i];
-                const int per_g = std::max(1, (1 << 20) / (std::max(out_w, 1) * 24));
                 decode_wire_rows(dst, reinterpret_cast<const int16_t*>(h_st), 4, rows, dpitch, out_w,
                                  q.rows, std::min(per_g, rows - q.rows), true);
             } else if (w16) {
@@ -967,12 +987,14 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
     sobel5_status st = SOBEL5_OK;
     for (int64_t u = 0; u < std::min<int64_t>(kFrameSlots, n_units) && st == SOBEL5_OK; ++u)
         st = enqueue_unit(u);
+    cudaError_t wait_err = cudaSuccess;
     for (int64_t u = 0; u < n_units && st == SOBEL5_OK; ++u) {
-        const cudaError_t e = cudaEventSynchronize(ctx->f_ev[3 * (u % n_slots) + 2]);
-        if (e != cudaSuccess) return fail(ctx, e);
+        wait_err = cudaEventSynchronize(ctx->f_ev[3 * (u % n_slots) + 2]);
+        if (wait_err != cudaSuccess) break;
         if (u + kFrameSlots < n_units) st = enqueue_unit(u + kFrameSlots);  // slot of unit u - 1
         finish_unit(u);
     }
+    if (wait_err != cudaSuccess) return fail(ctx, wait_err);
     CK(cudaMemcpyAsync(ctx->h_diag, ctx->d_diag, sizeof(sobel5_diag), cudaMemcpyDeviceToHost,
                        ctx->s_d2h));
     CK(cudaStreamSynchronize(ctx->s_d2h));

@@ -28,12 +28,12 @@ if len(sys.argv) > 1:
         t0 = time.perf_counter(); assert fn() == 0; ts.append((time.perf_counter() - t0) * 1e3)
     print(f"{sys.argv[1]:34s} median {np.median(ts):6.2f} ms  min {np.min(ts):6.2f}", flush=True)
     sys.exit(0)
-grid = [(16, 32, 4, sp) for sp in (0, 300)] + [(16, 32, 3, 300), (16, 32, 6, 300), (16, 64, 4, 300),
-                                              (16, 64, 8, 300), (16, 24, 4, 300), (16, 48, 6, 300)]
+grid = [(16, ch, 4, 300, sp) for ch in (32, 64) for sp in ("mib", "pool")]
 if os.environ.get("KNOB_GRID") == "threads":
-    grid = [(th, ch, sl, 0) for th, (ch, sl) in itertools.product((12, 14, 16), ((32, 4), (64, 4), (64, 6), (48, 4)))]
+    grid = [(th, ch, sl, 0, 1) for th, (ch, sl) in itertools.product((12, 14, 16), ((32, 4), (64, 4), (64, 6), (48, 4)))]
 for rep in range(2):
-    for th, ch, sl, sp in grid:
+    for th, ch, sl, sp, fd in grid:
         env = dict(os.environ, SOBEL5_HOST_THREADS=str(th), SOBEL5_FRAME_CHUNKS=str(ch),
-                   SOBEL5_FRAME_SLOTS=str(sl), SOBEL5_POOL_SPIN_US=str(sp))
-        subprocess.run([sys.executable, __file__, f"threads {th} chunks {ch} slots {sl} spin {sp}"], env=env)
+                   SOBEL5_FRAME_SLOTS=str(sl), SOBEL5_POOL_SPIN_US=str(sp), SOBEL5_DECODE_SPLIT=str(fd))
+        subprocess.run([sys.executable, __file__, f"threads {th} chunks {ch} slots {sl} spin {sp} split {fd}"],
+                       env=env)
