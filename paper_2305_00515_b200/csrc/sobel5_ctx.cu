@@ -830,9 +830,15 @@ sobel5_status sobel5_run_host_frames(sobel5_ctx* ctx, const uint8_t* h_in, int w
     ctx->wire = false;  // (the single-call wire state is not used here)
     const int64_t in_pitch = round_up(width, 128);
     const int64_t dpitch = round_up(out_w, 32);
+    // units: whole frames up to ~4 M output px, else frame_chunks row chunks,
+    // more when a unit's output would pass ~96 MB (the pinned staging of the
+    // ring stays bounded for any image: 32K x 32K takes 128-row units)
+    const int64_t row_out_bytes = static_cast<int64_t>(dpitch) * 24;
+    const int cap_rows = static_cast<int>(std::max<int64_t>(64, (int64_t{96} << 20) / row_out_bytes));
     const int chunk = out_px <= (int64_t{4} << 20)
                           ? out_h
-                          : std::min(out_h, std::max(64, (out_h + frame_chunks - 1) / frame_chunks));
+                          : std::min({out_h, cap_rows,
+                                      std::max(64, (out_h + frame_chunks - 1) / frame_chunks)});
     const int n_chunks = (out_h + chunk - 1) / chunk;
     const int64_t n_units = static_cast<int64_t>(n_frames) * n_chunks;
     // slot layouts (bytes): device [input rows][wire block | planes], host
