@@ -172,3 +172,26 @@ def test_frames_parity_pair_is_the_first_frames(ctx, reference):
         L.sobel5_ctx_set_strip_width(ctx.handle, 0)
     code, _, _, want = reference.run_stream(frames[1], t, lanes=lanes, prefetch=True, workers=1)
     assert code == 17 and want == f"odd sum/difference pair ({d.sum}, {d.diff})"
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_host_paths_random_shapes(ctx, oracle, seed):
+    """Random frame shapes / counts / strides / pinnedness through the frames
+    engine and sobel5_run_host (both on the wire with g rebuilt on the host):
+    every plane equals the oracle's."""
+    from paper_2305_00515_b200 import api
+    rng = np.random.default_rng(100 + seed)
+    h = int(rng.integers(5, 1400))
+    w = int(rng.integers(5, 1400))
+    n = int(rng.integers(1, 4))
+    frames = [rng.integers(0, 256, (h, w), dtype=np.uint8) for _ in range(n)]
+    out, d, _ = run_frames(ctx, frames, SR, api.make_stream_taps(), pinned=bool(seed % 2),
+                           in_pad=int(rng.integers(0, 9)), out_pad=int(rng.integers(0, 9)))
+    for f, img in enumerate(frames):
+        _, ref, _ = oracle.run_stream(img)
+        for k in SR:
+            np.testing.assert_array_equal(out[k][f], ref[k], err_msg=f"frames {h}x{w} frame {f} {k}")
+        st, res, _ = ctx.run_host(img, api.make_stream_taps())
+        assert st == 0
+        for k in SR:
+            np.testing.assert_array_equal(res[k], ref[k], err_msg=f"run_host {h}x{w} {k}")
