@@ -121,7 +121,7 @@ typedef struct sobel5_norm_table {
     float lo_f;         /* (float) lo */
     float scale_f;      /* (float) (255 / span), 0 if span <= 0 */
     uint32_t exact_s;   /* 1: thresholds valid (integer S), 0: use lo/span directly */
-    uint32_t pad_;
+    uint32_t one_step;  /* 1: the float index estimate is within 1/4 step (one-compare map) */
     uint32_t thr[257];  /* thr[0] = 0, thr[256] = UINT32_MAX */
     uint32_t pad2_[3];
 } sobel5_norm_table;

@@ -47,7 +47,11 @@ uint32_t* scratch_s32(void* s, int frames) {
     return reinterpret_cast<uint32_t*>(static_cast<char*>(s) + head_bytes(frames));
 }
 
+// The detect path's small kernels start with pdl_enter() and are launched
+// with launch_pdl: each one's launch overlaps its predecessor's tail (pass 1
+// -> table -> map), and each waits for that predecessor before any access.
 __global__ void minmax_init_kernel(sobel5_minmax* mm, int frames) {
+    pdl_enter();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < frames) {
         mm[i].lo_key = ~0ull;
@@ -58,7 +62,9 @@ __global__ void minmax_init_kernel(sobel5_minmax* mm, int frames) {
 // One block per frame.  lo / hi from the keys; for integer sums of squares
 // (exact_s) thread k in 1..255 binary-searches the smallest S in
 // [S_lo, S_hi] whose normalized value is >= k (the map is monotone).
-__global__ void norm_table_kernel(const sobel5_minmax* mm, sobel5_norm_table* tab, int exact_s) {
+__global__ void norm_table_kernel(const sobel5_minmax* mm, sobel5_norm_table* tab, int exact_s,
+                                  int allow_one_step) {
+    pdl_enter();
     const sobel5_minmax m = mm[blockIdx.x];
     sobel5_norm_table* t = tab + blockIdx.x;
     const bool any = m.lo_key <= m.hi_key;
@@ -72,6 +78,10 @@ __global__ void norm_table_kernel(const sobel5_minmax* mm, sobel5_norm_table* ta
         t->lo_f = static_cast<float>(lo);
         t->scale_f = span > 0.0 ? static_cast<float>(255.0 / span) : 0.0f;
         t->exact_s = static_cast<uint32_t>(exact_s);
+        // the map's float estimate y * scale - lo * scale of m = (g - lo) *
+        // 255 / span errs by a few ulps of max(hi * scale, lo * scale), so
+        // it is within 1/4 of m whenever hi * 255 / span <= 2^16 (lo <= hi)
+        t->one_step = (allow_one_step && exact_s && any && span > 0.0 && hi * (255.0 / span) <= 65536.0) ? 1u : 0u;
         t->thr[0] = 0u;
         t->thr[256] = 0xffffffffu;
     }
@@ -122,9 +132,57 @@ __device__ __forceinline__ uint32_t est_index(float m) {
     return min(__float_as_uint(m) - 0x4B400000u, 255u);
 }
 
+// One-compare form (table one_step): with the estimate m' within 1/4 of m,
+// j = round(m' + 1/2) lies in [0, 256] and leaves u(S) in {j - 1, j}, and
+// u(S) >= j <=> S >= thr[j] (thr[j] is the smallest S with u >= j; thr[0] = 0
+// and thr[256] = UINT32_MAX close both ends), so u = j - 1 + [S >= thr[j]]:
+// I2F, MUFU.SQRT, FFMA, FADD, one 4-byte shared load and one compare per
+// pixel, no clamp, no search (the unsigned min only keeps a broken estimate
+// inside the table).
+__device__ __forceinline__ uint32_t norm_one_step(uint32_t S, float scale, float off, const uint32_t* thr) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__uint2float_rn(S)));
+    const float m = __fadd_rn(__fmaf_rn(y, scale, off), 12582912.0f);  // off carries the + 1/2
+    const uint32_t j = min(__float_as_uint(m) - 0x4B400000u, 256u);
+    return j - (S < thr[j] ? 1u : 0u);
+}
+
+// One thread's 4-column slice in the one-compare form, rows y, y + step, ...
+// (top to bottom: reading the S plane bottom-up to catch pass 1's last rows
+// in L2 measured slower, 90.8 vs 88.2 us for the 8K detect).  FULL: all 4
+// columns inside the plane (one 4-byte store per row).
+template <bool FULL>
+__device__ __forceinline__ void norm_one_step_rows(const uint32_t* __restrict__ s, uint8_t* __restrict__ o,
+                                                   int64_t pitch, int y, int out_h, int step, int ncols,
+                                                   float sc, float off, const uint32_t* thr) {
+    constexpr int kRows = 4;
+    for (; y < out_h; y += step) {
+        uint4 S[kRows];
+#pragma unroll
+        for (int k = 0; k < kRows; ++k)
+            if (y + k < out_h) S[k] = __ldcs(reinterpret_cast<const uint4*>(s + static_cast<int64_t>(y + k) * pitch));
+#pragma unroll
+        for (int k = 0; k < kRows; ++k) {
+            if (y + k >= out_h) break;
+            const uint32_t u0 = norm_one_step(S[k].x, sc, off, thr);
+            const uint32_t u1 = norm_one_step(S[k].y, sc, off, thr);
+            const uint32_t u2 = norm_one_step(S[k].z, sc, off, thr);
+            const uint32_t u3 = norm_one_step(S[k].w, sc, off, thr);
+            uint8_t* q = o + static_cast<int64_t>(y + k) * pitch;
+            if (FULL) {
+                st_cs_u32(q, pack_u8x4(u0, u1, u2, u3));
+            } else {
+                const uint32_t u[4] = {u0, u1, u2, u3};
+                for (int j = 0; j < ncols; ++j) q[j] = static_cast<uint8_t>(u[j]);
+            }
+        }
+    }
+}
+
 __global__ void norm_map_kernel(const uint32_t* __restrict__ s32, int64_t pitch,
                                 int64_t frame_stride, int out_w, int out_h,
                                 const sobel5_norm_table* __restrict__ tab, uint8_t* __restrict__ u8) {
+    pdl_enter();
     __shared__ uint32_t s_thr[257];
     __shared__ uint2 s_pair[256];
     const sobel5_norm_table* t = tab + blockIdx.z;
@@ -142,6 +200,16 @@ __global__ void norm_map_kernel(const uint32_t* __restrict__ s32, int64_t pitch,
     // kRows rows per iteration: their loads are in flight together (one
     // 16-B load per thread per row would leave HBM latency exposed)
     constexpr int kRows = 4;
+    if (t->one_step) {  // uniform per frame
+        const float sc = t->scale_f;
+        const float off = __fadd_rn(-t->lo_f * sc, 0.5f);
+        const int y0 = blockIdx.y * kRows, step = gridDim.y * kRows;
+        if (x + 3 < out_w)
+            norm_one_step_rows<true>(s32 + base, u8 + base, pitch, y0, out_h, step, 4, sc, off, s_thr);
+        else
+            norm_one_step_rows<false>(s32 + base, u8 + base, pitch, y0, out_h, step, out_w - x, sc, off, s_thr);
+        return;
+    }
     for (int y0 = blockIdx.y * kRows; y0 < out_h; y0 += gridDim.y * kRows) {
         uint4 S[kRows];
 #pragma unroll
@@ -254,10 +322,17 @@ __global__ void plane_map_kernel(const T* plane, int64_t pitch, int width, int h
     }
 }
 
+// SOBEL5_NORM_ONE_STEP=0 keeps every frame on the estimate-check-search map
+// (tests compare both forms)
+int norm_one_step_allowed() {
+    const char* v = std::getenv("SOBEL5_NORM_ONE_STEP");
+    return (v && std::atoi(v) == 0) ? 0 : 1;
+}
+
 sobel5_status run_init(sobel5_minmax* mm, int frames, cudaStream_t s) {
-    minmax_init_kernel<<<(frames + 127) / 128, 128, 0, s>>>(mm, frames);
+    const cudaError_t e = launch_pdl(minmax_init_kernel, dim3((frames + 127) / 128), dim3(128), s, mm, frames);
     count_launch();
-    return map_cuda(cudaGetLastError());
+    return map_cuda(e);
 }
 
 // normalize export (image_io.hpp:242-255) around a stencil launcher:
@@ -287,9 +362,11 @@ sobel5_status detect_normalize(void* scratch, int frames, bool exact, const sobe
     e1.minmax = mm;
     if (exact) e1.s32 = scratch_s32(scratch, frames);
     if (sobel5_status st = launch(&p1, e1, d_diag); st != SOBEL5_OK) return st;
-    norm_table_kernel<<<frames, 256, 0, s>>>(mm, tab, exact ? 1 : 0);
+    if (cudaError_t e = launch_pdl(norm_table_kernel, dim3(frames), dim3(256), s, mm, tab, exact ? 1 : 0,
+                                   norm_one_step_allowed());
+        e != cudaSuccess)
+        return map_cuda(e);
     count_launch();
-    if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return map_cuda(e);
     if (exact) {
         // a few thousand CTAs that loop over rows: every CTA first stages the
         // 257-entry threshold table in shared memory, so one CTA per row
@@ -298,10 +375,10 @@ sobel5_status detect_normalize(void* scratch, int frames, bool exact, const sobe
         const unsigned gy = static_cast<unsigned>(std::max(
             1, std::min((out_h + 3) / 4, static_cast<int>(148u * 16u / (gx * frames)) + 1)));
         const dim3 grid(gx, gy, static_cast<unsigned>(frames));
-        norm_map_kernel<<<grid, 128, 0, s>>>(e1.s32, d_out->pitch, out_frame_stride, out_w, out_h,
-                                             tab, d_out->u8);
+        const cudaError_t e = launch_pdl(norm_map_kernel, grid, dim3(128), s, e1.s32, d_out->pitch,
+                                         out_frame_stride, out_w, out_h, tab, d_out->u8);
         count_launch();
-        return map_cuda(cudaGetLastError());
+        return map_cuda(e);
     }
     LaunchExtra e2 = ex;
     e2.norm = tab;
@@ -401,7 +478,7 @@ sobel5_status sobel5_quantize_plane(const void* d_plane, int kind, int64_t pitch
         else
             plane_minmax_kernel<<<blocks, 256, 0, s>>>(static_cast<const uint8_t*>(d_plane), pitch,
                                                        width, height, mm);
-        norm_table_kernel<<<1, 256, 0, s>>>(mm, tab, 0);
+        norm_table_kernel<<<1, 256, 0, s>>>(mm, tab, 0, 0);
         count_launch(2);
         if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return map_cuda(e);
     }

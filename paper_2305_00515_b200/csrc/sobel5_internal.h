@@ -5,6 +5,8 @@
 
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #include <cstdint>
 
 #include "sobel5_gpu.h"
@@ -32,6 +34,21 @@ cudaError_t launch_kp(Kernel k, dim3 grid, int threads, size_t smem, cudaStream_
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, k, kp);
+}
+
+// The same for any kernel signature (the detect path's small kernels).
+template <typename... P, typename... A>
+cudaError_t launch_pdl(void (*k)(P...), dim3 grid, dim3 block, cudaStream_t s, A&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
 }
 
 // Packed default-taps kernel (sobel5_packed.cuh), one launcher per geometry.

@@ -138,6 +138,48 @@ def test_detect_normalize_edge_cases(api, oracle, kind):
     np.testing.assert_array_equal(got["u8"], oracle.quantize(ref["g"], "normalize"))
 
 
+@pytest.mark.parametrize("one_step", ["1", "0"])
+@pytest.mark.parametrize("kind", ["random", "low", "narrow_span", "texture_ramp"])
+def test_normalize_map_forms(api, oracle, monkeypatch, kind, one_step):
+    """The S-plane map in both forms -- one compare against thr[j] when the
+    float estimate is within 1/4 step (hi * 255 / span <= 2^16), estimate +
+    check + search otherwise (SOBEL5_NORM_ONE_STEP=0 forces it) -- on
+    images whose g spans are wide, small and narrow (lo close to hi: the
+    one-compare form is refused and the search decides)."""
+    monkeypatch.setenv("SOBEL5_NORM_ONE_STEP", one_step)
+    h, w = 203, 1031
+    rng = np.random.default_rng(7)
+    if kind == "random":
+        img = rand_img(h, w, 5)
+    elif kind == "low":
+        img = rand_img(h, w, 6, 0x03)
+    elif kind == "narrow_span":
+        # a 0/255 checkerboard plus one-level noise: every g is large and
+        # close to every other one (span << hi)
+        yy, xx = np.mgrid[0:h, 0:w]
+        img = np.where((yy + xx) % 2 == 0, 255, 0).astype(np.int32)
+        img = np.clip(img + rng.integers(-1, 2, (h, w)), 0, 255).astype(np.uint8)
+    else:
+        img = ((np.arange(w)[None, :] * 3 + np.arange(h)[:, None] * 5) % 256).astype(np.uint8)
+        img ^= rng.integers(0, 4, (h, w), dtype=np.uint8)
+    for pad in (True, False):
+        got = _detect(api, img, pad, api.SaveMode.normalize, planes=("g",))
+        ref = padded_ref(oracle, img) if pad else oracle.run_stream(img)[1]
+        np.testing.assert_array_equal(got["g"], ref["g"])
+        np.testing.assert_array_equal(got["u8"], oracle.quantize(ref["g"], "normalize"),
+                                      err_msg=f"{kind} pad={pad}")
+
+
+def test_normalize_map_1080p(api, oracle):
+    """A full 1080p frame through the one-compare map (2 M pixels against
+    the oracle's quantize of the oracle's g)."""
+    img = rand_img(1080, 1920, 42)
+    got = _detect(api, img, True, api.SaveMode.normalize, planes=("g",))
+    ref = padded_ref(oracle, img)
+    np.testing.assert_array_equal(got["g"], ref["g"])
+    np.testing.assert_array_equal(got["u8"], oracle.quantize(ref["g"], "normalize"))
+
+
 def test_detect_normalize_generic_taps(api, oracle):
     """Non-default taps: the generic kernel maps g with the direct formula."""
     sys_taps = oracle.make_stream_taps(2, 3, 5, 7)
