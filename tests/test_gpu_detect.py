@@ -139,7 +139,7 @@ def test_detect_normalize_edge_cases(api, oracle, kind):
 
 
 @pytest.mark.parametrize("one_step", ["1", "0"])
-@pytest.mark.parametrize("kind", ["random", "low", "narrow_span", "texture_ramp"])
+@pytest.mark.parametrize("kind", ["random", "low", "checker", "narrow_span", "texture_ramp"])
 def test_normalize_map_forms(api, oracle, monkeypatch, kind, one_step):
     """The S-plane map in both forms -- one compare against thr[j] when the
     float estimate is within 1/4 step (hi * 255 / span <= 2^16), estimate +
@@ -153,12 +153,17 @@ def test_normalize_map_forms(api, oracle, monkeypatch, kind, one_step):
         img = rand_img(h, w, 5)
     elif kind == "low":
         img = rand_img(h, w, 6, 0x03)
-    elif kind == "narrow_span":
-        # a 0/255 checkerboard plus one-level noise: every g is large and
-        # close to every other one (span << hi)
+    elif kind == "checker":
         yy, xx = np.mgrid[0:h, 0:w]
         img = np.where((yy + xx) % 2 == 0, 255, 0).astype(np.int32)
         img = np.clip(img + rng.integers(-1, 2, (h, w)), 0, 255).astype(np.uint8)
+    elif kind == "narrow_span":
+        # a steep vertical ramp (every valid-mode g = 1488.96) with one
+        # corner pixel raised: g spans [1488.96, 1492.72], hi * 255 / span =
+        # 1.0e5 > 2^16, so the table refuses the one-compare form (valid
+        # mode; replicate padding widens the span again)
+        img = (8 * np.mgrid[0:30, 0:w][0]).astype(np.uint8)
+        img[0, 0] += 1
     else:
         img = ((np.arange(w)[None, :] * 3 + np.arange(h)[:, None] * 5) % 256).astype(np.uint8)
         img ^= rng.integers(0, 4, (h, w), dtype=np.uint8)
