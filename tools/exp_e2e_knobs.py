@@ -29,6 +29,8 @@ if len(sys.argv) > 1:
     print(f"{sys.argv[1]:34s} median {np.median(ts):6.2f} ms  min {np.min(ts):6.2f}", flush=True)
     sys.exit(0)
 grid = [(16, ch, 4, 300, sp) for ch in (32, 64) for sp in ("mib", "pool")]
+if os.environ.get("KNOB_GRID") == "chunks":  # DDIO-sized staging on host-memory-bound boxes
+    grid = [(16, ch, sl, 300, 0) for ch, sl in ((32, 4), (48, 4), (64, 4), (96, 6), (128, 8), (24, 3))]
 if os.environ.get("KNOB_GRID") == "threads":
     grid = [(th, ch, sl, 0, 1) for th, (ch, sl) in itertools.product((12, 14, 16), ((32, 4), (64, 4), (64, 6), (48, 4)))]
 for rep in range(2):
