@@ -186,9 +186,11 @@ __global__ void norm_map_kernel(const uint32_t* __restrict__ s32, int64_t pitch,
     __shared__ uint32_t s_thr[257];
     __shared__ uint2 s_pair[256];
     const sobel5_norm_table* t = tab + blockIdx.z;
+    const bool one_step = t->one_step != 0;  // uniform per frame
     for (int i = threadIdx.x; i < 257; i += blockDim.x) s_thr[i] = t->thr[i];
     __syncthreads();
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_pair[i] = make_uint2(s_thr[i], s_thr[i + 1]);
+    if (!one_step)  // the search form's (thr[k], thr[k+1]) pairs
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) s_pair[i] = make_uint2(s_thr[i], s_thr[i + 1]);
     const float2 scale2 = make_float2(t->scale_f, t->scale_f);
     const float nlo = -t->lo_f * t->scale_f;
     const float2 off2 = make_float2(nlo, nlo);
@@ -200,7 +202,7 @@ __global__ void norm_map_kernel(const uint32_t* __restrict__ s32, int64_t pitch,
     // kRows rows per iteration: their loads are in flight together (one
     // 16-B load per thread per row would leave HBM latency exposed)
     constexpr int kRows = 4;
-    if (t->one_step) {  // uniform per frame
+    if (one_step) {
         const float sc = t->scale_f;
         const float off = __fadd_rn(-t->lo_f * sc, 0.5f);
         const int y0 = blockIdx.y * kRows, step = gridDim.y * kRows;
